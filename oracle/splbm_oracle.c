@@ -1,0 +1,509 @@
+/*
+ * TEST INFRASTRUCTURE ONLY — the CPU oracle for the T2C hot path.
+ *
+ * A plain-C restatement of the reference solver's T2C time step (arXiv 1703.08015,
+ * reference `splbm`, /root/reference/proj). Every function cites the reference
+ * file:line it follows. It is pinned (tests/test_oracle.py) against
+ *   - the reference itself compiled in place (oracle/_ref, oracle/build_ref.sh), and
+ *   - the golden digests recorded in SURVEY.md Appendix B / tests/golden/.
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference legs may
+ * load this library; the product (paper_1703_08015_b200/) never does.
+ *
+ * Arithmetic is written out literally in the reference's operation order (including the
+ * products by zero direction components) and compiled with -ffp-contract=off, so it is
+ * bit-identical to the reference built with its CMake Release flags.
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define EMPTY_TILE 0xffffffffu /* kEmptyTile, tiling.hpp:16 */
+
+/* ---- lattice constants: lattice.cpp:18-25 (D2Q9), 33-42 (D3Q19) ---------------------- */
+static const int E2[9][3] = {{0, 0, 0},  {1, 0, 0},   {-1, 0, 0}, {0, 1, 0},  {0, -1, 0},
+                             {1, 1, 0},  {-1, -1, 0}, {1, -1, 0}, {-1, 1, 0}};
+static const int E3[19][3] = {{0, 0, 0},  {1, 0, 0},   {-1, 0, 0}, {0, 1, 0},  {0, -1, 0},
+                              {0, 0, 1},  {0, 0, -1},  {1, 1, 0},  {-1, -1, 0}, {1, -1, 0},
+                              {-1, 1, 0}, {1, 0, 1},   {-1, 0, -1}, {1, 0, -1}, {-1, 0, 1},
+                              {0, 1, 1},  {0, -1, -1}, {0, 1, -1}, {0, -1, 1}};
+
+typedef struct {
+  int d, q;
+  const int (*e)[3];
+  double w[19];
+  int opp[19];
+} lattice_t;
+
+static void lattice_init(lattice_t* L, int d) {
+  L->d = d;
+  if (d == 2) {
+    L->q = 9;
+    L->e = E2;
+    L->w[0] = 4.0 / 9.0;
+    for (int i = 1; i <= 4; ++i) L->w[i] = 1.0 / 9.0;
+    for (int i = 5; i <= 8; ++i) L->w[i] = 1.0 / 36.0;
+  } else {
+    L->q = 19;
+    L->e = E3;
+    for (int i = 0; i < 19; ++i) L->w[i] = 1.0 / 36.0;
+    L->w[0] = 1.0 / 3.0;
+    for (int i = 1; i <= 6; ++i) L->w[i] = 1.0 / 18.0;
+  }
+  /* opposite by search, lattice.cpp:65-74 */
+  for (int i = 0; i < L->q; ++i)
+    for (int j = 0; j < L->q; ++j)
+      if (L->e[j][0] == -L->e[i][0] && L->e[j][1] == -L->e[i][1] && L->e[j][2] == -L->e[i][2]) {
+        L->opp[i] = j;
+        break;
+      }
+}
+
+/* ---- tile cover: tiling.cpp:95-141 ------------------------------------------------------ */
+void oracle_tile_dims(int d, const int* dims, int a, int* grid_dims, int* padded_dims) {
+  for (int k = 0; k < 3; ++k) {
+    const int extent = (k == 2 && d == 2) ? 1 : dims[k];
+    const int te = (k == 2 && d == 2) ? 1 : a;
+    grid_dims[k] = (extent + te - 1) / te;
+    padded_dims[k] = grid_dims[k] * te;
+  }
+}
+
+/* Returns the number of non-empty tiles; outputs sized for the worst case (all cells).
+ * Validation as tiling.cpp:87-93 (returns -1 on a ConfigError condition). */
+int64_t oracle_build_tiles(const uint8_t* types, int d, const int* dims, int a, int periodic,
+                           uint32_t* tile_map, int32_t* origins, uint8_t* ttypes,
+                           uint32_t* fluid_count) {
+  if (a < 2) return -1;
+  for (int k = 0; k < d; ++k)
+    if (((periodic >> k) & 1) && dims[k] % a != 0) return -1;
+  int gd[3], pd[3];
+  oracle_tile_dims(d, dims, a, gd, pd);
+  const int az = d == 3 ? a : 1;
+  const int64_t n_tn = (int64_t)a * a * az;
+  int64_t T = 0;
+  for (int cz = 0; cz < gd[2]; ++cz)
+    for (int cy = 0; cy < gd[1]; ++cy)
+      for (int cx = 0; cx < gd[0]; ++cx) {
+        uint8_t* tt = ttypes + T * n_tn;
+        memset(tt, 0, (size_t)n_tn); /* padding is Solid */
+        uint32_t fc = 0;
+        for (int lz = 0; lz < az; ++lz) {
+          const int z = cz * az + lz;
+          if (z >= dims[2]) continue;
+          for (int ly = 0; ly < a; ++ly) {
+            const int y = cy * a + ly;
+            if (y >= dims[1]) continue;
+            for (int lx = 0; lx < a; ++lx) {
+              const int x = cx * a + lx;
+              if (x >= dims[0]) continue;
+              const uint8_t t = types[(size_t)x + (size_t)dims[0] * ((size_t)y + (size_t)dims[1] * z)];
+              tt[lx + a * (ly + a * lz)] = t;
+              if (t != 0) ++fc;
+            }
+          }
+        }
+        const size_t cell = (size_t)cx + (size_t)gd[0] * ((size_t)cy + (size_t)gd[1] * cz);
+        if (fc > 0) {
+          tile_map[cell] = (uint32_t)T;
+          origins[3 * T + 0] = cx * a;
+          origins[3 * T + 1] = cy * a;
+          origins[3 * T + 2] = cz * az;
+          fluid_count[T] = fc;
+          ++T;
+        } else {
+          tile_map[cell] = EMPTY_TILE;
+        }
+      }
+  return T;
+}
+
+/* tile_at with per-axis wrap: tiling.hpp:93-102 */
+static uint32_t tile_at(const int* gd, int periodic, const uint32_t* tile_map, int cx, int cy,
+                        int cz) {
+  int c[3] = {cx, cy, cz};
+  for (int k = 0; k < 3; ++k) {
+    if (c[k] < 0 || c[k] >= gd[k]) {
+      if (!((periodic >> k) & 1)) return EMPTY_TILE;
+      c[k] = ((c[k] % gd[k]) + gd[k]) % gd[k];
+    }
+  }
+  return tile_map[(size_t)c[0] + (size_t)gd[0] * ((size_t)c[1] + (size_t)gd[1] * c[2])];
+}
+
+/* 27-neighbour tile table: engine.hpp:446-463 */
+void oracle_nb_table(const int* gd, int periodic, const uint32_t* tile_map, uint32_t* nb) {
+  for (int cz = 0; cz < gd[2]; ++cz)
+    for (int cy = 0; cy < gd[1]; ++cy)
+      for (int cx = 0; cx < gd[0]; ++cx) {
+        const uint32_t t = tile_map[(size_t)cx + (size_t)gd[0] * ((size_t)cy + (size_t)gd[1] * cz)];
+        if (t == EMPTY_TILE) continue;
+        for (int dz = -1; dz <= 1; ++dz)
+          for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx)
+              nb[(size_t)t * 27 + (dx + 1) + 3 * ((dy + 1) + 3 * (dz + 1))] =
+                  tile_at(gd, periodic, tile_map, cx + dx, cy + dy, cz + dz);
+      }
+}
+
+/* degenerate BC mask: engine.hpp:110-140 */
+void oracle_degenerate_mask(const uint8_t* types, int d, const int* dims, int periodic,
+                            uint8_t* mask) {
+  lattice_t L;
+  lattice_init(&L, d);
+  const size_t n = (size_t)dims[0] * dims[1] * dims[2];
+  memset(mask, 0, n);
+  for (int z = 0; z < dims[2]; ++z)
+    for (int y = 0; y < dims[1]; ++y)
+      for (int x = 0; x < dims[0]; ++x) {
+        const size_t node = (size_t)x + (size_t)dims[0] * ((size_t)y + (size_t)dims[1] * z);
+        const uint8_t t = types[node];
+        if (t != 2 && t != 3) continue;
+        int degenerate = 0;
+        for (int i = 1; i < L.q && !degenerate; ++i) {
+          int s[3] = {x - L.e[i][0], y - L.e[i][1], z - L.e[i][2]};
+          int outside = 0;
+          for (int k = 0; k < 3; ++k) {
+            if (s[k] < 0 || s[k] >= dims[k]) {
+              if ((periodic >> k) & 1) {
+                s[k] = ((s[k] % dims[k]) + dims[k]) % dims[k];
+              } else {
+                outside = 1;
+                break;
+              }
+            }
+          }
+          degenerate = outside ||
+                       types[(size_t)s[0] + (size_t)dims[0] * ((size_t)s[1] + (size_t)dims[1] * s[2])] == 0;
+        }
+        if (degenerate) mask[node] = 1;
+      }
+}
+
+/* ---- node physics ------------------------------------------------------------------------ */
+/* equilibrium<T>: lattice.hpp:72-91 (squaredNorm in the shim's left-to-right order) */
+static void equilibrium(const lattice_t* L, int incompressible, double rho, const double* u,
+                        double* out) {
+  const double inv_cs2 = 3.0, inv_2cs4 = 4.5, half_inv_cs2 = 1.5;
+  const double uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+  for (int i = 0; i < L->q; ++i) {
+    const double cu = (double)L->e[i][0] * u[0] + (double)L->e[i][1] * u[1] + (double)L->e[i][2] * u[2];
+    const double shape = cu * inv_cs2 + cu * cu * inv_2cs4 - uu * half_inv_cs2;
+    if (!incompressible)
+      out[i] = L->w[i] * rho * (1.0 + shape);
+    else
+      out[i] = L->w[i] * (rho + shape);
+  }
+}
+
+/* BGK CollisionOperator::operator(): collision.hpp:35-65. Returns finite_moments
+ * (engine.hpp:96-102) of the returned moments. */
+static int collide_bgk(const lattice_t* L, int incompressible, double inv_tau, double* f) {
+  double rho = 0.0, m[3] = {0.0, 0.0, 0.0};
+  for (int i = 0; i < L->q; ++i) {
+    rho += f[i];
+    m[0] += (double)L->e[i][0] * f[i];
+    m[1] += (double)L->e[i][1] * f[i];
+    m[2] += (double)L->e[i][2] * f[i];
+  }
+  if (!incompressible) {
+    if (!(rho > 0.0) || !isfinite(rho)) return 0; /* NaN density, f untouched */
+    m[0] /= rho;
+    m[1] /= rho;
+    m[2] /= rho;
+  }
+  double feq[19];
+  equilibrium(L, incompressible, rho, m, feq);
+  for (int i = 0; i < L->q; ++i) f[i] += inv_tau * (feq[i] - f[i]);
+  return isfinite(rho) && isfinite(m[0]) && isfinite(m[1]) && isfinite(m[2]);
+}
+
+/* apply_boundary<T>: engine.hpp:32-65 */
+static int apply_boundary(const lattice_t* L, int incompressible, const double* bc_u,
+                          double bc_rho, int type, double* f, int rho_underdetermined) {
+  if (type == 2) { /* VelocityBC */
+    double rho = 1.0;
+    if (!rho_underdetermined) {
+      rho = 0.0;
+      for (int i = 0; i < L->q; ++i) rho += f[i];
+      if (!(rho > 0.0) || !isfinite(rho)) rho = 1.0;
+    }
+    equilibrium(L, incompressible, rho, bc_u, f);
+    return isfinite(rho) && isfinite(bc_u[0]) && isfinite(bc_u[1]) && isfinite(bc_u[2]);
+  }
+  double rho = 0.0, m[3] = {0.0, 0.0, 0.0};
+  for (int i = 0; i < L->q; ++i) {
+    rho += f[i];
+    m[0] += (double)L->e[i][0] * f[i];
+    m[1] += (double)L->e[i][1] * f[i];
+    m[2] += (double)L->e[i][2] * f[i];
+  }
+  double u[3] = {0.0, 0.0, 0.0};
+  if (!incompressible) {
+    if (rho > 0.0) {
+      u[0] = m[0] / rho;
+      u[1] = m[1] / rho;
+      u[2] = m[2] / rho;
+    }
+  } else {
+    u[0] = m[0];
+    u[1] = m[1];
+    u[2] = m[2];
+  }
+  equilibrium(L, incompressible, bc_rho, u, f);
+  return isfinite(bc_rho) && isfinite(u[0]) && isfinite(u[1]) && isfinite(u[2]);
+}
+
+/* ---- engine ------------------------------------------------------------------------------- */
+/* TileEngineT2C::initialize: engine.hpp:336-352; rho/u given per tile node (T*n_tn), i.e. the
+ * NodeInit already evaluated at node_coords(tile, p). Writes both copies. */
+void oracle_t2c_initialize(int d, int64_t T, int n_tn, int incompressible, const double* rho,
+                           const double* ux, const double* uy, const double* uz, double* pdf0,
+                           double* pdf1) {
+  lattice_t L;
+  lattice_init(&L, d);
+  double feq[19];
+  for (int64_t t = 0; t < T; ++t)
+    for (int p = 0; p < n_tn; ++p) {
+      const int64_t k = t * n_tn + p;
+      const double u[3] = {ux[k], uy[k], uz[k]};
+      equilibrium(&L, incompressible, rho[k], u, feq);
+      for (int i = 0; i < L.q; ++i) {
+        const size_t s = ((size_t)t * L.q + i) * n_tn + p;
+        pdf0[s] = feq[i];
+        pdf1[s] = feq[i];
+      }
+    }
+}
+
+/* Tile-range worker of the sweep (engine.hpp:466-508); the CPU-baseline threading splits
+ * [0,T) into equal contiguous chunks like ThreadPool::parallel_for (thread_pool.hpp:79-82). */
+typedef struct {
+  const lattice_t* L;
+  int a, n_tn;
+  int64_t T;
+  const uint8_t* ttypes;
+  const uint32_t* nb;
+  const uint8_t* bcdeg;
+  const double* read;
+  double* write;
+  double inv_tau;
+  int incompressible;
+  const double* bc_u;
+  double bc_rho;
+  const uint8_t* delta;
+  const uint32_t* src;
+  int64_t t_begin, t_end;
+  int ok;
+} step_ctx_t;
+
+static void* sweep_range(void* arg) {
+  step_ctx_t* c = (step_ctx_t*)arg;
+  const lattice_t* L = c->L;
+  const int q = L->q, n_tn = c->n_tn;
+  int ok = 1;
+  double fin[19];
+  for (int64_t t = c->t_begin; t < c->t_end; ++t) {
+    const uint8_t* own = c->ttypes + (size_t)t * n_tn;
+    const double* own_pdf = c->read + (size_t)t * q * n_tn;
+    for (int p = 0; p < n_tn; ++p) {
+      const uint8_t type = own[p];
+      if (type == 0) continue;
+      for (int i = 0; i < q; ++i) {
+        const int entry = i * n_tn + p;
+        const int dl = c->delta[entry];
+        const size_t sp = c->src[entry];
+        const double* src_pdf;
+        int blocked;
+        if (dl == 13) {
+          src_pdf = own_pdf;
+          blocked = own[sp] == 0;
+        } else {
+          const uint32_t s = c->nb[(size_t)t * 27 + dl];
+          src_pdf = s == EMPTY_TILE ? NULL : c->read + (size_t)s * q * n_tn;
+          blocked = s == EMPTY_TILE || c->ttypes[(size_t)s * n_tn + sp] == 0;
+        }
+        fin[i] = blocked ? own_pdf[(size_t)L->opp[i] * n_tn + p] : src_pdf[(size_t)i * n_tn + sp];
+      }
+      const int good = type == 1 ? collide_bgk(L, c->incompressible, c->inv_tau, fin)
+                                 : apply_boundary(L, c->incompressible, c->bc_u, c->bc_rho, type,
+                                                  fin, c->bcdeg[(size_t)t * n_tn + p] != 0);
+      ok &= good;
+      double* wt = c->write + (size_t)t * q * n_tn;
+      for (int i = 0; i < q; ++i) wt[(size_t)i * n_tn + p] = fin[i];
+    }
+  }
+  c->ok = ok;
+  return NULL;
+}
+
+static void run_chunks(step_ctx_t* ctx, int nthreads) {
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  const int64_t T = ctx->T;
+  const int64_t chunk = (T + nthreads - 1) / nthreads;
+  step_ctx_t sub[256];
+  pthread_t th[256];
+  for (int w = 0; w < nthreads; ++w) {
+    sub[w] = *ctx;
+    sub[w].t_begin = chunk * w < T ? chunk * w : T;
+    sub[w].t_end = sub[w].t_begin + chunk < T ? sub[w].t_begin + chunk : T;
+    if (w > 0) pthread_create(&th[w], NULL, sweep_range, &sub[w]);
+  }
+  sweep_range(&sub[0]);
+  int ok = sub[0].ok;
+  for (int w = 1; w < nthreads; ++w) {
+    pthread_join(th[w], NULL);
+    ok &= sub[w].ok;
+  }
+  ctx->ok = ok;
+}
+
+/* One T2C step: TileEngineT2C::step + sweep, engine.hpp:354-369, 466-514; direction tables
+ * delta_/src_ derived as build_neighbor_tables, engine.hpp:419-445. bcdeg is the degenerate
+ * flag per tile node (bc_degenerate(t,p), engine.hpp:409-417). Returns the step's ok flag. */
+int oracle_t2c_step(int d, int a, int64_t T, const uint8_t* ttypes, const uint32_t* nb,
+                    const uint8_t* bcdeg, const double* read, double* write, double inv_tau,
+                    int incompressible, const double* bc_u, double bc_rho, int nthreads) {
+  lattice_t L;
+  lattice_init(&L, d);
+  const int q = L.q;
+  const int n_tn = a * a * (d == 3 ? a : 1);
+  uint8_t* delta = (uint8_t*)malloc((size_t)q * n_tn);
+  uint32_t* src = (uint32_t*)malloc((size_t)q * n_tn * 4);
+  for (int i = 0; i < q; ++i)
+    for (int p = 0; p < n_tn; ++p) {
+      int l[3] = {p % a, (p / a) % a, p / (a * a)};
+      int dc[3] = {0, 0, 0};
+      for (int k = 0; k < 3; ++k) {
+        l[k] -= L.e[i][k];
+        const int extent = (k == 2 && d == 2) ? 1 : a;
+        if (l[k] < 0) {
+          dc[k] = -1;
+          l[k] += extent;
+        } else if (l[k] >= extent) {
+          dc[k] = 1;
+          l[k] -= extent;
+        }
+      }
+      delta[i * n_tn + p] = (uint8_t)((dc[0] + 1) + 3 * ((dc[1] + 1) + 3 * (dc[2] + 1)));
+      src[i * n_tn + p] = (uint32_t)(l[0] + a * (l[1] + a * l[2]));
+    }
+  step_ctx_t ctx = {&L, a, n_tn, T, ttypes, nb, bcdeg, read, write, inv_tau, incompressible,
+                    bc_u, bc_rho, delta, src, 0, 0, 1};
+  run_chunks(&ctx, nthreads);
+  const int ok = ctx.ok;
+  free(delta);
+  free(src);
+  return ok;
+}
+
+/* TileEngineT2C::fields: engine.hpp:371-390 with moments<T> (lattice.hpp:94-112), scattered
+ * to the unpadded raster (fields.hpp:12-23). Returns -2 on the quasi rho==0 DomainError. */
+int oracle_fields(int d, int a, int64_t T, const int32_t* origins, const uint8_t* ttypes,
+                  const int* geo_dims, const double* pdf, int incompressible, double* rho,
+                  double* ux, double* uy, double* uz, uint8_t* mask) {
+  lattice_t L;
+  lattice_init(&L, d);
+  const int q = L.q;
+  const int n_tn = a * a * (d == 3 ? a : 1);
+  const size_t n = (size_t)geo_dims[0] * geo_dims[1] * geo_dims[2];
+  memset(mask, 0, n);
+  memset(rho, 0, n * 8);
+  memset(ux, 0, n * 8);
+  memset(uy, 0, n * 8);
+  memset(uz, 0, n * 8);
+  for (int64_t t = 0; t < T; ++t)
+    for (int p = 0; p < n_tn; ++p) {
+      if (ttypes[(size_t)t * n_tn + p] == 0) continue;
+      double r = 0.0, m[3] = {0.0, 0.0, 0.0};
+      for (int i = 0; i < q; ++i) {
+        const double f = pdf[((size_t)t * q + i) * n_tn + p];
+        r += f;
+        m[0] += (double)L.e[i][0] * f;
+        m[1] += (double)L.e[i][1] * f;
+        m[2] += (double)L.e[i][2] * f;
+      }
+      if (!incompressible) {
+        if (r == 0.0) return -2;
+        m[0] /= r;
+        m[1] /= r;
+        m[2] /= r;
+      }
+      const int x = origins[3 * t] + p % a, y = origins[3 * t + 1] + (p / a) % a,
+                z = origins[3 * t + 2] + p / (a * a);
+      const size_t node = (size_t)x + (size_t)geo_dims[0] * ((size_t)y + (size_t)geo_dims[1] * z);
+      mask[node] = 1;
+      rho[node] = r;
+      ux[node] = m[0];
+      uy[node] = m[1];
+      uz[node] = m[2];
+    }
+  return 0;
+}
+
+/* FieldData::total_mass: fields.hpp:25-31 (sequential, raster order) */
+double oracle_total_mass(size_t n, const double* rho, const uint8_t* mask) {
+  double m = 0.0;
+  for (size_t i = 0; i < n; ++i)
+    if (mask[i]) m += rho[i];
+  return m;
+}
+
+/* ---- digests --------------------------------------------------------- */
+/* FNV-1a 64 fed one unsigned word per value. */
+uint64_t oracle_fnv_u32(uint64_t h, const uint32_t* v, size_t n) {
+  for (size_t i = 0; i < n; ++i) {
+    h ^= (uint64_t)v[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+uint64_t oracle_fnv_u8(uint64_t h, const uint8_t* v, size_t n) {
+  for (size_t i = 0; i < n; ++i) {
+    h ^= (uint64_t)v[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+/* tile-map digest: tile_map[], then per tile origin[0..2] and types[0..n_tn) */
+uint64_t oracle_tilemap_digest(size_t C, const uint32_t* tile_map, int64_t T, int n_tn,
+                               const int32_t* origins, const uint8_t* ttypes) {
+  uint64_t h = 1469598103934665603ull;
+  h = oracle_fnv_u32(h, tile_map, C);
+  for (int64_t t = 0; t < T; ++t) {
+    h = oracle_fnv_u32(h, (const uint32_t*)(origins + 3 * t), 3);
+    h = oracle_fnv_u8(h, ttypes + (size_t)t * n_tn, (size_t)n_tn);
+  }
+  return h;
+}
+/* fields digest: per non-solid raster node the bit patterns of rho, ux, uy, uz */
+uint64_t oracle_fields_digest(size_t n, const uint8_t* mask, const double* rho,
+                              const double* ux, const double* uy, const double* uz) {
+  uint64_t h = 1469598103934665603ull;
+  for (size_t i = 0; i < n; ++i) {
+    if (!mask[i]) continue;
+    const double* f[4] = {rho + i, ux + i, uy + i, uz + i};
+    for (int k = 0; k < 4; ++k) {
+      uint64_t b;
+      memcpy(&b, f[k], 8);
+      h ^= b;
+      h *= 1099511628211ull;
+    }
+  }
+  return h;
+}
+
+/* wavy_init: tests/test_util.hpp:39-46, evaluated at integer node coordinates (glibc libm,
+ * like the reference test helper). Used to build NodeInit fields for parity cases. */
+void oracle_wavy(size_t n, const int32_t* x, const int32_t* y, const int32_t* z, double* rho,
+                 double* ux, double* uy, double* uz) {
+  for (size_t i = 0; i < n; ++i) {
+    const double X = x[i], Y = y[i], Z = z[i];
+    rho[i] = 1.0 + 0.02 * sin(0.37 * X + 0.11) * cos(0.23 * Y - 0.05) * cos(0.19 * Z + 0.4);
+    ux[i] = 0.01 * sin(0.21 * X + 0.53 * Y);
+    uy[i] = 0.01 * cos(0.17 * Y + 0.29 * Z);
+    uz[i] = 0.01 * sin(0.13 * Z + 0.41 * X);
+  }
+}
