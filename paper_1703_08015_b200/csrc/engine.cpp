@@ -1,0 +1,692 @@
+// Device engine of the T2C path: TileEngineT2C (reference engine.hpp:311-551) with its state in
+// B200 HBM, behind the C ABI of include/splbm_b200.h.
+//
+// Life cycle: create() builds the tile map on the host (bit-exact, tiling.cpp), uploads the
+// tile node types and the 27-neighbour table, derives the per-node gather words on the device
+// and allocates the two PDF copies. step() enqueues fused step kernels on the engine stream
+// (batches are replayed from cached CUDA graphs) and reads back one 8-byte failure stamp per
+// batch. fields() computes moments on the device and scatters them to the raster on the host.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "kernels.h"
+#include "tiling.h"
+
+using namespace splbm_host;
+
+namespace splbm_host {
+thread_local std::string g_last_error;
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace splbm_host
+
+namespace {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(SPLBM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+constexpr uint64_t kChunkNodes = 1ull << 22;  // init / moments staging (4 x 32 MB)
+constexpr int kGraphSteps = 32;               // steps per captured graph (even)
+
+}  // namespace
+
+struct splbm_dev_engine {
+  // configuration
+  int d = 3, q = 19, a = 4, n_tn = 64, periodic = 0, incompressible = 0, device = 0;
+  double tau = 1.0, inv_tau = 1.0;
+  splbm_dev::BcParams bc{0, 0, 0, 1};
+  TileMap tm;  // global tile cover
+  // slab (stored = [low halo][owned][high halo], each in compact order)
+  int slab_axis = 2, slab_z0 = 0, slab_z1 = 0;
+  uint64_t n_low = 0, n_own = 0, n_high = 0, n_stored = 0;
+  uint64_t g_low0 = 0, g_own0 = 0, g_high0 = 0;  // global index of each group's first tile
+  uint64_t send_low_tiles = 0, send_high_tiles = 0;  // tiles of the bottom / top owned plane
+  uint64_t fluid_nodes = 0;
+  // device state
+  cudaStream_t stream = nullptr;
+  double* pdf[2] = {nullptr, nullptr};
+  uint32_t* info = nullptr;
+  uint32_t* nb = nullptr;
+  unsigned long long* failed = nullptr;
+  long long* step_base = nullptr;
+  int* domain_err = nullptr;
+  int* halo_dirs = nullptr;  // [0..4] ez=+1 set, [5..9] ez=-1 set (or 3+3 in 2D)
+  int n_halo_dirs = 0;
+  double* scratch = nullptr;
+  uint64_t device_bytes = 0;
+  int read = 0;
+  long step_count = 0;
+  uint64_t visits = 0;
+  uint64_t launches = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool batch_timed = false;
+  long pending_steps = 0;
+  std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
+
+  ~splbm_dev_engine() {
+    if (device >= 0) cudaSetDevice(device);
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (void* p : {static_cast<void*>(pdf[0]), static_cast<void*>(pdf[1]),
+                    static_cast<void*>(info), static_cast<void*>(nb), static_cast<void*>(failed),
+                    static_cast<void*>(step_base), static_cast<void*>(domain_err),
+                    static_cast<void*>(halo_dirs), static_cast<void*>(scratch)})
+      if (p) cudaFree(p);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  template <class T>
+  T* alloc(std::size_t count) {
+    void* p = nullptr;
+    const std::size_t bytes = std::max<std::size_t>(count, 1) * sizeof(T);
+    const cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess)
+      throw Error(SPLBM_ERR_CUDA, "cudaMalloc of " + std::to_string(bytes) +
+                                      " bytes failed: " + cudaGetErrorString(e));
+    device_bytes += bytes;
+    return static_cast<T*>(p);
+  }
+
+  uint64_t tile_stride() const { return static_cast<uint64_t>(q) * n_tn; }
+
+  splbm_dev::StepArgs step_args(int rd, int rel) const {
+    splbm_dev::StepArgs s{};
+    s.read = pdf[rd];
+    s.write = pdf[1 - rd];
+    s.info = info;
+    s.nb = nb;
+    s.t0 = n_low;
+    s.n_nodes = n_own * n_tn;
+    s.a = a;
+    s.inv_tau = inv_tau;
+    s.bc = bc;
+    s.failed = failed;
+    s.step_base = step_base;
+    s.rel = rel;
+    return s;
+  }
+
+  // Enqueue k steps starting from parity rd (direct launches) + the counter bump.
+  void enqueue_direct(int rd, int k) {
+    for (int r = 0; r < k; ++r) {
+      CK(splbm_dev::launch_step(d, incompressible != 0, step_args(rd, r), stream));
+      rd = 1 - rd;
+      ++launches;
+    }
+    CK(splbm_dev::launch_bump(step_base, k, stream));
+    ++launches;
+  }
+
+  cudaGraphExec_t graph_for(int rd) {
+    const auto key = std::make_pair(kGraphSteps, rd);
+    auto it = graphs.find(key);
+    if (it != graphs.end()) return it->second;
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    const uint64_t saved = launches;
+    try {
+      enqueue_direct(rd, kGraphSteps);
+    } catch (...) {
+      cudaStreamEndCapture(stream, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    launches = saved;
+    CK(cudaStreamEndCapture(stream, &g));
+    cudaGraphExec_t ex = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    CK(e);
+    graphs[key] = ex;
+    return ex;
+  }
+
+  void enqueue_steps(long n) {
+    long left = n;
+    while (left >= kGraphSteps) {
+      CK(cudaGraphLaunch(graph_for(read), stream));
+      launches += kGraphSteps + 1;
+      left -= kGraphSteps;  // kGraphSteps is even: parity unchanged
+    }
+    if (left > 0) {
+      enqueue_direct(read, static_cast<int>(left));
+      if (left & 1) read = 1 - read;
+    }
+    step_count += n;
+    visits += n_own * static_cast<uint64_t>(n);
+  }
+};
+
+namespace {
+
+splbm_dev_engine* checked(splbm_dev_engine* e) {
+  if (!e) throw config_error("null engine");
+  CK(cudaSetDevice(e->device));
+  return e;
+}
+
+void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
+  if (!desc || !desc->types) throw config_error("null descriptor");
+  const int d = desc->d;
+  if (d != 2 && d != 3) throw config_error("dimension must be 2 or 3");
+  if (!(desc->tau > 0.5)) throw config_error("relaxation time tau must be > 0.5");  // collision.cpp:90
+  e->d = d;
+  e->q = d == 2 ? 9 : 19;
+  e->a = desc->tile > 0 ? desc->tile : (d == 2 ? 16 : 4);  // SimConfig::tile_edge (engine.hpp:575)
+  e->periodic = desc->periodic;
+  e->incompressible = desc->incompressible ? 1 : 0;
+  e->tau = desc->tau;
+  e->inv_tau = 1.0 / desc->tau;  // collision.cpp:93
+  e->bc = {desc->bc_velocity[0], desc->bc_velocity[1], desc->bc_velocity[2], desc->bc_density};
+  e->device = desc->device;
+  int dims[3] = {desc->dims[0], desc->dims[1], d == 2 ? 1 : desc->dims[2]};
+  if (d == 2 && desc->dims[2] != 1 && desc->dims[2] != 0)
+    throw config_error("2D geometry requires nz = 1");
+
+  e->tm = build_tile_map(desc->types, d, dims, e->a, e->periodic);
+  TileMap& tm = e->tm;
+  e->n_tn = tm.n_tn;
+  const std::vector<uint32_t> nb_global = neighbour_table(tm);
+  const std::vector<uint8_t> deg = degenerate_mask(desc->types, d, dims, e->periodic);
+
+  // PressureBC under the quasi-compressible model needs rho_bc > 0 (lattice.hpp:76-78)
+  if (!e->incompressible && !(desc->bc_density > 0.0)) {
+    bool has_p = false;
+    for (std::size_t i = 0, n = static_cast<std::size_t>(dims[0]) * dims[1] * dims[2]; i < n && !has_p; ++i)
+      has_p = desc->types[i] == 3;
+    if (has_p) throw domain_error("equilibrium requires rho > 0 for the quasi-compressible model");
+  }
+
+  // ---- slab selection along the last axis -----------------------------------
+  const int ax = d == 3 ? 2 : 1;
+  const int L = tm.grid_dims[ax];
+  e->slab_axis = ax;
+  int z0 = desc->slab_z0, z1 = desc->slab_z1;
+  if (z0 == 0 && z1 == 0) z1 = L;
+  if (z0 < 0 || z1 > L || z0 >= z1) throw config_error("invalid slab range");
+  e->slab_z0 = z0;
+  e->slab_z1 = z1;
+  const uint64_t plane_cells = static_cast<uint64_t>(tm.grid_dims[0]) * (d == 3 ? tm.grid_dims[1] : 1);
+  // F(z): first compact index of plane z (tile_map is z-major, compact order preserved)
+  std::vector<uint64_t> F(static_cast<std::size_t>(L) + 1, 0);
+  for (int z = 0; z < L; ++z) {
+    uint64_t cnt = 0;
+    const uint32_t* row = tm.tile_map.data() + static_cast<uint64_t>(z) * plane_cells;
+    for (uint64_t c = 0; c < plane_cells; ++c) cnt += row[c] != kEmpty;
+    F[z + 1] = F[z] + cnt;
+  }
+  const bool whole = (z0 == 0 && z1 == L);
+  const bool per_ax = (e->periodic >> ax) & 1;
+  int zl = -1, zh = -1;
+  if (!whole) {
+    if (z0 > 0) zl = z0 - 1; else if (per_ax) zl = L - 1;
+    if (z1 < L) zh = z1; else if (per_ax) zh = 0;
+    if ((zl >= z0 && zl < z1) || (zh >= z0 && zh < z1) || (zl >= 0 && zl == zh))
+      throw config_error("slab too thick for its periodic halo planes");
+  }
+  e->g_own0 = F[z0];
+  e->n_own = F[z1] - F[z0];
+  e->g_low0 = zl >= 0 ? F[zl] : 0;
+  e->n_low = zl >= 0 ? F[zl + 1] - F[zl] : 0;
+  e->g_high0 = zh >= 0 ? F[zh] : 0;
+  e->n_high = zh >= 0 ? F[zh + 1] - F[zh] : 0;
+  e->n_stored = e->n_low + e->n_own + e->n_high;
+  e->send_low_tiles = whole ? 0 : F[z0 + 1] - F[z0];
+  e->send_high_tiles = whole ? 0 : F[z1] - F[z1 - 1];
+
+  auto to_local = [&](uint32_t g) -> uint32_t {
+    if (g == kEmpty) return kEmpty;
+    if (g >= e->g_own0 && g < e->g_own0 + e->n_own) return static_cast<uint32_t>(e->n_low + (g - e->g_own0));
+    if (e->n_low && g >= e->g_low0 && g < e->g_low0 + e->n_low) return static_cast<uint32_t>(g - e->g_low0);
+    if (e->n_high && g >= e->g_high0 && g < e->g_high0 + e->n_high)
+      return static_cast<uint32_t>(e->n_low + e->n_own + (g - e->g_high0));
+    return kEmpty;
+  };
+  auto global_of = [&](uint64_t s) -> uint64_t {
+    if (s < e->n_low) return e->g_low0 + s;
+    if (s < e->n_low + e->n_own) return e->g_own0 + (s - e->n_low);
+    return e->g_high0 + (s - e->n_low - e->n_own);
+  };
+
+  const uint64_t S = e->n_stored;
+  const int n_tn = e->n_tn;
+  std::vector<uint32_t> nb_local(S * 27);
+  std::vector<uint8_t> types_local(S * n_tn);
+  parallel_for(S, [&](std::size_t b, std::size_t en) {
+    for (std::size_t s = b; s < en; ++s) {
+      const uint64_t g = global_of(s);
+      for (int k = 0; k < 27; ++k) nb_local[s * 27 + k] = to_local(nb_global[g * 27 + k]);
+      const int32_t* o = &tm.origins[3 * g];
+      for (int p = 0; p < n_tn; ++p) {
+        uint8_t t = tm.types[g * n_tn + p];
+        if (t == 2 || t == 3) {  // bc_degenerate(t, p) (engine.hpp:409-417)
+          const int x = o[0] + p % e->a, y = o[1] + (p / e->a) % e->a,
+                    z = o[2] + (d == 3 ? p / (e->a * e->a) : 0);
+          if (deg[raster_index(dims, x, y, z)]) t |= 4;
+        }
+        types_local[s * n_tn + p] = t;
+      }
+    }
+  }, 1024);
+  for (uint64_t s = e->n_low; s < e->n_low + e->n_own; ++s) e->fluid_nodes += tm.fluid_count[global_of(s)];
+
+  // ---- device ------------------------------------------------------------------------------
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw Error(SPLBM_ERR_CUDA, "no CUDA device available (the T2C path has no CPU fallback)");
+  if (e->device < 0 || e->device >= ndev) throw config_error("invalid CUDA device ordinal");
+  CK(cudaSetDevice(e->device));
+  CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&e->ev0));
+  CK(cudaEventCreate(&e->ev1));
+  const uint64_t nslots = S * e->tile_stride();
+  e->pdf[0] = e->alloc<double>(nslots);
+  e->pdf[1] = e->alloc<double>(nslots);
+  e->info = e->alloc<uint32_t>(S * n_tn);
+  e->nb = e->alloc<uint32_t>(S * 27);
+  e->failed = e->alloc<unsigned long long>(1);
+  e->step_base = e->alloc<long long>(1);
+  e->domain_err = e->alloc<int>(1);
+  e->scratch = e->alloc<double>(4 * std::min<uint64_t>(kChunkNodes, std::max<uint64_t>(S * n_tn, 1)));
+  // face direction sets: slab axis component +1 then -1 (lattice.cpp order)
+  {
+    static const int e3z[19] = {0, 0, 0, 0, 0, 1, -1, 0, 0, 0, 0, 1, -1, -1, 1, 1, -1, -1, 1};
+    static const int e2y[9] = {0, 0, 0, 1, -1, 1, -1, -1, 1};
+    std::vector<int> dirs;
+    for (int sgn : {1, -1})
+      for (int i = 0; i < e->q; ++i)
+        if ((d == 3 ? e3z[i] : e2y[i]) == sgn) dirs.push_back(i);
+    e->n_halo_dirs = static_cast<int>(dirs.size()) / 2;
+    e->halo_dirs = e->alloc<int>(dirs.size());
+    CK(cudaMemcpy(e->halo_dirs, dirs.data(), dirs.size() * sizeof(int), cudaMemcpyHostToDevice));
+  }
+  CK(cudaMemsetAsync(e->step_base, 0, sizeof(long long), e->stream));
+  CK(cudaMemsetAsync(e->pdf[0], 0, nslots * 8, e->stream));
+  CK(cudaMemsetAsync(e->pdf[1], 0, nslots * 8, e->stream));
+  CK(cudaMemcpyAsync(e->nb, nb_local.data(), nb_local.size() * 4, cudaMemcpyHostToDevice, e->stream));
+  {
+    uint8_t* types_d = nullptr;
+    CK(cudaMalloc(&types_d, std::max<std::size_t>(types_local.size(), 1)));
+    CK(cudaMemcpyAsync(types_d, types_local.data(), types_local.size(), cudaMemcpyHostToDevice, e->stream));
+    splbm_dev::NodeInfoArgs ni{types_d, e->nb, e->info, S, e->a};
+    CK(splbm_dev::launch_node_info(d, ni, e->stream));
+    ++e->launches;
+    CK(cudaStreamSynchronize(e->stream));
+    cudaFree(types_d);
+  }
+}
+
+void check_domain_flag(splbm_dev_engine* e, const char* msg) {
+  int flag = 0;
+  CK(cudaMemcpyAsync(&flag, e->domain_err, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  if (flag) throw domain_error(msg);
+}
+
+void read_failure(splbm_dev_engine* e, int* ok_out, long* failed_out) {
+  unsigned long long f = 0;
+  CK(cudaMemcpyAsync(&f, e->failed, sizeof(f), cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  e->pending_steps = 0;
+  if (ok_out) *ok_out = f == ULLONG_MAX ? 1 : 0;
+  if (failed_out) *failed_out = f == ULLONG_MAX ? 0 : static_cast<long>(f);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* splbm_last_error(void) { return g_last_error.c_str(); }
+const char* splbm_version(void) { return "splbm_b200 0.1 (sm_100a)"; }
+
+int splbm_dev_create(const splbm_dev_desc* desc, splbm_dev_engine** out) {
+  if (!out) return SPLBM_ERR_CONFIG;
+  *out = nullptr;
+  auto e = std::make_unique<splbm_dev_engine>();
+  e->device = desc ? desc->device : 0;
+  const int rc = guarded([&] { build(e.get(), desc); });
+  if (rc == SPLBM_OK) *out = e.release();
+  return rc;
+}
+
+void splbm_dev_destroy(splbm_dev_engine* e) { delete e; }
+
+int splbm_dev_get_info(const splbm_dev_engine* e, splbm_dev_info* out) {
+  return guarded([&] {
+    if (!e || !out) throw config_error("null argument");
+    out->n_tiles = e->n_own;
+    out->n_tiles_stored = e->n_stored;
+    out->n_tn = e->n_tn;
+    out->q = e->q;
+    out->a = e->a;
+    out->d = e->d;
+    for (int k = 0; k < 3; ++k) {
+      out->grid_dims[k] = e->tm.grid_dims[k];
+      out->padded_dims[k] = e->tm.padded_dims[k];
+    }
+    out->fluid_nodes = e->fluid_nodes;
+    out->device_bytes = e->device_bytes;
+    out->phi_t = e->n_own ? static_cast<double>(e->fluid_nodes) / (static_cast<double>(e->n_own) * e->n_tn) : 0.0;
+    const double cells = static_cast<double>(e->tm.grid_dims[0]) * e->tm.grid_dims[1] * e->tm.grid_dims[2];
+    out->ratio_tiles = e->tm.n_tiles ? cells / static_cast<double>(e->tm.n_tiles) : 0.0;
+  });
+}
+
+int splbm_dev_get_tile_grid(const splbm_dev_engine* e, uint32_t* tile_map, int32_t* origins,
+                            uint8_t* tile_types, uint32_t* fluid_count, uint32_t* nb) {
+  return guarded([&] {
+    if (!e) throw config_error("null engine");
+    const TileMap& tm = e->tm;
+    if (tile_map) std::memcpy(tile_map, tm.tile_map.data(), tm.tile_map.size() * 4);
+    if (origins) std::memcpy(origins, tm.origins.data(), tm.origins.size() * 4);
+    if (tile_types) std::memcpy(tile_types, tm.types.data(), tm.types.size());
+    if (fluid_count) std::memcpy(fluid_count, tm.fluid_count.data(), tm.fluid_count.size() * 4);
+    if (nb) {
+      const auto n = neighbour_table(tm);
+      std::memcpy(nb, n.data(), n.size() * 4);
+    }
+  });
+}
+
+int splbm_dev_stored_tiles(const splbm_dev_engine* e, uint64_t* global_ids) {
+  return guarded([&] {
+    if (!e || !global_ids) throw config_error("null argument");
+    for (uint64_t s = 0; s < e->n_stored; ++s) {
+      if (s < e->n_low) global_ids[s] = e->g_low0 + s;
+      else if (s < e->n_low + e->n_own) global_ids[s] = e->g_own0 + (s - e->n_low);
+      else global_ids[s] = e->g_high0 + (s - e->n_low - e->n_own);
+    }
+  });
+}
+
+static int initialize_impl(splbm_dev_engine* e, const double* rho, const double* ux,
+                           const double* uy, const double* uz, double rho0, const double* u0) {
+  return guarded([&] {
+    checked(e);
+    const uint64_t total = e->n_stored * e->n_tn;
+    CK(cudaMemsetAsync(e->domain_err, 0, sizeof(int), e->stream));
+    for (uint64_t node0 = 0; node0 < total; node0 += kChunkNodes) {
+      const uint64_t cnt = std::min(kChunkNodes, total - node0);
+      splbm_dev::InitArgs ia{};
+      ia.pdf0 = e->pdf[0];
+      ia.pdf1 = e->pdf[1];
+      ia.node0 = node0;
+      ia.count = cnt;
+      ia.n_tn = e->n_tn;
+      ia.domain_error = e->domain_err;
+      if (rho) {
+        double* s = e->scratch;
+        CK(cudaMemcpyAsync(s, rho + node0, cnt * 8, cudaMemcpyHostToDevice, e->stream));
+        CK(cudaMemcpyAsync(s + cnt, ux + node0, cnt * 8, cudaMemcpyHostToDevice, e->stream));
+        CK(cudaMemcpyAsync(s + 2 * cnt, uy + node0, cnt * 8, cudaMemcpyHostToDevice, e->stream));
+        CK(cudaMemcpyAsync(s + 3 * cnt, uz + node0, cnt * 8, cudaMemcpyHostToDevice, e->stream));
+        ia.rho = s;
+        ia.ux = s + cnt;
+        ia.uy = s + 2 * cnt;
+        ia.uz = s + 3 * cnt;
+      } else {
+        ia.rho0 = rho0;
+        ia.u0[0] = u0[0];
+        ia.u0[1] = u0[1];
+        ia.u0[2] = u0[2];
+      }
+      CK(splbm_dev::launch_init(e->d, e->incompressible != 0, ia, e->stream));
+      ++e->launches;
+    }
+    check_domain_flag(e, "equilibrium requires rho > 0 for the quasi-compressible model");
+    e->read = 0;
+    e->step_count = 0;  // engine.hpp:350-351
+    CK(cudaMemsetAsync(e->step_base, 0, sizeof(long long), e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+  });
+}
+
+int splbm_dev_initialize(splbm_dev_engine* e, const double* rho, const double* ux,
+                         const double* uy, const double* uz) {
+  if (!rho || !ux || !uy || !uz) {
+    set_last_error("null initial field");
+    return SPLBM_ERR_CONFIG;
+  }
+  return initialize_impl(e, rho, ux, uy, uz, 0.0, nullptr);
+}
+
+int splbm_dev_initialize_uniform(splbm_dev_engine* e, double rho, const double u[3]) {
+  const double zero[3] = {0.0, 0.0, 0.0};
+  return initialize_impl(e, nullptr, nullptr, nullptr, nullptr, rho, u ? u : zero);
+}
+
+int splbm_dev_step_async(splbm_dev_engine* e, long nsteps) {
+  return guarded([&] {
+    checked(e);
+    if (nsteps < 0) throw config_error("steps must be non-negative");
+    if (e->pending_steps == 0) {
+      CK(cudaMemsetAsync(e->failed, 0xff, sizeof(unsigned long long), e->stream));
+    }
+    CK(cudaEventRecord(e->ev0, e->stream));
+    e->enqueue_steps(nsteps);
+    CK(cudaEventRecord(e->ev1, e->stream));
+    e->batch_timed = true;
+    e->pending_steps += nsteps;
+  });
+}
+
+int splbm_dev_sync(splbm_dev_engine* e, int* ok_out, long* failed_step_out) {
+  return guarded([&] {
+    checked(e);
+    read_failure(e, ok_out, failed_step_out);
+  });
+}
+
+int splbm_dev_step(splbm_dev_engine* e, long nsteps, int* ok_out, long* failed_step_out) {
+  int rc = splbm_dev_step_async(e, nsteps);
+  if (rc != SPLBM_OK) return rc;
+  return splbm_dev_sync(e, ok_out, failed_step_out);
+}
+
+long splbm_dev_current_step(const splbm_dev_engine* e) { return e ? e->step_count : 0; }
+uint64_t splbm_dev_tile_visits(const splbm_dev_engine* e) { return e ? e->visits : 0; }
+uint64_t splbm_dev_launch_count(const splbm_dev_engine* e) { return e ? e->launches : 0; }
+
+int splbm_dev_padded_dims(const splbm_dev_engine* e, int out[3]) {
+  if (!e || !out) return SPLBM_ERR_CONFIG;
+  for (int k = 0; k < 3; ++k) out[k] = e->tm.padded_dims[k];
+  return SPLBM_OK;
+}
+
+int splbm_dev_fields(splbm_dev_engine* e, double* rho, double* ux, double* uy, double* uz,
+                     uint8_t* mask, double* mass_out) {
+  return guarded([&] {
+    checked(e);
+    const int* dims = e->tm.dims;
+    const std::size_t n = static_cast<std::size_t>(dims[0]) * dims[1] * dims[2];
+    // FieldData frame: zeros, mask at non-solid nodes (engine.hpp:516-534)
+    std::vector<double> hr, hx, hy, hz;
+    double* out[4] = {rho, ux, uy, uz};
+    std::vector<double>* own[4] = {&hr, &hx, &hy, &hz};
+    const bool need_mass = mass_out != nullptr;
+    for (int k = 0; k < 4; ++k) {
+      if (!out[k] && (k > 0 || !need_mass)) continue;
+      if (!out[k]) {
+        own[k]->assign(n, 0.0);
+        out[k] = own[k]->data();
+      } else {
+        std::memset(out[k], 0, n * 8);
+      }
+    }
+    std::vector<uint8_t> mloc;
+    if (!mask && need_mass) {
+      mloc.assign(n, 0);
+      mask = mloc.data();
+    }
+    if (mask) std::memset(mask, 0, n);
+    CK(cudaMemsetAsync(e->domain_err, 0, sizeof(int), e->stream));
+    const uint64_t first = e->n_low * e->n_tn, total = e->n_own * e->n_tn;
+    std::vector<double> stage(4 * std::min<uint64_t>(kChunkNodes, std::max<uint64_t>(total, 1)));
+    const int a = e->a, n_tn = e->n_tn;
+    for (uint64_t k0 = 0; k0 < total; k0 += kChunkNodes) {
+      const uint64_t cnt = std::min(kChunkNodes, total - k0);
+      splbm_dev::MomentsArgs ma{};
+      ma.pdf = e->pdf[e->read];
+      ma.info = e->info;
+      ma.rho = e->scratch;
+      ma.ux = e->scratch + cnt;
+      ma.uy = e->scratch + 2 * cnt;
+      ma.uz = e->scratch + 3 * cnt;
+      ma.node0 = first + k0;
+      ma.count = cnt;
+      ma.n_tn = n_tn;
+      ma.domain_error = e->domain_err;
+      CK(splbm_dev::launch_moments(e->d, e->incompressible != 0, ma, e->stream));
+      ++e->launches;
+      CK(cudaMemcpyAsync(stage.data(), e->scratch, 4 * cnt * 8, cudaMemcpyDeviceToHost, e->stream));
+      CK(cudaStreamSynchronize(e->stream));
+      parallel_for(cnt / n_tn, [&](std::size_t b, std::size_t en) {
+        for (std::size_t tl = b; tl < en; ++tl) {
+          const uint64_t s = (first + k0) / n_tn + tl;  // stored tile index
+          const uint64_t g = e->g_own0 + (s - e->n_low);
+          const int32_t* o = &e->tm.origins[3 * g];
+          const uint8_t* tt = &e->tm.types[g * n_tn];
+          for (int p = 0; p < n_tn; ++p) {
+            if (tt[p] == 0) continue;
+            const int x = o[0] + p % a, y = o[1] + (p / a) % a, z = o[2] + (e->d == 3 ? p / (a * a) : 0);
+            const std::size_t node = raster_index(dims, x, y, z);
+            const std::size_t k = tl * n_tn + p;
+            for (int c = 0; c < 4; ++c)
+              if (out[c]) out[c][node] = stage[c * cnt + k];
+            if (mask) mask[node] = 1;
+          }
+        }
+      }, 256);
+    }
+    int flag = 0;
+    CK(cudaMemcpy(&flag, e->domain_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (flag) throw domain_error("moments: zero density under the quasi-compressible model");
+    if (mass_out) {  // FieldData::total_mass, sequential raster order (fields.hpp:25-31)
+      double m = 0.0;
+      for (std::size_t i = 0; i < n; ++i)
+        if (mask[i]) m += out[0][i];
+      *mass_out = m;
+    }
+  });
+}
+
+int splbm_dev_reduce(splbm_dev_engine* e, double out[3]) {
+  return guarded([&] {
+    checked(e);
+    const int blocks = 1184;  // 8 x 148 SMs, fixed so the summation order is fixed
+    double* dev = e->alloc<double>(3 * blocks + 3);
+    splbm_dev::ReduceArgs ra{e->pdf[e->read], e->info, e->n_low * e->n_tn, e->n_own * e->n_tn,
+                             e->n_tn, dev};
+    cudaError_t err = splbm_dev::launch_reduce(e->d, e->incompressible != 0, ra, blocks,
+                                               dev + 3 * blocks, e->stream);
+    e->launches += 2;
+    if (err == cudaSuccess)
+      err = cudaMemcpyAsync(out, dev + 3 * blocks, 3 * sizeof(double), cudaMemcpyDeviceToHost, e->stream);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(e->stream);
+    cudaFree(dev);
+    e->device_bytes -= (3 * blocks + 3) * sizeof(double);
+    CK(err);
+  });
+}
+
+int splbm_dev_get_pdf(splbm_dev_engine* e, double* f_out) {
+  return guarded([&] {
+    checked(e);
+    CK(cudaMemcpyAsync(f_out, e->pdf[e->read], e->n_stored * e->tile_stride() * 8,
+                       cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+  });
+}
+
+int splbm_dev_set_pdf(splbm_dev_engine* e, const double* f) {
+  return guarded([&] {
+    checked(e);
+    CK(cudaMemcpyAsync(e->pdf[e->read], f, e->n_stored * e->tile_stride() * 8,
+                       cudaMemcpyHostToDevice, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+  });
+}
+
+void* splbm_dev_stream(splbm_dev_engine* e) { return e ? static_cast<void*>(e->stream) : nullptr; }
+
+int splbm_dev_last_batch_ms(splbm_dev_engine* e, float* ms_out) {
+  return guarded([&] {
+    checked(e);
+    if (!e->batch_timed) throw config_error("no timed batch yet");
+    CK(cudaEventSynchronize(e->ev1));
+    CK(cudaEventElapsedTime(ms_out, e->ev0, e->ev1));
+  });
+}
+
+int splbm_dev_halo_bytes(const splbm_dev_engine* e, uint64_t* low_bytes, uint64_t* high_bytes) {
+  if (!e) return SPLBM_ERR_CONFIG;
+  const uint64_t face = static_cast<uint64_t>(e->n_tn / e->a) * e->n_halo_dirs * 8;
+  if (low_bytes) *low_bytes = e->send_low_tiles * face;
+  if (high_bytes) *high_bytes = e->send_high_tiles * face;
+  return SPLBM_OK;
+}
+
+int splbm_dev_halo_recv_bytes(const splbm_dev_engine* e, uint64_t* low_bytes, uint64_t* high_bytes) {
+  if (!e) return SPLBM_ERR_CONFIG;
+  const uint64_t face = static_cast<uint64_t>(e->n_tn / e->a) * e->n_halo_dirs * 8;
+  if (low_bytes) *low_bytes = e->n_low * face;
+  if (high_bytes) *high_bytes = e->n_high * face;
+  return SPLBM_OK;
+}
+
+// pack: low_dev <- bottom owned plane, layer 0, directions leaving downwards (axis comp -1);
+//       high_dev <- top owned plane, layer a-1, directions leaving upwards (axis comp +1).
+int splbm_dev_halo_pack(splbm_dev_engine* e, void* low_dev, void* high_dev) {
+  return guarded([&] {
+    checked(e);
+    const int nd = e->n_halo_dirs;
+    if (low_dev && e->send_low_tiles) {
+      splbm_dev::HaloArgs h{e->pdf[e->read], static_cast<double*>(low_dev), e->n_low,
+                            e->send_low_tiles, e->a, 0, nd, e->halo_dirs + nd, 1};
+      CK(splbm_dev::launch_halo(e->d, h, e->stream));
+      ++e->launches;
+    }
+    if (high_dev && e->send_high_tiles) {
+      splbm_dev::HaloArgs h{e->pdf[e->read], static_cast<double*>(high_dev),
+                            e->n_low + e->n_own - e->send_high_tiles, e->send_high_tiles, e->a,
+                            e->a - 1, nd, e->halo_dirs, 1};
+      CK(splbm_dev::launch_halo(e->d, h, e->stream));
+      ++e->launches;
+    }
+  });
+}
+
+// unpack: low_dev (the lower neighbour's high face) -> low halo plane, layer a-1, upward dirs;
+//         high_dev (the upper neighbour's low face) -> high halo plane, layer 0, downward dirs.
+int splbm_dev_halo_unpack(splbm_dev_engine* e, const void* low_dev, const void* high_dev) {
+  return guarded([&] {
+    checked(e);
+    const int nd = e->n_halo_dirs;
+    if (low_dev && e->n_low) {
+      splbm_dev::HaloArgs h{e->pdf[e->read], const_cast<double*>(static_cast<const double*>(low_dev)),
+                            0, e->n_low, e->a, e->a - 1, nd, e->halo_dirs, 0};
+      CK(splbm_dev::launch_halo(e->d, h, e->stream));
+      ++e->launches;
+    }
+    if (high_dev && e->n_high) {
+      splbm_dev::HaloArgs h{e->pdf[e->read], const_cast<double*>(static_cast<const double*>(high_dev)),
+                            e->n_low + e->n_own, e->n_high, e->a, 0, nd, e->halo_dirs + nd, 0};
+      CK(splbm_dev::launch_halo(e->d, h, e->stream));
+      ++e->launches;
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,410 @@
+// sm_100a kernels of the T2C time-step path (arXiv 1703.08015; reference engine.hpp:311-551).
+//
+// HBM layout: per-tile structure of arrays, slot (t*q + i)*n_tn + p exactly as
+// the reference (engine.hpp:397-399), two copies (read/write swapped per step). Per tile node a
+// 32-bit gather word `info` replaces the reference's per-direction node-type lookups:
+//   bits 0..q-1  direction i is blocked (own solid source, EMPTY neighbour tile or solid
+//                neighbour source) -> half-way bounce-back from the own opposite slot
+//   bits 24..25  NodeType; bit 26 bc_degenerate (engine.hpp:409-417)
+//   bit 27       solid node whose 32-B sector holds a non-solid node: written (as 0.0) so
+//                every store sector is whole (no L2 partial-write fills); never read.
+// One thread per tile node, 256 threads per CTA, consecutive threads = consecutive p so all
+// q stores of a warp are 256-B coalesced runs; the gather reads the own tile (L1) and the
+// face-adjacent neighbour tiles (L2 hits: neighbours are near in the compact z-major order).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "lattice.cuh"
+#include "kernels.h"
+
+namespace splbm_dev {
+
+constexpr uint32_t kEmpty = 0xffffffffu;
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ void st_stream(double* p, double v) {
+  asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------------------------
+// The fused gather-propagation + BGK/boundary + store step (engine.hpp:466-514, collision.hpp:35-65,
+// engine.hpp:32-65). A > 0 is a compile-time tile edge; A == 0 reads a_rt.
+template <int D, int A, bool INC>
+__global__ void __launch_bounds__(kThreads) t2c_step_kernel(StepArgs args) {
+  constexpr int Q = Lat<D>::Q;
+  const int a = A > 0 ? A : args.a;
+  const int az = D == 3 ? a : 1;
+  const int n_tn = a * a * az;
+  const uint64_t g = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
+  if (g >= args.n_nodes) return;
+  const uint64_t t = args.t0 + g / static_cast<uint64_t>(n_tn);
+  const int p = static_cast<int>(g % static_cast<uint64_t>(n_tn));
+  const uint64_t node = t * n_tn + p;
+  const uint32_t info = __ldg(args.info + node);
+  const int type = (info >> 24) & 3;
+  const uint64_t tile_stride = static_cast<uint64_t>(Q) * n_tn;
+  double* wr = args.write + t * tile_stride + p;
+  if (type == 0) {
+    if (info & (1u << 27)) {
+#pragma unroll
+      for (int i = 0; i < Q; ++i) st_stream(wr + i * n_tn, 0.0);
+    }
+    return;
+  }
+  const int lx = p % a;
+  const int ly = (p / a) % a;
+  const int lz = D == 3 ? p / (a * a) : 0;
+  const double* own = args.read + t * tile_stride;
+  const uint32_t* nbt = args.nb + t * 27;
+
+  double f[Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    // source node x - e_i (engine.hpp:421-445): local coordinates and neighbour cell offset
+    int sx = lx - ex<D>(i), sy = ly - ey<D>(i), sz = lz - ez<D>(i);
+    int dx = 0, dy = 0, dz = 0;
+    if (ex<D>(i) != 0) {
+      if (sx < 0) { dx = -1; sx += a; } else if (sx >= a) { dx = 1; sx -= a; }
+    }
+    if (ey<D>(i) != 0) {
+      if (sy < 0) { dy = -1; sy += a; } else if (sy >= a) { dy = 1; sy -= a; }
+    }
+    if (D == 3 && ez<D>(i) != 0) {
+      if (sz < 0) { dz = -1; sz += a; } else if (sz >= a) { dz = 1; sz -= a; }
+    }
+    const int delta = (dx + 1) + 3 * ((dy + 1) + 3 * (dz + 1));
+    const int sp = sx + a * (sy + a * sz);
+    const bool blocked = (info >> i) & 1u;
+    const double* src;
+    if (blocked) {
+      src = own + opp(i) * n_tn + p;  // half-way bounce-back (engine.hpp:498-500)
+    } else if (delta == 13) {
+      src = own + i * n_tn + sp;
+    } else {
+      const uint64_t s = __ldg(nbt + delta);
+      src = args.read + s * tile_stride + i * n_tn + sp;
+    }
+    f[i] = __ldg(src);
+  }
+
+  bool good;
+  if (type == 1) {
+    good = collide_bgk<D, INC>(f, args.inv_tau);
+  } else {
+    good = apply_boundary<D, INC>(f, type, (info >> 26) & 1u, args.bc);
+  }
+  if (!good) atomicMin(args.failed, static_cast<unsigned long long>(*args.step_base + args.rel + 1));
+#pragma unroll
+  for (int i = 0; i < Q; ++i) st_stream(wr + i * n_tn, f[i]);
+}
+
+// Advances the step counter the failure stamps are relative to (one per enqueued batch).
+__global__ void bump_kernel(long long* step_base, long long by) { *step_base += by; }
+
+// ---------------------------------------------------------------------------------------------
+// Gather words (see file header). Mirrors the blocked test of the sweep (engine.hpp:485-500).
+template <int D>
+__global__ void node_info_kernel(NodeInfoArgs args) {
+  constexpr int Q = Lat<D>::Q;
+  const int a = args.a;
+  const int az = D == 3 ? a : 1;
+  const int n_tn = a * a * az;
+  const uint64_t node = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (node >= args.n_stored * n_tn) return;
+  const uint64_t t = node / n_tn;
+  const int p = static_cast<int>(node % n_tn);
+  const uint8_t own_byte = args.types[node];
+  const int type = own_byte & 3;
+  uint32_t info = static_cast<uint32_t>(type) << 24;
+  if (own_byte & 4) info |= 1u << 26;
+  if (type == 0) {
+    if ((n_tn & 3) == 0) {
+      const uint8_t* grp = args.types + (node & ~static_cast<uint64_t>(3));
+      if ((grp[0] | grp[1] | grp[2] | grp[3]) & 3) info |= 1u << 27;
+    }
+    args.info[node] = info;
+    return;
+  }
+  const int lx = p % a, ly = (p / a) % a, lz = D == 3 ? p / (a * a) : 0;
+  for (int i = 0; i < Q; ++i) {
+    int sx = lx - ex<D>(i), sy = ly - ey<D>(i), sz = lz - ez<D>(i);
+    int dx = 0, dy = 0, dz = 0;
+    if (sx < 0) { dx = -1; sx += a; } else if (sx >= a) { dx = 1; sx -= a; }
+    if (sy < 0) { dy = -1; sy += a; } else if (sy >= a) { dy = 1; sy -= a; }
+    if (D == 3) {
+      if (sz < 0) { dz = -1; sz += a; } else if (sz >= a) { dz = 1; sz -= a; }
+    }
+    const int delta = (dx + 1) + 3 * ((dy + 1) + 3 * (dz + 1));
+    const int sp = sx + a * (sy + a * sz);
+    bool blocked;
+    if (delta == 13) {
+      blocked = (args.types[t * n_tn + sp] & 3) == 0;
+    } else {
+      const uint32_t s = args.nb[t * 27 + delta];
+      // a neighbour outside the stored range (slab mode edge) counts as EMPTY
+      blocked = s == kEmpty || (args.types[static_cast<uint64_t>(s) * n_tn + sp] & 3) == 0;
+    }
+    if (blocked) info |= 1u << i;
+  }
+  args.info[node] = info;
+}
+
+// ---------------------------------------------------------------------------------------------
+// TileEngineT2C::initialize (engine.hpp:336-352): equilibrium of per-node (rho, u) into both copies.
+template <int D, bool INC>
+__global__ void init_kernel(InitArgs args) {
+  constexpr int Q = Lat<D>::Q;
+  const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= args.count) return;
+  const uint64_t node = args.node0 + k;
+  const uint64_t t = node / args.n_tn;
+  const int p = static_cast<int>(node % args.n_tn);
+  double rho, u0, u1, u2;
+  if (args.rho) {
+    rho = args.rho[k];
+    u0 = args.ux[k];
+    u1 = args.uy[k];
+    u2 = args.uz[k];
+  } else {
+    rho = args.rho0;
+    u0 = args.u0[0];
+    u1 = args.u0[1];
+    u2 = args.u0[2];
+  }
+  if (!INC && !(rho > 0.0)) atomicOr(args.domain_error, 1);  // lattice.hpp:76-78
+  double f[Q];
+  equilibrium<D, INC>(rho, u0, u1, u2, f);
+  const uint64_t base = t * static_cast<uint64_t>(Q) * args.n_tn + p;
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    args.pdf0[base + static_cast<uint64_t>(i) * args.n_tn] = f[i];
+    args.pdf1[base + static_cast<uint64_t>(i) * args.n_tn] = f[i];
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// moments<T> per stored tile node (lattice.hpp:94-112), tile-node order; solid nodes -> 0.
+template <int D, bool INC>
+__global__ void moments_kernel(MomentsArgs args) {
+  constexpr int Q = Lat<D>::Q;
+  const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= args.count) return;
+  const uint64_t node = args.node0 + k;
+  const uint64_t t = node / args.n_tn;
+  const int p = static_cast<int>(node % args.n_tn);
+  const int type = (args.info[node] >> 24) & 3;
+  double r = 0.0, m0 = 0.0, m1 = 0.0, m2 = 0.0;
+  if (type != 0) {
+    double f[Q];
+    const double* src = args.pdf + t * static_cast<uint64_t>(Q) * args.n_tn + p;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) f[i] = src[static_cast<uint64_t>(i) * args.n_tn];
+    r = density<D>(f);
+    m0 = momentum<D, 0>(f);
+    m1 = momentum<D, 1>(f);
+    m2 = momentum<D, 2>(f);
+    if (!INC) {
+      if (r == 0.0) {
+        atomicOr(args.domain_error, 1);  // lattice.hpp:105-108
+      } else {
+        m0 = ddiv(m0, r);
+        m1 = ddiv(m1, r);
+        m2 = ddiv(m2, r);
+      }
+    }
+  }
+  args.rho[k] = r;
+  args.ux[k] = m0;
+  args.uy[k] = m1;
+  args.uz[k] = m2;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Deterministic reduction over owned non-solid nodes: fixed per-block tree, then one block.
+template <int D, bool INC>
+__global__ void __launch_bounds__(kThreads) reduce_partial_kernel(ReduceArgs args) {
+  constexpr int Q = Lat<D>::Q;
+  __shared__ double s_mass[kThreads];
+  __shared__ double s_umax[kThreads];
+  __shared__ double s_bad[kThreads];
+  double mass = 0.0, umax = 0.0, bad = 0.0;
+  const uint64_t n = args.n_nodes;
+  for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x; k < n;
+       k += static_cast<uint64_t>(gridDim.x) * kThreads) {
+    const uint64_t node = args.node0 + k;
+    const int type = (args.info[node] >> 24) & 3;
+    if (type == 0) continue;
+    const uint64_t t = node / args.n_tn;
+    const int p = static_cast<int>(node % args.n_tn);
+    double f[Q];
+    const double* src = args.pdf + t * static_cast<uint64_t>(Q) * args.n_tn + p;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) f[i] = src[static_cast<uint64_t>(i) * args.n_tn];
+    const double r = density<D>(f);
+    double u0 = momentum<D, 0>(f), u1 = momentum<D, 1>(f), u2 = momentum<D, 2>(f);
+    if (!INC && r != 0.0) {
+      u0 = ddiv(u0, r);
+      u1 = ddiv(u1, r);
+      u2 = ddiv(u2, r);
+    }
+    const double sp = sqrt(sqnorm(u0, u1, u2));
+    if (!(isfinite(r) && isfinite(sp))) {
+      bad += 1.0;
+    } else {
+      mass += r;
+      umax = fmax(umax, sp);
+    }
+  }
+  s_mass[threadIdx.x] = mass;
+  s_umax[threadIdx.x] = umax;
+  s_bad[threadIdx.x] = bad;
+  __syncthreads();
+  for (int w = kThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      s_mass[threadIdx.x] += s_mass[threadIdx.x + w];
+      s_umax[threadIdx.x] = fmax(s_umax[threadIdx.x], s_umax[threadIdx.x + w]);
+      s_bad[threadIdx.x] += s_bad[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    args.partial[3 * blockIdx.x + 0] = s_mass[0];
+    args.partial[3 * blockIdx.x + 1] = s_umax[0];
+    args.partial[3 * blockIdx.x + 2] = s_bad[0];
+  }
+}
+
+__global__ void reduce_final_kernel(const double* partial, int n, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double m = 0.0, u = 0.0, b = 0.0;
+  for (int i = 0; i < n; ++i) {
+    m += partial[3 * i];
+    u = fmax(u, partial[3 * i + 1]);
+    b += partial[3 * i + 2];
+  }
+  out[0] = m;
+  out[1] = u;
+  out[2] = b;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Slab-mode halo faces: copy the lz == a-1 (high face) or lz == 0 (low face) layer of
+// the directions crossing that face, for a contiguous range of tiles, to/from a packed buffer.
+// Packed order: [tile k][direction j of the face set][a*a face nodes], all contiguous runs.
+template <int D>
+__global__ void halo_copy_kernel(HaloArgs args) {
+  constexpr int Q = Lat<D>::Q;
+  const int a = args.a;
+  const int n_tn = D == 3 ? a * a * a : a * a;
+  const int face = n_tn / a;  // one layer normal to the slab axis (z in 3D, y in 2D)
+  const uint64_t per_tile = static_cast<uint64_t>(args.n_dirs) * face;
+  const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= args.n_tiles * per_tile) return;
+  const uint64_t tk = k / per_tile;
+  const int rem = static_cast<int>(k % per_tile);
+  const int j = rem / face;
+  const int fnode = rem % face;
+  const int dir = args.dirs[j];
+  const uint64_t slot = ((args.tile0 + tk) * Q + dir) * static_cast<uint64_t>(n_tn) +
+                        static_cast<uint64_t>(args.layer) * face + fnode;
+  if (args.pack)
+    args.buf[k] = args.pdf[slot];
+  else
+    args.pdf[slot] = args.buf[k];
+}
+
+// ---------------------------------------------------------------------------------------------
+// Launchers (host side of this translation unit)
+template <int D, bool INC>
+static cudaError_t launch_step_d(const StepArgs& a, cudaStream_t st) {
+  const unsigned blocks = static_cast<unsigned>((a.n_nodes + kThreads - 1) / kThreads);
+  if (blocks == 0) return cudaSuccess;
+  switch (a.a) {
+    case 2: t2c_step_kernel<D, 2, INC><<<blocks, kThreads, 0, st>>>(a); break;
+    case 4: t2c_step_kernel<D, 4, INC><<<blocks, kThreads, 0, st>>>(a); break;
+    case 8: t2c_step_kernel<D, 8, INC><<<blocks, kThreads, 0, st>>>(a); break;
+    case 16:
+      if (D == 2) {
+        t2c_step_kernel<D, (D == 2 ? 16 : 0), INC><<<blocks, kThreads, 0, st>>>(a);
+        break;
+      }
+      [[fallthrough]];
+    default: t2c_step_kernel<D, 0, INC><<<blocks, kThreads, 0, st>>>(a); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_step(int d, bool inc, const StepArgs& a, cudaStream_t st) {
+  if (d == 2) return inc ? launch_step_d<2, true>(a, st) : launch_step_d<2, false>(a, st);
+  return inc ? launch_step_d<3, true>(a, st) : launch_step_d<3, false>(a, st);
+}
+
+cudaError_t launch_bump(long long* step_base, long long by, cudaStream_t st) {
+  bump_kernel<<<1, 1, 0, st>>>(step_base, by);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_node_info(int d, const NodeInfoArgs& a, cudaStream_t st) {
+  const int n_tn = a.a * a.a * (d == 3 ? a.a : 1);
+  const uint64_t n = a.n_stored * n_tn;
+  const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
+  if (blocks == 0) return cudaSuccess;
+  if (d == 2)
+    node_info_kernel<2><<<blocks, 256, 0, st>>>(a);
+  else
+    node_info_kernel<3><<<blocks, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init(int d, bool inc, const InitArgs& a, cudaStream_t st) {
+  const unsigned blocks = static_cast<unsigned>((a.count + 255) / 256);
+  if (blocks == 0) return cudaSuccess;
+  if (d == 2) {
+    if (inc) init_kernel<2, true><<<blocks, 256, 0, st>>>(a);
+    else init_kernel<2, false><<<blocks, 256, 0, st>>>(a);
+  } else {
+    if (inc) init_kernel<3, true><<<blocks, 256, 0, st>>>(a);
+    else init_kernel<3, false><<<blocks, 256, 0, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_moments(int d, bool inc, const MomentsArgs& a, cudaStream_t st) {
+  const unsigned blocks = static_cast<unsigned>((a.count + 255) / 256);
+  if (blocks == 0) return cudaSuccess;
+  if (d == 2) {
+    if (inc) moments_kernel<2, true><<<blocks, 256, 0, st>>>(a);
+    else moments_kernel<2, false><<<blocks, 256, 0, st>>>(a);
+  } else {
+    if (inc) moments_kernel<3, true><<<blocks, 256, 0, st>>>(a);
+    else moments_kernel<3, false><<<blocks, 256, 0, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce(int d, bool inc, const ReduceArgs& a, int blocks, double* out,
+                          cudaStream_t st) {
+  if (d == 2) {
+    if (inc) reduce_partial_kernel<2, true><<<blocks, kThreads, 0, st>>>(a);
+    else reduce_partial_kernel<2, false><<<blocks, kThreads, 0, st>>>(a);
+  } else {
+    if (inc) reduce_partial_kernel<3, true><<<blocks, kThreads, 0, st>>>(a);
+    else reduce_partial_kernel<3, false><<<blocks, kThreads, 0, st>>>(a);
+  }
+  reduce_final_kernel<<<1, 32, 0, st>>>(a.partial, blocks, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_halo(int d, const HaloArgs& a, cudaStream_t st) {
+  const uint64_t n = a.n_tiles * static_cast<uint64_t>(a.n_dirs) * (d == 3 ? a.a * a.a : a.a);
+  const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
+  if (blocks == 0) return cudaSuccess;
+  if (d == 2)
+    halo_copy_kernel<2><<<blocks, 256, 0, st>>>(a);
+  else
+    halo_copy_kernel<3><<<blocks, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace splbm_dev

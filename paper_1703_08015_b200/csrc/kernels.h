@@ -1,0 +1,88 @@
+// Launch interface between the host runtime (engine.cpp) and the sm_100a kernels (kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "lattice.cuh"
+
+namespace splbm_dev {
+
+struct StepArgs {
+  const double* read;
+  double* write;
+  const uint32_t* info;  // per stored tile node gather word
+  const uint32_t* nb;    // stored tiles x 27, local indices
+  uint64_t t0;           // first stepped tile (stored index)
+  uint64_t n_nodes;      // stepped tiles * n_tn
+  int a;
+  double inv_tau;
+  BcParams bc;
+  unsigned long long* failed;  // min failing step number (ULLONG_MAX = none)
+  const long long* step_base;  // steps completed before this batch
+  int rel;                     // step index within the batch
+};
+
+struct NodeInfoArgs {
+  const uint8_t* types;  // stored tiles x n_tn: bits 0-1 NodeType, bit 2 bc_degenerate
+  const uint32_t* nb;
+  uint32_t* info;
+  uint64_t n_stored;
+  int a;
+};
+
+struct InitArgs {
+  double* pdf0;
+  double* pdf1;
+  const double* rho;  // nullptr -> uniform (rho0, u0)
+  const double* ux;
+  const double* uy;
+  const double* uz;
+  double rho0;
+  double u0[3];
+  uint64_t node0, count;
+  int n_tn;
+  int* domain_error;
+};
+
+struct MomentsArgs {
+  const double* pdf;
+  const uint32_t* info;
+  double* rho;
+  double* ux;
+  double* uy;
+  double* uz;
+  uint64_t node0, count;
+  int n_tn;
+  int* domain_error;
+};
+
+struct ReduceArgs {
+  const double* pdf;
+  const uint32_t* info;
+  uint64_t node0, n_nodes;
+  int n_tn;
+  double* partial;  // 3 per block
+};
+
+struct HaloArgs {
+  double* pdf;
+  double* buf;
+  uint64_t tile0, n_tiles;
+  int a;
+  int layer;  // local coordinate along the slab axis of the face layer
+  int n_dirs;
+  const int* dirs;  // device array of direction indices
+  int pack;         // 1: pdf -> buf, 0: buf -> pdf
+};
+
+cudaError_t launch_step(int d, bool inc, const StepArgs& a, cudaStream_t st);
+cudaError_t launch_bump(long long* step_base, long long by, cudaStream_t st);
+cudaError_t launch_node_info(int d, const NodeInfoArgs& a, cudaStream_t st);
+cudaError_t launch_init(int d, bool inc, const InitArgs& a, cudaStream_t st);
+cudaError_t launch_moments(int d, bool inc, const MomentsArgs& a, cudaStream_t st);
+cudaError_t launch_reduce(int d, bool inc, const ReduceArgs& a, int blocks, double* out,
+                          cudaStream_t st);
+cudaError_t launch_halo(int d, const HaloArgs& a, cudaStream_t st);
+
+}  // namespace splbm_dev

@@ -1,0 +1,202 @@
+// Lattice constants and the per-node physics of the T2C step, shared by all device kernels.
+//
+// Directions follow the reference order exactly (lattice.cpp:18-25 D2Q9, 33-42 D3Q19): rest,
+// axes, planar diagonals, opposite directions in adjacent pairs. Components are packed two bits
+// per direction so every lookup folds to an immediate in the unrolled loops.
+//
+// Arithmetic contract: every floating-point operation is an explicit
+// round-to-nearest intrinsic (__dadd_rn/__dmul_rn/__ddiv_rn) in the reference's operation order,
+// so nvcc cannot contract to FMA and results are bit-identical to the reference built with its
+// CMake Release flags. Products by a zero direction component are omitted: x + (+-0) == x for
+// x != 0 and a zero sum starts from +0, so the omitted terms never change a finite result (the
+// only difference is on states that already fail the step's finite check).
+#pragma once
+#include <cstdint>
+
+namespace splbm_dev {
+
+template <int D>
+struct Lat;
+
+// (e+1) packed 2 bits per direction, direction 0 in the low bits.
+__host__ __device__ constexpr uint64_t pack_dirs(const int* v, int q) {
+  uint64_t r = 0;
+  for (int i = q - 1; i >= 0; --i) r = (r << 2) | static_cast<uint64_t>(v[i] + 1);
+  return r;
+}
+
+template <>
+struct Lat<2> {
+  static constexpr int Q = 9;
+  static constexpr int ex_[9] = {0, 1, -1, 0, 0, 1, -1, 1, -1};
+  static constexpr int ey_[9] = {0, 0, 0, 1, -1, 1, -1, -1, 1};
+  static constexpr int ez_[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  static constexpr uint64_t EX = pack_dirs(ex_, 9);
+  static constexpr uint64_t EY = pack_dirs(ey_, 9);
+  static constexpr uint64_t EZ = pack_dirs(ez_, 9);
+  __host__ __device__ static constexpr double w(int i) {
+    return i == 0 ? 4.0 / 9.0 : (i <= 4 ? 1.0 / 9.0 : 1.0 / 36.0);
+  }
+};
+
+template <>
+struct Lat<3> {
+  static constexpr int Q = 19;
+  static constexpr int ex_[19] = {0, 1, -1, 0, 0, 0, 0, 1, -1, 1, -1, 1, -1, 1, -1, 0, 0, 0, 0};
+  static constexpr int ey_[19] = {0, 0, 0, 1, -1, 0, 0, 1, -1, -1, 1, 0, 0, 0, 0, 1, -1, 1, -1};
+  static constexpr int ez_[19] = {0, 0, 0, 0, 0, 1, -1, 0, 0, 0, 0, 1, -1, -1, 1, 1, -1, -1, 1};
+  static constexpr uint64_t EX = pack_dirs(ex_, 19);
+  static constexpr uint64_t EY = pack_dirs(ey_, 19);
+  static constexpr uint64_t EZ = pack_dirs(ez_, 19);
+  __host__ __device__ static constexpr double w(int i) {
+    return i == 0 ? 1.0 / 3.0 : (i <= 6 ? 1.0 / 18.0 : 1.0 / 36.0);
+  }
+};
+
+template <int D>
+__host__ __device__ constexpr int ex(int i) {
+  return static_cast<int>((Lat<D>::EX >> (2 * i)) & 3ull) - 1;
+}
+template <int D>
+__host__ __device__ constexpr int ey(int i) {
+  return static_cast<int>((Lat<D>::EY >> (2 * i)) & 3ull) - 1;
+}
+template <int D>
+__host__ __device__ constexpr int ez(int i) {
+  return static_cast<int>((Lat<D>::EZ >> (2 * i)) & 3ull) - 1;
+}
+// opposite pairs are adjacent (lattice.cpp:65-74 finds exactly this)
+__host__ __device__ constexpr int opp(int i) { return i == 0 ? 0 : ((i & 1) ? i + 1 : i - 1); }
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ bool finite(double v) { return isfinite(v); }
+
+// sum_i e_ik * f_i in direction order, zero components omitted (moments<T>, lattice.hpp:97-102)
+template <int D, int K>
+__device__ __forceinline__ double momentum(const double* f) {
+  double m = 0.0;
+#pragma unroll
+  for (int i = 0; i < Lat<D>::Q; ++i) {
+    const int e = K == 0 ? ex<D>(i) : (K == 1 ? ey<D>(i) : ez<D>(i));
+    if (e > 0) m = dadd(m, f[i]);
+    if (e < 0) m = dsub(m, f[i]);
+  }
+  return m;
+}
+
+template <int D>
+__device__ __forceinline__ double density(const double* f) {
+  double r = 0.0;
+#pragma unroll
+  for (int i = 0; i < Lat<D>::Q; ++i) r = dadd(r, f[i]);
+  return r;
+}
+
+// e_i . u in the order (e0 u0 + e1 u1) + e2 u2 with zero terms omitted (lattice.hpp:82)
+template <int D>
+__device__ __forceinline__ double edotu(int i, double u0, double u1, double u2) {
+  const int a = ex<D>(i), b = ey<D>(i), c = ez<D>(i);
+  double cu = 0.0;
+  bool first = true;
+  if (a != 0) {
+    cu = a > 0 ? u0 : -u0;
+    first = false;
+  }
+  if (b != 0) {
+    const double t = b > 0 ? u1 : -u1;
+    cu = first ? t : dadd(cu, t);
+    first = false;
+  }
+  if (c != 0) {
+    const double t = c > 0 ? u2 : -u2;
+    cu = first ? t : dadd(cu, t);
+  }
+  return cu;
+}
+
+// equilibrium<T> (lattice.hpp:72-91); uu = (u0^2 + u1^2) + u2^2 (oracle Eigen-shim order).
+template <int D, bool INC>
+__device__ __forceinline__ double feq(int i, double rho, double u0, double u1, double u2,
+                                      double uu) {
+  const double cu = edotu<D>(i, u0, u1, u2);
+  const double shape = dsub(dadd(dmul(cu, 3.0), dmul(dmul(cu, cu), 4.5)), dmul(uu, 1.5));
+  const double w = Lat<D>::w(i);
+  return INC ? dmul(w, dadd(rho, shape)) : dmul(dmul(w, rho), dadd(1.0, shape));
+}
+
+__device__ __forceinline__ double sqnorm(double u0, double u1, double u2) {
+  return dadd(dadd(dmul(u0, u0), dmul(u1, u1)), dmul(u2, u2));
+}
+
+template <int D, bool INC>
+__device__ __forceinline__ void equilibrium(double rho, double u0, double u1, double u2,
+                                            double* out) {
+  const double uu = sqnorm(u0, u1, u2);
+#pragma unroll
+  for (int i = 0; i < Lat<D>::Q; ++i) out[i] = feq<D, INC>(i, rho, u0, u1, u2, uu);
+}
+
+// CollisionOperator<T>::operator() BGK branch (collision.hpp:35-65). Returns
+// finite_moments(m) (engine.hpp:96-102); on a broken quasi-compressible density f is left
+// untouched and the step fails (collision.hpp:44-47).
+template <int D, bool INC>
+__device__ __forceinline__ bool collide_bgk(double* f, double inv_tau) {
+  const double rho = density<D>(f);
+  double u0 = momentum<D, 0>(f);
+  double u1 = momentum<D, 1>(f);
+  double u2 = momentum<D, 2>(f);
+  if (!INC) {
+    if (!(rho > 0.0) || !finite(rho)) return false;
+    u0 = ddiv(u0, rho);
+    u1 = ddiv(u1, rho);
+    u2 = ddiv(u2, rho);
+  }
+  const double uu = sqnorm(u0, u1, u2);
+#pragma unroll
+  for (int i = 0; i < Lat<D>::Q; ++i) {
+    const double fe = feq<D, INC>(i, rho, u0, u1, u2, uu);
+    f[i] = dadd(f[i], dmul(inv_tau, dsub(fe, f[i])));
+  }
+  return finite(rho) && finite(u0) && finite(u1) && finite(u2);
+}
+
+struct BcParams {
+  double u0, u1, u2;
+  double rho;
+};
+
+// apply_boundary<T> (engine.hpp:32-65). type 2 = VelocityBC, 3 = PressureBC.
+template <int D, bool INC>
+__device__ __forceinline__ bool apply_boundary(double* f, int type, bool rho_underdetermined,
+                                            const BcParams bc) {
+  if (type == 2) {
+    double rho = 1.0;
+    if (!rho_underdetermined) {
+      rho = density<D>(f);
+      if (!(rho > 0.0) || !finite(rho)) rho = 1.0;
+    }
+    equilibrium<D, INC>(rho, bc.u0, bc.u1, bc.u2, f);
+    return finite(rho) && finite(bc.u0) && finite(bc.u1) && finite(bc.u2);
+  }
+  const double rho = density<D>(f);
+  const double m0 = momentum<D, 0>(f), m1 = momentum<D, 1>(f), m2 = momentum<D, 2>(f);
+  double u0 = 0.0, u1 = 0.0, u2 = 0.0;
+  if (!INC) {
+    if (rho > 0.0) {
+      u0 = ddiv(m0, rho);
+      u1 = ddiv(m1, rho);
+      u2 = ddiv(m2, rho);
+    }
+  } else {
+    u0 = m0;
+    u1 = m1;
+    u2 = m2;
+  }
+  equilibrium<D, INC>(bc.rho, u0, u1, u2, f);
+  return finite(bc.rho) && finite(u0) && finite(u1) && finite(u2);
+}
+
+}  // namespace splbm_dev
