@@ -1,0 +1,314 @@
+#!/usr/bin/env python3
+"""Benchmark of the T2C time-step path on B200 (BASELINE.json metric: MLUPS (D3Q19 fp64 BGK) vs
+porosity; % of HBM peak GB/s; at 1/2/4/8 B200).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Workload at N=1: BASELINE configs[1], the D3Q19 BGK fp64 128^3 channel with bounce-back walls
+(velocity inlet / pressure outlet), tiles 4^3, synthetic geometry. A "step" is one LBM time step
+(one launch of the fused step kernel over all tiles). value = N_f * K / device time of the K
+timed steps (CUDA events on the engine stream, max over ranks). The two PDF copies (1.3 GB) are
+larger than L2, so no flush is needed between steps. Also reported: the MLUPS-vs-porosity sweep
+(configs[2]: RAS 256^3, d=40, seed 7, periodic), the roofline of the step kernel against the
+measured HBM copy peak, the CPU reference baseline, and an end-to-end number through the public
+API with host buffers.
+
+N>1 (torchrun, one process per GPU): weak scaling of the z-slab mode — every rank
+owns a 128^3-node channel slab of one (128 x 128 x 128*N) duct and exchanges tile-face halos with
+its neighbours over NCCL each step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+B_NODE = {2: 144.0, 3: 304.0}  # algorithmic bytes per node update, 2*q*8 (overhead.cpp:59-62)
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.samples = []
+        self._stop = threading.Event()
+        self.index = index
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                return
+            self._stop.wait(0.05)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 2 + k and s[2 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def load_ncu_traffic(workload):
+    """dram bytes per launch of the step kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_step_kernel.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    rec = d.get(workload)
+    return rec.get("dram_bytes_per_launch") if rec else None
+
+
+# ---------------------------------------------------------------------------------------------
+def channel_geometry(P, dims):
+    return P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=dims, inlet_speed=0.05,
+                                                                  outlet_density=1.0))
+
+
+def time_steps(eng, K, W, sampler_index=0):
+    """W warm-up steps, then exactly K timed steps in one device batch (events on the engine
+    stream, synchronised on both sides)."""
+    if W > 0:
+        ok, _ = eng.step_n(W)
+        assert ok, "non-finite state during warm-up"
+    eng.sync()
+    l0 = eng.launch_count()
+    with ClockSampler(sampler_index) as cs:
+        eng.step_async(K)
+        ok, failed = eng.sync()
+    assert ok, f"non-finite state at step {failed}"
+    ms = eng.last_batch_ms()
+    return ms, eng.launch_count() - l0, cs.summary()
+
+
+def porosity_sweep(P, K, W, peak):
+    out = []
+    for phi in (0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 1.0):
+        if phi < 1.0:
+            g = P.generate(P.GeometryKind.Ras3D, P.GenerateParams(
+                dims=(256, 256, 256), sphere_diameter=40, target_porosity=phi, seed=7))
+        else:
+            g = P.Geometry.filled(3, (256, 256, 256))
+        eng = P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8), (1, 1, 1))
+        eng.initialize_uniform(1.0, (0.01, 0.005, 0.0))
+        ms, _, _ = time_steps(eng, K, W)
+        nf = eng.fluid_nodes()
+        mlups = nf * K / (ms * 1e-3) / 1e6
+        gbs = mlups * 1e6 * B_NODE[3] / 1e9
+        out.append({"phi": round(P.porosity(g).phi, 4), "phi_t": round(eng.info.phi_t, 4),
+                    "tiles": int(eng.info.n_tiles), "fluid_nodes": nf, "mlups": round(mlups, 1),
+                    "achieved_gbs": round(gbs, 1), "frac_of_measured_peak": round(gbs / peak, 4),
+                    "bu_of_8tbs": round(gbs / 8000.0, 4)})
+        del eng
+    return out
+
+
+def e2e_public_api(P, g, steps):
+    """End to end through the public API with host buffers: NodeInit fields H2D from pinned host
+    memory, `steps` LBM steps (first-failure check), final (rho, u) fields + mass D2H."""
+    import torch
+    eng = P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8))
+    n = int(eng.info.n_tiles_stored) * eng.n_tn
+    pinned = [torch.empty(n, dtype=torch.float64, pin_memory=True).numpy() for _ in range(4)]
+    pinned[0][:] = 1.0
+    for a in pinned[1:]:
+        a[:] = 0.0
+    eng.initialize_arrays(*pinned)  # warm
+    eng.step_n(2)
+    eng.fields()
+    t0 = time.perf_counter()
+    eng.initialize_arrays(*pinned)
+    ok, failed = eng.step_n(steps)
+    f, mass = eng.fields(with_mass=True)
+    wall = time.perf_counter() - t0
+    assert ok and np.isfinite(mass)
+    nf = eng.fluid_nodes()
+    h2d = 4 * n * 8
+    d2h = 4 * n * 8 + 8  # moments of every stored tile node + the failure stamp
+    return {"value": round(nf * steps / wall / 1e6, 1), "unit": "MLUPS",
+            "h2d_bytes_per_step": round(h2d / steps, 1), "d2h_bytes_per_step": round(d2h / steps, 1),
+            "steps": steps, "wall_s": round(wall, 4)}
+
+
+def cpu_baseline(P, dims, budget_s=15.0):
+    """The reference's own T2C engine (oracle/_ref, built from /root/reference) on all host cores,
+    on a bounded sample of the same workload (same geometry, fewer steps)."""
+    from oracle import ref as R
+    fast = R.available(fast=True) and _cpu_has_avx2()
+    if not R.available(fast=fast):
+        return None
+    threads = os.cpu_count() or 1
+    g = channel_geometry(P, dims)
+    rg = R.RefGeometry.from_raster(3, g.dims, g.types, g.bc.velocity, g.bc.density, fast=fast)
+    e = R.RefEngine(rg, "t2c", 4, 0.8, threads=threads)
+    e.initialize_uniform()
+    e.step(1)
+    probe = max(e.last_seconds, 1e-3)
+    steps = int(max(2, min(200, budget_s / probe)))
+    e.step(steps)
+    sec = e.last_seconds
+    nf = g.fluid_count()
+    return {"value": round(nf * steps / sec / 1e6, 2), "unit": "MLUPS", "cores": threads,
+            "kind": "reference",
+            "sample": f"{steps} T2C steps of the {dims[0]}x{dims[1]}x{dims[2]} channel "
+                      f"({'-march=x86-64-v3' if fast else '-O3'} build of /root/reference sources, "
+                      f"ThreadPool({threads}))",
+            "seconds": round(sec, 3)}
+
+
+def _cpu_has_avx2():
+    try:
+        flags = open("/proc/cpuinfo").read()
+        return " avx2" in flags and " fma" in flags
+    except OSError:
+        return False
+
+
+# ---------------------------------------------------------------------------------------------
+def run_reference_arm(args):
+    """--impl reference: the reference's own CPU T2C implementation (oracle/_ref) on the host cores,
+    same metric/config; rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import paper_1703_08015_b200 as P
+    from oracle import ref as R
+    dims = (128, 128, 128)
+    fast = R.available(fast=True) and _cpu_has_avx2()
+    if not R.available(fast=fast):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return 0
+    threads = os.cpu_count() or 1
+    g = channel_geometry(P, dims)
+    rg = R.RefGeometry.from_raster(3, g.dims, g.types, g.bc.velocity, g.bc.density, fast=fast)
+    e = R.RefEngine(rg, "t2c", 4, 0.8, threads=threads)
+    e.initialize_uniform()
+    e.step(max(args.warmup, 1))
+    times = []
+    for _ in range(args.steps):
+        e.step(1)
+        times.append(e.last_seconds)
+    sec = float(np.sum(times))
+    nf = g.fluid_count()
+    mlups = nf * args.steps / sec / 1e6
+    line = {"metric": "MLUPS (D3Q19 fp64 BGK) vs porosity; % of HBM peak GB/s; at 1/2/4/8 B200",
+            "value": round(mlups, 2), "unit": "MLUPS", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(sec / args.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": "D3Q19 BGK fp64 channel 128^3, bounce-back walls, tiles 4^3",
+                       "lattice": "D3Q19", "tile": 4, "fluid_nodes": nf},
+            "cpu_baseline": {"value": round(mlups, 2), "unit": "MLUPS", "cores": threads,
+                             "kind": "reference",
+                             "sample": f"{args.steps} steps of the full 128^3 channel, "
+                                       f"TileEngineT2C<double> + ThreadPool({threads})"},
+            "e2e": {"value": round(mlups, 2), "unit": "MLUPS", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args):
+    import paper_1703_08015_b200 as P
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.gpus > 1:
+        from paper_1703_08015_b200 import slab
+        return slab.bench_main(args, P)
+    peak, peak_kind = measured_peaks()
+    K, W = args.steps, args.warmup
+    dims = (128, 128, 128)
+    g = channel_geometry(P, dims)
+    eng = P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8))
+    eng.initialize_uniform()
+    ms, launches, clocks = time_steps(eng, K, W)
+    nf = eng.fluid_nodes()
+    mlups = nf * K / (ms * 1e-3) / 1e6
+    step_ms = ms / K
+    alg_bytes = nf * B_NODE[3]
+    achieved = alg_bytes / (step_ms * 1e-3) / 1e9
+    workload = "channel3d_128"
+    line = {
+        "metric": "MLUPS (D3Q19 fp64 BGK) vs porosity; % of HBM peak GB/s; at 1/2/4/8 B200",
+        "value": round(mlups, 1), "unit": "MLUPS", "n_gpus": 1, "steps": K, "warmup": W,
+        "ms_per_step": round(step_ms, 5), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "D3Q19 BGK fp64 channel 128^3 (BASELINE configs[1]), bounce-back "
+                               "walls, V inlet / P outlet, tiles 4^3, quasi-compressible, tau 0.8",
+                   "fluid_nodes": nf, "tiles": int(eng.info.n_tiles),
+                   "phi_t": round(eng.info.phi_t, 4),
+                   "l2": "inputs > L2 (two PDF copies of 1.3 GB); no flush",
+                   "parallelism": "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "peak_source": peak_kind,
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "traffic": load_ncu_traffic(workload)},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    del eng
+    if not args.no_sweep:
+        line["porosity_sweep"] = porosity_sweep(P, min(K, 50), max(W, 3), peak)
+    line["e2e"] = e2e_public_api(P, g, 1000)
+    if not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(P, dims)
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

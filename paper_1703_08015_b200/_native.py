@@ -13,7 +13,7 @@ import numpy as np
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsplbm_b200.so")
+LIB_PATH = os.environ.get("SPLBM_LIB") or os.path.join(_HERE, "libsplbm_b200.so")
 
 _dp = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
 _u8 = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")

@@ -37,27 +37,32 @@ def _newer(target: str, deps: list[str]) -> bool:
     return all(os.path.getmtime(d) <= t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines: list[str] | None = None,
+          lib: str | None = None, build_dir: str | None = None) -> str:
+    """Compile the sources; `defines`/`lib`/`build_dir` build an experiment variant elsewhere."""
+    out_lib = lib or LIB
+    bdir = build_dir or BUILD
+    os.makedirs(bdir, exist_ok=True)
+    extra = [f"-D{d}" for d in (defines or [])]
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "splbm_b200.h")]
     objs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src + ".o")
+        o = os.path.join(bdir, src + ".o")
         objs.append(o)
         if not force and _newer(o, [s] + hdrs):
             continue
-        cmd = [nvcc()] + NVCC_FLAGS + ["-c", s, "-o", o]
+        cmd = [nvcc()] + NVCC_FLAGS + extra + ["-c", s, "-o", o]
         if src.endswith(".cpp"):
-            cmd = [nvcc()] + NVCC_FLAGS + ["-x", "cu", "-c", s, "-o", o]
+            cmd = [nvcc()] + NVCC_FLAGS + extra + ["-x", "cu", "-c", s, "-o", o]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
-    if force or not _newer(LIB, objs):
-        tmp = LIB + ".tmp"
+    if force or not _newer(out_lib, objs):
+        tmp = out_lib + ".tmp"
         subprocess.run([nvcc()] + ARCH + ["-shared", "-o", tmp] + objs + ["-lpthread"], check=True)
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, out_lib)
+    return out_lib
 
 
 if __name__ == "__main__":

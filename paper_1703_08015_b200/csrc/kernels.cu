@@ -22,9 +22,19 @@ namespace splbm_dev {
 
 constexpr uint32_t kEmpty = 0xffffffffu;
 constexpr int kThreads = 256;
+#ifndef SPLBM_MINB3
+#define SPLBM_MINB3 4  // resident CTAs per SM the 3D step kernel is register-budgeted for
+#endif
+#ifndef SPLBM_STORE_CS
+#define SPLBM_STORE_CS 1  // evict-first stores: the written copy is not re-read this step
+#endif
 
 __device__ __forceinline__ void st_stream(double* p, double v) {
+#if SPLBM_STORE_CS
   asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+#else
+  *p = v;
+#endif
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -97,6 +107,80 @@ __global__ void __launch_bounds__(kThreads) t2c_step_kernel(StepArgs args) {
   if (!good) atomicMin(args.failed, static_cast<unsigned long long>(*args.step_base + args.rel + 1));
 #pragma unroll
   for (int i = 0; i < Q; ++i) st_stream(wr + i * n_tn, f[i]);
+}
+
+// Fast path for power-of-two tiles of at most 256 nodes (a = 4 in 3D, a <= 16 in 2D): a CTA owns
+// kThreads / n_tn whole tiles. The 27 neighbour-tile base pointers of each tile are staged in
+// shared memory once per CTA (one coalesced read of nb, overlapped with the gather-word load), so
+// the per-direction source address is pure integer arithmetic on compile-time lattice constants
+// plus one shared-memory lookup and two selects — no divergent branches, no dependent global load
+// before the PDF gather.
+template <int D, int LOGA, bool INC>
+__global__ void __launch_bounds__(kThreads, (D == 3 ? SPLBM_MINB3 : 5)) t2c_step_pow2_kernel(StepArgs args) {
+  constexpr int Q = Lat<D>::Q;
+  constexpr int A = 1 << LOGA;
+  constexpr int NTN = D == 3 ? A * A * A : A * A;
+  constexpr int TILES = kThreads / NTN;
+  constexpr uint64_t STRIDE = static_cast<uint64_t>(Q) * NTN;
+  __shared__ const double* s_base[TILES][27];
+
+  const uint64_t n_tiles = args.n_nodes / NTN;
+  const uint64_t tile_blk = static_cast<uint64_t>(blockIdx.x) * TILES;
+  for (int k = threadIdx.x; k < TILES * 27; k += kThreads) {
+    const int tl = k / 27, dd = k % 27;
+    const uint64_t tt = tile_blk + tl;
+    const double* b = nullptr;
+    if (tt < n_tiles) {
+      const uint32_t s = __ldg(args.nb + (args.t0 + tt) * 27 + dd);
+      b = s == kEmpty ? nullptr : args.read + static_cast<uint64_t>(s) * STRIDE;
+    }
+    s_base[tl][dd] = b;
+  }
+  const int tl = threadIdx.x / NTN;
+  const int p = threadIdx.x % NTN;
+  const uint64_t tloc = tile_blk + tl;
+  const bool live = tloc < n_tiles;
+  const uint64_t t = args.t0 + tloc;
+  const uint32_t info = live ? __ldg(args.info + t * NTN + p) : 0u;
+  __syncthreads();
+  const int type = (info >> 24) & 3;
+  double* wr = args.write + t * STRIDE + p;
+  if (type == 0) {
+    if (info & (1u << 27)) {
+#pragma unroll
+      for (int i = 0; i < Q; ++i) st_stream(wr + i * NTN, 0.0);
+    }
+    return;
+  }
+  const int lx = p & (A - 1);
+  const int ly = (p >> LOGA) & (A - 1);
+  const int lz = D == 3 ? (p >> (2 * LOGA)) : 0;
+  const double* own = args.read + t * STRIDE;
+  const double* const* nbp = s_base[tl];
+
+  double f[Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    const int vx = lx - ex<D>(i), vy = ly - ey<D>(i), vz = lz - ez<D>(i);
+    const int dx = ex<D>(i) ? (vx >> LOGA) : 0;  // arithmetic shift: -1, 0 or +1
+    const int dy = ey<D>(i) ? (vy >> LOGA) : 0;
+    const int dz = (D == 3 && ez<D>(i)) ? (vz >> LOGA) : 0;
+    const int sp = (vx & (A - 1)) | ((vy & (A - 1)) << LOGA) | (D == 3 ? ((vz & (A - 1)) << (2 * LOGA)) : 0);
+    const int delta = 13 + dx + 3 * dy + 9 * dz;
+    const double* src = (delta == 13 ? own : nbp[delta]) + (i * NTN + sp);
+    const double* bb = own + (opp(i) * NTN + p);  // half-way bounce-back (engine.hpp:498-500)
+    f[i] = __ldg(((info >> i) & 1u) ? bb : src);
+  }
+
+  bool good;
+  if (type == 1) {
+    good = collide_bgk<D, INC>(f, args.inv_tau);
+  } else {
+    good = apply_boundary<D, INC>(f, type, (info >> 26) & 1u, args.bc);
+  }
+  if (!good) atomicMin(args.failed, static_cast<unsigned long long>(*args.step_base + args.rel + 1));
+#pragma unroll
+  for (int i = 0; i < Q; ++i) st_stream(wr + i * NTN, f[i]);
 }
 
 // Advances the step counter the failure stamps are relative to (one per enqueued batch).
@@ -316,21 +400,34 @@ __global__ void halo_copy_kernel(HaloArgs args) {
 
 // ---------------------------------------------------------------------------------------------
 // Launchers (host side of this translation unit)
+template <int D, int LOGA, bool INC>
+static void launch_pow2(const StepArgs& a, cudaStream_t st) {
+  constexpr int NTN = D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA));
+  constexpr int TILES = kThreads / NTN;
+  const uint64_t tiles = a.n_nodes / NTN;
+  const unsigned blocks = static_cast<unsigned>((tiles + TILES - 1) / TILES);
+  t2c_step_pow2_kernel<D, LOGA, INC><<<blocks, kThreads, 0, st>>>(a);
+}
+
 template <int D, bool INC>
 static cudaError_t launch_step_d(const StepArgs& a, cudaStream_t st) {
   const unsigned blocks = static_cast<unsigned>((a.n_nodes + kThreads - 1) / kThreads);
   if (blocks == 0) return cudaSuccess;
-  switch (a.a) {
-    case 2: t2c_step_kernel<D, 2, INC><<<blocks, kThreads, 0, st>>>(a); break;
-    case 4: t2c_step_kernel<D, 4, INC><<<blocks, kThreads, 0, st>>>(a); break;
-    case 8: t2c_step_kernel<D, 8, INC><<<blocks, kThreads, 0, st>>>(a); break;
-    case 16:
-      if (D == 2) {
-        t2c_step_kernel<D, (D == 2 ? 16 : 0), INC><<<blocks, kThreads, 0, st>>>(a);
-        break;
-      }
-      [[fallthrough]];
-    default: t2c_step_kernel<D, 0, INC><<<blocks, kThreads, 0, st>>>(a); break;
+  if constexpr (D == 3) {
+    switch (a.a) {
+      case 2: launch_pow2<D, 1, INC>(a, st); break;
+      case 4: launch_pow2<D, 2, INC>(a, st); break;
+      case 8: t2c_step_kernel<D, 8, INC><<<blocks, kThreads, 0, st>>>(a); break;
+      default: t2c_step_kernel<D, 0, INC><<<blocks, kThreads, 0, st>>>(a); break;
+    }
+  } else {
+    switch (a.a) {
+      case 2: launch_pow2<D, 1, INC>(a, st); break;
+      case 4: launch_pow2<D, 2, INC>(a, st); break;
+      case 8: launch_pow2<D, 3, INC>(a, st); break;
+      case 16: launch_pow2<D, 4, INC>(a, st); break;
+      default: t2c_step_kernel<D, 0, INC><<<blocks, kThreads, 0, st>>>(a); break;
+    }
   }
   return cudaGetLastError();
 }
