@@ -119,6 +119,7 @@ typedef struct {
   uint64_t device_bytes;   /* HBM held by the engine */
   double phi_t;            /* tile porosity (tiling.cpp:223-225) */
   double ratio_tiles;      /* cells / non-empty tiles (tiling.cpp:227) */
+  uint64_t n_tiles_global; /* non-empty tiles of the whole tile map */
 } splbm_dev_info;
 
 /* TileEngineT2C(g, a, model, periodic) ctor (engine.hpp:314-334): validates like the reference

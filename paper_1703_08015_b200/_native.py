@@ -40,7 +40,8 @@ class DevInfo(C.Structure):
     _fields_ = [("n_tiles", C.c_uint64), ("n_tiles_stored", C.c_uint64), ("n_tn", C.c_int),
                 ("q", C.c_int), ("a", C.c_int), ("d", C.c_int), ("grid_dims", C.c_int * 3),
                 ("padded_dims", C.c_int * 3), ("fluid_nodes", C.c_uint64),
-                ("device_bytes", C.c_uint64), ("phi_t", C.c_double), ("ratio_tiles", C.c_double)]
+                ("device_bytes", C.c_uint64), ("phi_t", C.c_double), ("ratio_tiles", C.c_double),
+                ("n_tiles_global", C.c_uint64)]
 
 
 _lib = None

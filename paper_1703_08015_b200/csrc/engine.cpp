@@ -381,6 +381,7 @@ int splbm_dev_get_info(const splbm_dev_engine* e, splbm_dev_info* out) {
     out->phi_t = e->n_own ? static_cast<double>(e->fluid_nodes) / (static_cast<double>(e->n_own) * e->n_tn) : 0.0;
     const double cells = static_cast<double>(e->tm.grid_dims[0]) * e->tm.grid_dims[1] * e->tm.grid_dims[2];
     out->ratio_tiles = e->tm.n_tiles ? cells / static_cast<double>(e->tm.n_tiles) : 0.0;
+    out->n_tiles_global = e->tm.n_tiles;
   });
 }
 

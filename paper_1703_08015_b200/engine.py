@@ -91,7 +91,7 @@ class TileEngineT2C:
             tile_map = np.empty(T, np.uint32)
             _native.check(L.splbm_dev_get_tile_grid(self._h, _native.ptr(tile_map), None, None,
                                                     None, None))
-            nt = int(np.count_nonzero(tile_map != 0xFFFFFFFF))
+            nt = int(self.info.n_tiles_global)
             origins = np.empty(max(nt, 1) * 3, np.int32)
             types = np.empty(max(nt, 1) * self.n_tn, np.uint8)
             fc = np.empty(max(nt, 1), np.uint32)
