@@ -83,6 +83,25 @@ int splbm_count_tiles(const uint8_t* types, int d, const int dims[3], int a, int
 int splbm_build_tile_map(const uint8_t* types, int d, const int dims[3], int a, int periodic,
                          uint32_t* tile_map, int32_t* origins, uint8_t* tile_types,
                          uint32_t* fluid_count, uint32_t* nb);
+/* Non-empty tiles per tile plane along the last axis (z in 3D, y in 2D): the prefix sums give the
+ * contiguous compact-index range of every z-slab, used to balance slabs by tiles. */
+int splbm_plane_tile_counts(const uint8_t* types, int d, const int dims[3], int a, int periodic,
+                            uint64_t* counts_out);
+
+/* Slab layout of the multi-GPU mode for the owned tile planes [z0, z1): stored tiles are
+ * [low halo plane zl][owned][high halo plane zh] (zl/zh = -1 when absent). Optional outputs (may be
+ * NULL): the local 27-neighbour table (stored*27; tiles outside the stored set -> EMPTY) and the
+ * local tile node types (stored*n_tn; bits 0-1 NodeType, bit 2 bc_degenerate). This is exactly the
+ * table set splbm_dev_create builds for a slab engine. */
+typedef struct {
+  int axis, z0, z1, zl, zh;
+  uint64_t n_low, n_own, n_high;
+  uint64_t g_low0, g_own0, g_high0;
+  uint64_t send_low_tiles, send_high_tiles;
+} splbm_slab_layout_t;
+int splbm_slab_layout(const uint8_t* types, int d, const int dims[3], int a, int periodic, int z0,
+                      int z1, splbm_slab_layout_t* out, uint32_t* nb_local, uint8_t* types_local);
+
 /* degenerate_bc_mask (engine.hpp:110-140) over the raster. */
 int splbm_degenerate_bc_mask(const uint8_t* types, int d, const int dims[3], int periodic,
                              uint8_t* mask_out);

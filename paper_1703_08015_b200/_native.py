@@ -44,6 +44,14 @@ class DevInfo(C.Structure):
                 ("n_tiles_global", C.c_uint64)]
 
 
+class SlabLayout(C.Structure):
+    _fields_ = [("axis", C.c_int), ("z0", C.c_int), ("z1", C.c_int), ("zl", C.c_int),
+                ("zh", C.c_int), ("n_low", C.c_uint64), ("n_own", C.c_uint64),
+                ("n_high", C.c_uint64), ("g_low0", C.c_uint64), ("g_own0", C.c_uint64),
+                ("g_high0", C.c_uint64), ("send_low_tiles", C.c_uint64),
+                ("send_high_tiles", C.c_uint64)]
+
+
 _lib = None
 
 # every symbol include/splbm_b200.h declares (checked by tests/test_native_abi.py)
@@ -60,6 +68,9 @@ SIGNATURES = {
     "splbm_build_tile_map": ([_u8, C.c_int, _i32, C.c_int, C.c_int, _u32, _i32, _u8, _u32,
                               C.c_void_p], C.c_int),
     "splbm_degenerate_bc_mask": ([_u8, C.c_int, _i32, C.c_int, _u8], C.c_int),
+    "splbm_plane_tile_counts": ([_u8, C.c_int, _i32, C.c_int, C.c_int, _u64], C.c_int),
+    "splbm_slab_layout": ([_u8, C.c_int, _i32, C.c_int, C.c_int, C.c_int, C.c_int,
+                           C.POINTER(SlabLayout), C.c_void_p, C.c_void_p], C.c_int),
     "splbm_dev_create": ([C.POINTER(DevDesc), C.POINTER(_vp)], C.c_int),
     "splbm_dev_destroy": ([_vp], None),
     "splbm_dev_get_info": ([_vp, C.POINTER(DevInfo)], C.c_int),

@@ -209,77 +209,26 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
     if (has_p) throw domain_error("equilibrium requires rho > 0 for the quasi-compressible model");
   }
 
-  // ---- slab selection along the last axis -----------------------------------
-  const int ax = d == 3 ? 2 : 1;
-  const int L = tm.grid_dims[ax];
-  e->slab_axis = ax;
-  int z0 = desc->slab_z0, z1 = desc->slab_z1;
-  if (z0 == 0 && z1 == 0) z1 = L;
-  if (z0 < 0 || z1 > L || z0 >= z1) throw config_error("invalid slab range");
-  e->slab_z0 = z0;
-  e->slab_z1 = z1;
-  const uint64_t plane_cells = static_cast<uint64_t>(tm.grid_dims[0]) * (d == 3 ? tm.grid_dims[1] : 1);
-  // F(z): first compact index of plane z (tile_map is z-major, compact order preserved)
-  std::vector<uint64_t> F(static_cast<std::size_t>(L) + 1, 0);
-  for (int z = 0; z < L; ++z) {
-    uint64_t cnt = 0;
-    const uint32_t* row = tm.tile_map.data() + static_cast<uint64_t>(z) * plane_cells;
-    for (uint64_t c = 0; c < plane_cells; ++c) cnt += row[c] != kEmpty;
-    F[z + 1] = F[z] + cnt;
-  }
-  const bool whole = (z0 == 0 && z1 == L);
-  const bool per_ax = (e->periodic >> ax) & 1;
-  int zl = -1, zh = -1;
-  if (!whole) {
-    if (z0 > 0) zl = z0 - 1; else if (per_ax) zl = L - 1;
-    if (z1 < L) zh = z1; else if (per_ax) zh = 0;
-    if ((zl >= z0 && zl < z1) || (zh >= z0 && zh < z1) || (zl >= 0 && zl == zh))
-      throw config_error("slab too thick for its periodic halo planes");
-  }
-  e->g_own0 = F[z0];
-  e->n_own = F[z1] - F[z0];
-  e->g_low0 = zl >= 0 ? F[zl] : 0;
-  e->n_low = zl >= 0 ? F[zl + 1] - F[zl] : 0;
-  e->g_high0 = zh >= 0 ? F[zh] : 0;
-  e->n_high = zh >= 0 ? F[zh + 1] - F[zh] : 0;
-  e->n_stored = e->n_low + e->n_own + e->n_high;
-  e->send_low_tiles = whole ? 0 : F[z0 + 1] - F[z0];
-  e->send_high_tiles = whole ? 0 : F[z1] - F[z1 - 1];
-
-  auto to_local = [&](uint32_t g) -> uint32_t {
-    if (g == kEmpty) return kEmpty;
-    if (g >= e->g_own0 && g < e->g_own0 + e->n_own) return static_cast<uint32_t>(e->n_low + (g - e->g_own0));
-    if (e->n_low && g >= e->g_low0 && g < e->g_low0 + e->n_low) return static_cast<uint32_t>(g - e->g_low0);
-    if (e->n_high && g >= e->g_high0 && g < e->g_high0 + e->n_high)
-      return static_cast<uint32_t>(e->n_low + e->n_own + (g - e->g_high0));
-    return kEmpty;
-  };
-  auto global_of = [&](uint64_t s) -> uint64_t {
-    if (s < e->n_low) return e->g_low0 + s;
-    if (s < e->n_low + e->n_own) return e->g_own0 + (s - e->n_low);
-    return e->g_high0 + (s - e->n_low - e->n_own);
-  };
-
+  // ---- slab of tile planes along the last axis ---------------------------------
+  const SlabLayout sl = slab_layout(tm, desc->slab_z0, desc->slab_z1);
+  e->slab_axis = sl.axis;
+  e->slab_z0 = sl.z0;
+  e->slab_z1 = sl.z1;
+  e->n_low = sl.n_low;
+  e->n_own = sl.n_own;
+  e->n_high = sl.n_high;
+  e->g_low0 = sl.g_low0;
+  e->g_own0 = sl.g_own0;
+  e->g_high0 = sl.g_high0;
+  e->n_stored = sl.stored();
+  e->send_low_tiles = sl.send_low_tiles;
+  e->send_high_tiles = sl.send_high_tiles;
+  auto global_of = [&](uint64_t s) { return sl.global_of(s); };
   const uint64_t S = e->n_stored;
   const int n_tn = e->n_tn;
-  std::vector<uint32_t> nb_local(S * 27);
-  std::vector<uint8_t> types_local(S * n_tn);
-  parallel_for(S, [&](std::size_t b, std::size_t en) {
-    for (std::size_t s = b; s < en; ++s) {
-      const uint64_t g = global_of(s);
-      for (int k = 0; k < 27; ++k) nb_local[s * 27 + k] = to_local(nb_global[g * 27 + k]);
-      const int32_t* o = &tm.origins[3 * g];
-      for (int p = 0; p < n_tn; ++p) {
-        uint8_t t = tm.types[g * n_tn + p];
-        if (t == 2 || t == 3) {  // bc_degenerate(t, p) (engine.hpp:409-417)
-          const int x = o[0] + p % e->a, y = o[1] + (p / e->a) % e->a,
-                    z = o[2] + (d == 3 ? p / (e->a * e->a) : 0);
-          if (deg[raster_index(dims, x, y, z)]) t |= 4;
-        }
-        types_local[s * n_tn + p] = t;
-      }
-    }
-  }, 1024);
+  std::vector<uint32_t> nb_local;
+  std::vector<uint8_t> types_local;
+  slab_tables(tm, sl, nb_global, deg, nb_local, types_local);
   for (uint64_t s = e->n_low; s < e->n_low + e->n_own; ++s) e->fluid_nodes += tm.fluid_count[global_of(s)];
 
   // ---- device ------------------------------------------------------------------------------

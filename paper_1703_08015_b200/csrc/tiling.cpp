@@ -174,6 +174,81 @@ std::vector<uint8_t> degenerate_mask(const uint8_t* types, int d, const int* dim
   return mask;
 }
 
+std::vector<uint64_t> plane_tile_counts(const TileMap& tm) {
+  const int ax = tm.d == 3 ? 2 : 1;
+  const int L = tm.grid_dims[ax];
+  const uint64_t plane_cells = static_cast<uint64_t>(tm.grid_dims[0]) * (tm.d == 3 ? tm.grid_dims[1] : 1);
+  std::vector<uint64_t> cnt(static_cast<std::size_t>(L), 0);
+  for (int z = 0; z < L; ++z) {
+    const uint32_t* row = tm.tile_map.data() + static_cast<uint64_t>(z) * plane_cells;
+    for (uint64_t c = 0; c < plane_cells; ++c) cnt[z] += row[c] != kEmpty;
+  }
+  return cnt;
+}
+
+uint32_t SlabLayout::to_local(uint32_t g) const {
+  if (g == kEmpty) return kEmpty;
+  if (g >= g_own0 && g < g_own0 + n_own) return static_cast<uint32_t>(n_low + (g - g_own0));
+  if (n_low && g >= g_low0 && g < g_low0 + n_low) return static_cast<uint32_t>(g - g_low0);
+  if (n_high && g >= g_high0 && g < g_high0 + n_high)
+    return static_cast<uint32_t>(n_low + n_own + (g - g_high0));
+  return kEmpty;
+}
+
+SlabLayout slab_layout(const TileMap& tm, int z0, int z1) {
+  SlabLayout sl;
+  sl.axis = tm.d == 3 ? 2 : 1;
+  const int L = tm.grid_dims[sl.axis];
+  if (z0 == 0 && z1 == 0) z1 = L;
+  if (z0 < 0 || z1 > L || z0 >= z1) throw config_error("invalid slab range");
+  sl.z0 = z0;
+  sl.z1 = z1;
+  const std::vector<uint64_t> cnt = plane_tile_counts(tm);
+  std::vector<uint64_t> F(static_cast<std::size_t>(L) + 1, 0);  // first compact index of plane z
+  for (int z = 0; z < L; ++z) F[z + 1] = F[z] + cnt[z];
+  const bool whole = (z0 == 0 && z1 == L);
+  const bool per_ax = (tm.periodic >> sl.axis) & 1;
+  if (!whole) {
+    if (z0 > 0) sl.zl = z0 - 1; else if (per_ax) sl.zl = L - 1;
+    if (z1 < L) sl.zh = z1; else if (per_ax) sl.zh = 0;
+    if ((sl.zl >= z0 && sl.zl < z1) || (sl.zh >= z0 && sl.zh < z1) || (sl.zl >= 0 && sl.zl == sl.zh))
+      throw config_error("slab too thick for its periodic halo planes");
+  }
+  sl.g_own0 = F[z0];
+  sl.n_own = F[z1] - F[z0];
+  sl.g_low0 = sl.zl >= 0 ? F[sl.zl] : 0;
+  sl.n_low = sl.zl >= 0 ? F[sl.zl + 1] - F[sl.zl] : 0;
+  sl.g_high0 = sl.zh >= 0 ? F[sl.zh] : 0;
+  sl.n_high = sl.zh >= 0 ? F[sl.zh + 1] - F[sl.zh] : 0;
+  sl.send_low_tiles = whole ? 0 : F[z0 + 1] - F[z0];
+  sl.send_high_tiles = whole ? 0 : F[z1] - F[z1 - 1];
+  return sl;
+}
+
+void slab_tables(const TileMap& tm, const SlabLayout& sl, const std::vector<uint32_t>& nb_global,
+                 const std::vector<uint8_t>& deg, std::vector<uint32_t>& nb_local,
+                 std::vector<uint8_t>& types_local) {
+  const uint64_t S = sl.stored();
+  const int n_tn = tm.n_tn, a = tm.a;
+  nb_local.assign(S * 27, kEmpty);
+  types_local.assign(S * n_tn, 0);
+  parallel_for(S, [&](std::size_t b, std::size_t en) {
+    for (std::size_t s = b; s < en; ++s) {
+      const uint64_t g = sl.global_of(s);
+      for (int k = 0; k < 27; ++k) nb_local[s * 27 + k] = sl.to_local(nb_global[g * 27 + k]);
+      const int32_t* o = &tm.origins[3 * g];
+      for (int p = 0; p < n_tn; ++p) {
+        uint8_t t = tm.types[g * n_tn + p];
+        if (t == 2 || t == 3) {  // bc_degenerate(t, p) (engine.hpp:409-417)
+          const int x = o[0] + p % a, y = o[1] + (p / a) % a, z = o[2] + (tm.d == 3 ? p / (a * a) : 0);
+          if (deg[raster_index(tm.dims, x, y, z)]) t |= 4;
+        }
+        types_local[s * n_tn + p] = t;
+      }
+    }
+  }, 1024);
+}
+
 }  // namespace splbm_host
 
 using namespace splbm_host;
@@ -212,6 +287,44 @@ int splbm_build_tile_map(const uint8_t* types, int d, const int dims[3], int a, 
     if (nb) {
       const auto n = neighbour_table(tm);
       std::memcpy(nb, n.data(), n.size() * 4);
+    }
+  });
+}
+
+int splbm_plane_tile_counts(const uint8_t* types, int d, const int dims[3], int a, int periodic,
+                            uint64_t* counts_out) {
+  return guarded([&] {
+    const TileMap tm = build_tile_map(types, d, dims, a, periodic);
+    const auto c = plane_tile_counts(tm);
+    std::memcpy(counts_out, c.data(), c.size() * sizeof(uint64_t));
+  });
+}
+
+int splbm_slab_layout(const uint8_t* types, int d, const int dims[3], int a, int periodic, int z0,
+                      int z1, splbm_slab_layout_t* out, uint32_t* nb_local, uint8_t* types_local) {
+  return guarded([&] {
+    if (!out) throw config_error("null argument");
+    const TileMap tm = build_tile_map(types, d, dims, a, periodic);
+    const SlabLayout sl = slab_layout(tm, z0, z1);
+    out->axis = sl.axis;
+    out->z0 = sl.z0;
+    out->z1 = sl.z1;
+    out->zl = sl.zl;
+    out->zh = sl.zh;
+    out->n_low = sl.n_low;
+    out->n_own = sl.n_own;
+    out->n_high = sl.n_high;
+    out->g_low0 = sl.g_low0;
+    out->g_own0 = sl.g_own0;
+    out->g_high0 = sl.g_high0;
+    out->send_low_tiles = sl.send_low_tiles;
+    out->send_high_tiles = sl.send_high_tiles;
+    if (nb_local || types_local) {
+      std::vector<uint32_t> nbl;
+      std::vector<uint8_t> tl;
+      slab_tables(tm, sl, neighbour_table(tm), degenerate_mask(types, d, dims, periodic), nbl, tl);
+      if (nb_local) std::memcpy(nb_local, nbl.data(), nbl.size() * 4);
+      if (types_local) std::memcpy(types_local, tl.data(), tl.size());
     }
   });
 }

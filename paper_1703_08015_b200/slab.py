@@ -1,0 +1,256 @@
+"""Multi-GPU z-slab mode of the T2C path (the reference has no counterpart —
+multi-GPU is the paper's future work).
+
+The compact tile index is z-major, so a slab of tile planes is a contiguous tile range. Each rank
+(one process per GPU) owns a slab balanced by non-empty tiles, stores one halo plane on each side,
+and after every step exchanges the tile-face PDFs that cross its two slab faces:
+
+  upward:   my top plane, layer a-1, directions with e_axis = +1  -> upper rank's low halo plane
+  downward: my bottom plane, layer 0, directions with e_axis = -1 -> lower rank's high halo plane
+
+The transfers are NCCL point-to-point over NVLink (torch.distributed), enqueued on the engine's own
+CUDA stream so pack -> send/recv -> unpack -> next step are stream-ordered with no host sync. The
+per-node arithmetic is unchanged, so N-GPU results are bitwise equal to the 1-GPU run.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+
+import numpy as np
+
+from . import _native
+from .geometry import Geometry
+from .tiling import Periodicity
+
+
+def plane_tile_counts(g: Geometry, a: int, periodic=None) -> np.ndarray:
+    """Non-empty tiles per tile plane along the slab axis (z in 3D, y in 2D)."""
+    from .tiling import tile_dims
+    gd, _ = tile_dims(g.d, g.dims, a)
+    L = gd[2] if g.d == 3 else gd[1]
+    out = np.zeros(L, np.uint64)
+    _native.check(_native.lib().splbm_plane_tile_counts(
+        np.ascontiguousarray(g.types, np.uint8), g.d, np.asarray(g.dims, np.int32), a,
+        Periodicity.of(periodic).mask(), out))
+    return out
+
+
+def plan_slabs(counts, world: int) -> list[tuple[int, int]]:
+    """Contiguous plane ranges [z0, z1), one per rank, minimising the largest per-rank count of
+    non-empty tiles (equal z-extents would be load-imbalanced on sparse media). Linear partition:
+    binary search on the capacity with a greedy sweep, then split groups until every rank owns at
+    least one plane."""
+    counts = [int(c) for c in np.asarray(counts).ravel()]
+    L = len(counts)
+    if world < 1 or world > L:
+        raise ValueError(f"cannot split {L} tile planes over {world} ranks")
+
+    def greedy(cap):
+        cuts, load = [0], 0
+        for z, c in enumerate(counts):
+            if load + c > cap and z > cuts[-1]:
+                cuts.append(z)
+                load = 0
+            load += c
+        return cuts + [L]
+
+    lo, hi = max(counts + [0]), sum(counts)
+    while lo < hi:
+        mid = (lo + hi) // 2
+        if len(greedy(mid)) - 1 <= world:
+            hi = mid
+        else:
+            lo = mid + 1
+    cuts = greedy(lo)
+    while len(cuts) - 1 < world:  # split the heaviest multi-plane group at its balance point
+        groups = [(sum(counts[cuts[i]:cuts[i + 1]]), i) for i in range(len(cuts) - 1)
+                  if cuts[i + 1] - cuts[i] > 1]
+        _, i = max(groups)
+        a, b = cuts[i], cuts[i + 1]
+        half, acc, z = sum(counts[a:b]) / 2.0, 0, a + 1
+        for zz in range(a, b - 1):
+            acc += counts[zz]
+            z = zz + 1
+            if acc >= half:
+                break
+        cuts.insert(i + 1, z)
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+def slab_layout(g: Geometry, a: int, periodic, z0: int, z1: int, tables: bool = False):
+    """The stored-tile layout a slab engine builds (splbm_slab_layout)."""
+    L = _native.lib()
+    per = Periodicity.of(periodic)
+    lay = _native.SlabLayout()
+    types = np.ascontiguousarray(g.types, np.uint8)
+    dims = np.asarray(g.dims, np.int32)
+    _native.check(L.splbm_slab_layout(types, g.d, dims, a, per.mask(), z0, z1, C.byref(lay), None,
+                                      None))
+    out = {k: getattr(lay, k) for k, _ in _native.SlabLayout._fields_}
+    if tables:
+        S = lay.n_low + lay.n_own + lay.n_high
+        n_tn = a * a * (a if g.d == 3 else 1)
+        nb = np.empty(max(S, 1) * 27, np.uint32)
+        tt = np.empty(max(S, 1) * n_tn, np.uint8)
+        _native.check(L.splbm_slab_layout(types, g.d, dims, a, per.mask(), z0, z1, C.byref(lay),
+                                          _native.ptr(nb), _native.ptr(tt)))
+        out["nb_local"] = nb[:S * 27]
+        out["types_local"] = tt[:S * n_tn]
+    return out
+
+
+def neighbours(rank: int, world: int, periodic_axis: bool) -> tuple[int | None, int | None]:
+    """(lower, upper) ranks along the slab axis; None at a non-periodic domain edge."""
+    if world == 1:
+        return None, None
+    lower = rank - 1 if rank > 0 else (world - 1 if periodic_axis else None)
+    upper = rank + 1 if rank < world - 1 else (0 if periodic_axis else None)
+    return lower, upper
+
+
+class HaloExchange:
+    """Per-step face exchange. `comm.exchange(ops)` runs a batch of point-to-point operations
+    [(op, tensor, peer)], op in {"send", "recv"}, and returns when they are enqueued/complete.
+    Two batches (upward then downward) keep the send/recv matching unambiguous even when the
+    lower and upper neighbour are the same rank (two ranks, periodic axis)."""
+
+    def __init__(self, rank, world, periodic_axis, sizes, alloc, comm):
+        self.lower, self.upper = neighbours(rank, world, periodic_axis)
+        self.comm = comm
+        n = {k: int(v) // 8 for k, v in sizes.items()}
+        self.send_low = alloc(n["send_low"])
+        self.send_high = alloc(n["send_high"])
+        self.recv_low = alloc(n["recv_low"])
+        self.recv_high = alloc(n["recv_high"])
+
+    def exchange(self, pack, unpack):
+        pack(self.send_low, self.send_high)
+        up, down = [], []
+        if self.upper is not None and self.send_high.numel():
+            up.append(("send", self.send_high, self.upper))
+        if self.lower is not None and self.recv_low.numel():
+            up.append(("recv", self.recv_low, self.lower))
+        if self.lower is not None and self.send_low.numel():
+            down.append(("send", self.send_low, self.lower))
+        if self.upper is not None and self.recv_high.numel():
+            down.append(("recv", self.recv_high, self.upper))
+        for batch in (up, down):
+            if batch:
+                self.comm.exchange(batch)
+        unpack(self.recv_low if self.lower is not None else None,
+               self.recv_high if self.upper is not None else None)
+
+
+class TorchComm:
+    """torch.distributed point-to-point (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, stream=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.stream = stream
+
+    def exchange(self, ops):
+        import torch
+        dist = self.dist
+        p2p = [dist.P2POp(dist.isend if op == "send" else dist.irecv, t, peer) for op, t, peer in ops]
+        if self.stream is not None:
+            with torch.cuda.stream(self.stream):
+                for w in dist.batch_isend_irecv(p2p):
+                    w.wait()  # enqueues the completion on the engine stream (no host sync)
+        else:
+            for w in dist.batch_isend_irecv(p2p):
+                w.wait()
+
+
+class SlabRun:
+    """One rank of the multi-GPU slab mode: a slab TileEngineT2C + its NCCL halo exchange."""
+
+    def __init__(self, g: Geometry, a: int, model, periodic, rank: int, world: int, device: int,
+                 slabs=None):
+        import torch
+        from .engine import TileEngineT2C
+        per = Periodicity.of(periodic)
+        self.rank, self.world = rank, world
+        self.slabs = slabs or plan_slabs(plane_tile_counts(g, a, per), world)
+        z0, z1 = self.slabs[rank]
+        self.engine = TileEngineT2C(g, a, model, per, device=device,
+                                    slab=None if world == 1 else (z0, z1))
+        axis_periodic = per.axis(2 if g.d == 3 else 1)
+        self.stream = torch.cuda.ExternalStream(self.engine.stream_handle(), device=device)
+        dev = torch.device("cuda", device)
+        self.xchg = HaloExchange(rank, world, axis_periodic, self.engine.halo_bytes(),
+                                 lambda n: torch.empty(n, dtype=torch.float64, device=dev),
+                                 TorchComm(self.stream))
+
+    def _pack(self, lo, hi):
+        self.engine.halo_pack(lo.data_ptr() if lo.numel() else 0, hi.data_ptr() if hi.numel() else 0)
+
+    def _unpack(self, lo, hi):
+        self.engine.halo_unpack(lo.data_ptr() if lo is not None and lo.numel() else 0,
+                                hi.data_ptr() if hi is not None and hi.numel() else 0)
+
+    def step_async(self, n: int) -> None:
+        """n steps, each followed by the halo exchange; all stream-ordered on the engine stream."""
+        for _ in range(n):
+            self.engine.step_async(1)
+            if self.world > 1:
+                self.xchg.exchange(self._pack, self._unpack)
+
+    def sync(self):
+        return self.engine.sync()
+
+
+def bench_main(args, P) -> int:
+    """bench.py at N>1 (torchrun): weak scaling — each rank owns a 128^3-node slab of one
+    (128 x 128 x 128*N) D3Q19 channel; N_f*K summed over ranks / max-over-ranks device time."""
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    g = P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=(128, 128, 128 * world)))
+    L = g.dims[2] // 4
+    slabs = [(r * L // world, (r + 1) * L // world) for r in range(world)]
+    run = SlabRun(g, 4, P.FluidModel(tau=0.8), None, rank, world, local, slabs=slabs)
+    eng = run.engine
+    eng.initialize_uniform()
+    run.step_async(args.warmup)
+    run.sync()
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(run.stream):
+        start.record()
+    launches0 = eng.launch_count()
+    run.step_async(args.steps)
+    with torch.cuda.stream(run.stream):
+        stop.record()
+    ok, failed = run.sync()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([start.elapsed_time(stop)], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    nf = torch.tensor([float(eng.fluid_nodes())], device="cuda", dtype=torch.float64)
+    dist.all_reduce(nf)
+    ok_t = torch.tensor([1 if ok else 0], device="cuda")
+    dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        t = float(ms.item()) * 1e-3
+        mlups = float(nf.item()) * args.steps / t / 1e6
+        print(json.dumps({
+            "metric": "MLUPS (D3Q19 fp64 BGK) vs porosity; % of HBM peak GB/s; at 1/2/4/8 B200",
+            "value": round(mlups, 1), "unit": "MLUPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t / args.steps * 1e3, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "ok": bool(ok_t.item()),
+            "config": {"workload": f"D3Q19 BGK fp64 channel 128x128x{128 * world}, z-slab per GPU "
+                                   "(128^3 nodes each), NCCL tile-face halo exchange",
+                       "parallelism": f"zslab{world}", "fluid_nodes": int(nf.item())},
+            "gpu_launches": int(eng.launch_count() - launches0)}))
+    dist.destroy_process_group()
+    return 0

@@ -1,0 +1,78 @@
+"""Slab mode on one B200: several slab engines (the ranks) in one process exchange their face
+halos through device buffers; owned PDFs and fields stay bitwise equal to the single-engine run.
+This exercises the device halo pack/unpack kernels and the slab layout; the NCCL schedule itself
+is covered by tests/test_slab_cpu.py (gloo, world 2 and 3)."""
+import numpy as np
+import pytest
+
+import paper_1703_08015_b200 as P
+from paper_1703_08015_b200 import slab
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "ras48_periodic": (lambda: P.generate(P.GeometryKind.Ras3D, P.GenerateParams(
+        dims=(48, 48, 48), sphere_diameter=12, target_porosity=0.5, seed=2)), 4, 7),
+    "channel3d": (lambda: P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=(32, 24, 64))), 4, 0),
+    "channel2d": (lambda: P.generate(P.GeometryKind.Channel2D, P.GenerateParams(dims=(64, 128, 1))), 4, 0),
+    "full2d_periodic_a16": (lambda: P.Geometry.filled(2, (64, 128, 1)), 16, 3),
+}
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_slab_engines_match_whole(name, world):
+    import torch
+    from oracle import oracle as O
+    factory, a, per = CASES[name]
+    g = factory()
+    m = P.FluidModel(tau=0.8)
+    whole = P.TileEngineT2C(g, a, m, per)
+    whole.initialize(O.wavy)
+    slabs = slab.plan_slabs(slab.plane_tile_counts(g, a, per), world)
+    ranks = [P.TileEngineT2C(g, a, m, per, slab=s) for s in slabs]
+    for e in ranks:
+        e.initialize(O.wavy)
+    ax_per = P.Periodicity.of(per).axis(2 if g.d == 3 else 1)
+    buf = []
+    for e in ranks:
+        hb = e.halo_bytes()
+        buf.append({k: torch.zeros(max(v // 8, 1), dtype=torch.float64, device="cuda")
+                    for k, v in hb.items()})
+    K = 9
+    assert whole.step_n(K)[0]
+    for _ in range(K):
+        for r, e in enumerate(ranks):
+            e.step_async(1)
+            e.halo_pack(buf[r]["send_low"].data_ptr(), buf[r]["send_high"].data_ptr())
+        for e in ranks:
+            assert e.sync()[0]
+        for r, e in enumerate(ranks):
+            lo, hi = slab.neighbours(r, world, ax_per)
+            if lo is not None:
+                n = buf[r]["recv_low"].numel()
+                buf[r]["recv_low"][:n].copy_(buf[lo]["send_high"][:n])
+            if hi is not None:
+                n = buf[r]["recv_high"].numel()
+                buf[r]["recv_high"][:n].copy_(buf[hi]["send_low"][:n])
+        torch.cuda.synchronize()
+        for r, e in enumerate(ranks):
+            lo, hi = slab.neighbours(r, world, ax_per)
+            e.halo_unpack(buf[r]["recv_low"].data_ptr() if lo is not None else 0,
+                          buf[r]["recv_high"].data_ptr() if hi is not None else 0)
+    wf = whole.fields()
+    tg = whole.tile_grid()
+    st = whole.q * whole.n_tn
+    wp = whole.get_pdf()
+    rho = np.zeros_like(wf.rho)
+    for e in ranks:
+        lay = slab.slab_layout(g, a, per, e.info.n_tiles and slabs[ranks.index(e)][0],
+                               slabs[ranks.index(e)][1])
+        g0, n = lay["g_own0"], lay["n_own"]
+        mine = e.get_pdf()[lay["n_low"] * st:(lay["n_low"] + n) * st]
+        ref = wp[g0 * st:(g0 + n) * st]
+        fluid = np.broadcast_to((tg.types[g0:g0 + n] != 0)[:, None, :], (n, whole.q, whole.n_tn)).ravel()
+        assert np.array_equal(mine[fluid].view(np.uint64), ref[fluid].view(np.uint64))
+        f = e.fields()
+        rho += f.rho
+    assert np.array_equal(rho, wf.rho)
