@@ -208,6 +208,11 @@ int splbm_dev_halo_recv_bytes(const splbm_dev_engine* e, uint64_t* low_bytes, ui
 int splbm_dev_halo_pack(splbm_dev_engine* e, void* low_dev, void* high_dev);
 int splbm_dev_halo_unpack(splbm_dev_engine* e, const void* low_dev, const void* high_dev);
 
+/* ---- self-test ------------------------------------------------------------------------------- */
+/* Runs the step kernel's velocity division u_k = m_k / rho (collision.hpp:48) on the device for n
+ * (m0, m1, m2, rho) tuples; every quotient must equal IEEE division bit for bit. */
+int splbm_selftest_divide(uint64_t n, const double* m3, const double* rho, double* out3);
+
 #ifdef __cplusplus
 }
 #endif

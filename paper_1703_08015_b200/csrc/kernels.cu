@@ -25,6 +25,12 @@ constexpr int kThreads = 256;
 #ifndef SPLBM_MINB3
 #define SPLBM_MINB3 4  // resident CTAs per SM the 3D step kernel is register-budgeted for
 #endif
+#ifndef SPLBM_MINB2
+#define SPLBM_MINB2 6  // resident CTAs per SM the 2D step kernel is register-budgeted for
+#endif
+#ifndef SPLBM_ZERO_FILL
+#define SPLBM_ZERO_FILL 1  // write 0.0 to solid slots sharing a 32-B sector with fluid slots
+#endif
 #ifndef SPLBM_STORE_CS
 #define SPLBM_STORE_CS 1  // evict-first stores: the written copy is not re-read this step
 #endif
@@ -116,7 +122,7 @@ __global__ void __launch_bounds__(kThreads) t2c_step_kernel(StepArgs args) {
 // plus one shared-memory lookup and two selects — no divergent branches, no dependent global load
 // before the PDF gather.
 template <int D, int LOGA, bool INC>
-__global__ void __launch_bounds__(kThreads, (D == 3 ? SPLBM_MINB3 : 5)) t2c_step_pow2_kernel(StepArgs args) {
+__global__ void __launch_bounds__(kThreads, (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2)) t2c_step_pow2_kernel(StepArgs args) {
   constexpr int Q = Lat<D>::Q;
   constexpr int A = 1 << LOGA;
   constexpr int NTN = D == 3 ? A * A * A : A * A;
@@ -203,7 +209,7 @@ __global__ void node_info_kernel(NodeInfoArgs args) {
   uint32_t info = static_cast<uint32_t>(type) << 24;
   if (own_byte & 4) info |= 1u << 26;
   if (type == 0) {
-    if ((n_tn & 3) == 0) {
+    if (SPLBM_ZERO_FILL && (n_tn & 3) == 0) {
       const uint8_t* grp = args.types + (node & ~static_cast<uint64_t>(3));
       if ((grp[0] | grp[1] | grp[2] | grp[3]) & 3) info |= 1u << 27;
     }
@@ -292,9 +298,7 @@ __global__ void moments_kernel(MomentsArgs args) {
       if (r == 0.0) {
         atomicOr(args.domain_error, 1);  // lattice.hpp:105-108
       } else {
-        m0 = ddiv(m0, r);
-        m1 = ddiv(m1, r);
-        m2 = ddiv(m2, r);
+        divide3(m0, m1, m2, r);
       }
     }
   }
@@ -398,6 +402,17 @@ __global__ void halo_copy_kernel(HaloArgs args) {
     args.pdf[slot] = args.buf[k];
 }
 
+// Self-test of the shared-reciprocal division against IEEE division (tests/test_device_division.py).
+__global__ void divide_selftest_kernel(uint64_t n, const double* m, const double* rho, double* out) {
+  const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double a = m[3 * k], b = m[3 * k + 1], c = m[3 * k + 2];
+  divide3(a, b, c, rho[k]);
+  out[3 * k] = a;
+  out[3 * k + 1] = b;
+  out[3 * k + 2] = c;
+}
+
 // ---------------------------------------------------------------------------------------------
 // Launchers (host side of this translation unit)
 template <int D, int LOGA, bool INC>
@@ -490,6 +505,13 @@ cudaError_t launch_reduce(int d, bool inc, const ReduceArgs& a, int blocks, doub
     else reduce_partial_kernel<3, false><<<blocks, kThreads, 0, st>>>(a);
   }
   reduce_final_kernel<<<1, 32, 0, st>>>(a.partial, blocks, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_divide_selftest(uint64_t n, const double* m, const double* rho, double* out,
+                                   cudaStream_t st) {
+  const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
+  if (blocks) divide_selftest_kernel<<<blocks, 256, 0, st>>>(n, m, rho, out);
   return cudaGetLastError();
 }
 

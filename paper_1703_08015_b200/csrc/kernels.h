@@ -84,5 +84,7 @@ cudaError_t launch_moments(int d, bool inc, const MomentsArgs& a, cudaStream_t s
 cudaError_t launch_reduce(int d, bool inc, const ReduceArgs& a, int blocks, double* out,
                           cudaStream_t st);
 cudaError_t launch_halo(int d, const HaloArgs& a, cudaStream_t st);
+cudaError_t launch_divide_selftest(uint64_t n, const double* m, const double* rho, double* out,
+                                   cudaStream_t st);
 
 }  // namespace splbm_dev

@@ -74,6 +74,43 @@ __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a,
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 __device__ __forceinline__ bool finite(double v) { return isfinite(v); }
 
+#ifndef SPLBM_FAST_DIV
+#define SPLBM_FAST_DIV 1
+#endif
+
+// u_k = m_k / rho for the three momenta, each correctly rounded (IEEE division, as the reference
+// computes mom.u /= mom.rho, collision.hpp:48). Fast path: one correctly rounded reciprocal
+// y = RN(1/rho) shared by the three quotients, then Markstein's correction per quotient:
+//   q0 = RN(m*y) (within 1 ulp of m/rho), r = fma(-rho, q0, m) (exact), q = RN(q0 + r*y) = RN(m/rho)
+// (Markstein's theorem; Handbook of Floating-Point Arithmetic, Th. 8.10). It holds while no
+// intermediate leaves the normal range, which the exponent guard ensures; zeros keep their sign
+// via m*y; anything else takes the full IEEE division.
+__device__ __forceinline__ bool div_safe(double v) {
+  const double av = fabs(v);
+  return av == 0.0 || (av >= 0x1p-480 && av <= 0x1p480);
+}
+__device__ __forceinline__ void divide3(double& m0, double& m1, double& m2, double rho) {
+#if SPLBM_FAST_DIV
+  const double ar = fabs(rho);
+  if (ar >= 0x1p-480 && ar <= 0x1p480 && div_safe(m0) && div_safe(m1) && div_safe(m2)) {
+    const double y = __drcp_rn(rho);
+    auto q = [&](double m) {
+      const double q0 = __dmul_rn(m, y);
+      if (m == 0.0) return q0;
+      const double r = __fma_rn(-rho, q0, m);
+      return __fma_rn(r, y, q0);
+    };
+    m0 = q(m0);
+    m1 = q(m1);
+    m2 = q(m2);
+    return;
+  }
+#endif
+  m0 = ddiv(m0, rho);
+  m1 = ddiv(m1, rho);
+  m2 = ddiv(m2, rho);
+}
+
 // sum_i e_ik * f_i in direction order, zero components omitted (moments<T>, lattice.hpp:97-102)
 template <int D, int K>
 __device__ __forceinline__ double momentum(const double* f) {
@@ -150,9 +187,7 @@ __device__ __forceinline__ bool collide_bgk(double* f, double inv_tau) {
   double u2 = momentum<D, 2>(f);
   if (!INC) {
     if (!(rho > 0.0) || !finite(rho)) return false;
-    u0 = ddiv(u0, rho);
-    u1 = ddiv(u1, rho);
-    u2 = ddiv(u2, rho);
+    divide3(u0, u1, u2, rho);
   }
   const double uu = sqnorm(u0, u1, u2);
 #pragma unroll
@@ -186,9 +221,10 @@ __device__ __forceinline__ bool apply_boundary(double* f, int type, bool rho_und
   double u0 = 0.0, u1 = 0.0, u2 = 0.0;
   if (!INC) {
     if (rho > 0.0) {
-      u0 = ddiv(m0, rho);
-      u1 = ddiv(m1, rho);
-      u2 = ddiv(m2, rho);
+      u0 = m0;
+      u1 = m1;
+      u2 = m2;
+      divide3(u0, u1, u2, rho);
     }
   } else {
     u0 = m0;

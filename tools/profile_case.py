@@ -1,0 +1,23 @@
+"""Runs one workload for a few steps (for ncu captures): python tools/profile_case.py NAME [steps]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1703_08015_b200 as P  # noqa: E402
+
+CASES = {
+    "channel128": lambda: (P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=(128, 128, 128))), 4, 0),
+    "ras256_phi02": lambda: (P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(256, 256, 256), sphere_diameter=40, target_porosity=0.2, seed=7)), 4, 7),
+    "ras256_phi05": lambda: (P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(256, 256, 256), sphere_diameter=40, target_porosity=0.5, seed=7)), 4, 7),
+    "cavity2d_4096_a4": lambda: (P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(4096, 4096, 1))), 4, 0),
+    "vessel4096_a4": lambda: (P.generate(P.GeometryKind.Vessel2D, P.GenerateParams(dims=(4096, 4096, 1), target_porosity=0.2, seed=1)), 4, 0),
+}
+
+if __name__ == "__main__":
+    name = sys.argv[1]
+    steps = int(sys.argv[2]) if len(sys.argv) > 2 else 6
+    g, a, per = CASES[name]()
+    e = P.TileEngineT2C(g, a, P.FluidModel(tau=0.8), per)
+    e.initialize_uniform(1.0, (0.01, 0.0, 0.0))
+    ok, _ = e.step_n(steps)
+    print(name, "ok" if ok else "FAILED", "fluid nodes", e.fluid_nodes(), "tiles", e.info.n_tiles)
