@@ -52,12 +52,15 @@ class ClockSampler:
 
     def __init__(self, index=0):
         self.samples = []
+        self.error = None
         self._stop = threading.Event()
+        self._first = threading.Event()
         self.index = index
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        self._first.wait(5.0)  # the first sample precedes the timed region's start
         return self
 
     def _run(self):
@@ -66,14 +69,16 @@ class ClockSampler:
             N.nvmlInit()
             h = N.nvmlDeviceGetHandleByIndex(self.index)
             mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
-            while not self._stop.is_set():
+            reasons = (getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None)
+                       or N.nvmlDeviceGetCurrentClocksThrottleReasons)
+            while True:
                 sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
-                rs = N.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((sm, mx, rs))
-                self._stop.wait(0.002)
-            return
-        except Exception:
-            pass
+                self.samples.append((sm, mx, reasons(h)))
+                self._first.set()
+                if self._stop.wait(0.002):
+                    return
+        except Exception as ex:  # noqa: BLE001 - fall back to nvidia-smi
+            self.error = repr(ex)
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index),
@@ -83,7 +88,9 @@ class ClockSampler:
                 sm, mx, rs = [v.strip() for v in out.split(",")]
                 self.samples.append((float(sm), float(mx), int(rs, 16)))
             except Exception:
+                self._first.set()
                 return
+            self._first.set()
             self._stop.wait(0.02)
 
     def __exit__(self, *a):
@@ -92,7 +99,8 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0,
+                    "error": self.error}
         reasons = sorted({n for _, _, rs in self.samples for n, bit in self.REASONS.items()
                           if rs & bit})
         return {"sm_mhz": float(np.median([s[0] for s in self.samples])),
@@ -154,6 +162,33 @@ def porosity_sweep(P, K, W, peak):
     return out
 
 
+def other_configs(P, K, W, peak):
+    """The other BASELINE configs on one GPU: configs[0] (D2Q9 cavity 256^2, 1000 steps, a=4 and
+    the reference 2D default a=16) and configs[3] (D2Q9 4096^2 seeded vessel tree, a=4)."""
+    rows = []
+    cases = [("configs[0] D2Q9 cavity 256^2 a=4, 1000 steps",
+              lambda: P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(256, 256, 1))), 4, 1000),
+             ("configs[0] D2Q9 cavity 256^2 a=16, 1000 steps",
+              lambda: P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(256, 256, 1))), 16, 1000),
+             ("configs[3] D2Q9 vessel tree 4096^2 a=4 (seed 1, phi~0.23)",
+              lambda: P.generate(P.GeometryKind.Vessel2D, P.GenerateParams(
+                  dims=(4096, 4096, 1), target_porosity=0.2, seed=1)), 4, K)]
+    for name, mk, a, steps in cases:
+        g = mk()
+        eng = P.TileEngineT2C(g, a, P.FluidModel(tau=0.8))
+        eng.initialize_uniform()
+        ms, _, _ = time_steps(eng, steps, W)
+        nf = eng.fluid_nodes()
+        mlups = nf * steps / (ms * 1e-3) / 1e6
+        gbs = mlups * 1e6 * B_NODE[2] / 1e9
+        rows.append({"config": name, "steps": steps, "fluid_nodes": nf,
+                     "phi_t": round(eng.info.phi_t, 4), "us_per_step": round(ms / steps * 1e3, 2),
+                     "mlups": round(mlups, 1), "achieved_gbs": round(gbs, 1),
+                     "frac_of_measured_peak": round(gbs / peak, 4)})
+        del eng
+    return rows
+
+
 def e2e_public_api(P, g, steps):
     """End to end through the public API with host buffers: NodeInit fields H2D from pinned host
     memory, `steps` LBM steps (first-failure check), final (rho, u) fields + mass D2H."""
@@ -164,18 +199,23 @@ def e2e_public_api(P, g, steps):
     pinned[0][:] = 1.0
     for a in pinned[1:]:
         a[:] = 0.0
+    nr = g.node_count()
+    out = P.FieldData(g.d, g.dims, torch.empty(nr, dtype=torch.uint8, pin_memory=True).numpy(),
+                      *[torch.empty(nr, dtype=torch.float64, pin_memory=True).numpy()
+                        for _ in range(4)])
     eng.initialize_arrays(*pinned)  # warm
     eng.step_n(2)
-    eng.fields()
+    eng.fields(out=out)
     t0 = time.perf_counter()
     eng.initialize_arrays(*pinned)
     ok, failed = eng.step_n(steps)
-    f, mass = eng.fields(with_mass=True)
+    f, mass = eng.fields(with_mass=True, out=out)
     wall = time.perf_counter() - t0
     assert ok and np.isfinite(mass)
     nf = eng.fluid_nodes()
     h2d = 4 * n * 8
     d2h = 4 * n * 8 + 8  # moments of every stored tile node + the failure stamp
+    # (the host then scatters them into the pinned raster FieldData and sums the mass)
     return {"value": round(nf * steps / wall / 1e6, 1), "unit": "MLUPS",
             "h2d_bytes_per_step": round(h2d / steps, 1), "d2h_bytes_per_step": round(d2h / steps, 1),
             "steps": steps, "wall_s": round(wall, 4)}
@@ -299,6 +339,7 @@ def run_ours(args):
     del eng
     if not args.no_sweep:
         line["porosity_sweep"] = porosity_sweep(P, min(K, 50), max(W, 3), peak)
+        line["other_configs"] = other_configs(P, min(K, 50), max(W, 3), peak)
     line["e2e"] = e2e_public_api(P, g, 1000)
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(P, dims)

@@ -37,6 +37,9 @@ void cuda_check(cudaError_t e, const char* what) {
 #define CK(x) cuda_check((x), #x)
 
 constexpr uint64_t kChunkNodes = 1ull << 22;  // init / moments staging (4 x 32 MB)
+#ifndef SPLBM_L2_FETCH
+#define SPLBM_L2_FETCH 0  // L2 fetch granularity hint in bytes (0 = driver default)
+#endif
 constexpr int kGraphSteps = 32;               // steps per captured graph (even)
 
 }  // namespace
@@ -73,6 +76,19 @@ struct splbm_dev_engine {
   bool batch_timed = false;
   long pending_steps = 0;
   std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
+  double* pinned = nullptr;  // host staging for fields() (page-locked, grown on demand)
+  std::size_t pinned_count = 0;
+
+  double* host_stage(std::size_t count) {
+    if (count > pinned_count) {
+      if (pinned) cudaFreeHost(pinned);
+      pinned = nullptr;
+      pinned_count = 0;
+      CK(cudaMallocHost(&pinned, count * sizeof(double)));
+      pinned_count = count;
+    }
+    return pinned;
+  }
 
   ~splbm_dev_engine() {
     if (device >= 0) cudaSetDevice(device);
@@ -82,6 +98,7 @@ struct splbm_dev_engine {
                     static_cast<void*>(step_base), static_cast<void*>(domain_err),
                     static_cast<void*>(halo_dirs), static_cast<void*>(scratch)})
       if (p) cudaFree(p);
+    if (pinned) cudaFreeHost(pinned);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
@@ -237,6 +254,7 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
     throw Error(SPLBM_ERR_CUDA, "no CUDA device available (the T2C path has no CPU fallback)");
   if (e->device < 0 || e->device >= ndev) throw config_error("invalid CUDA device ordinal");
   CK(cudaSetDevice(e->device));
+  if (SPLBM_L2_FETCH > 0) CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, SPLBM_L2_FETCH));
   CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   CK(cudaEventCreate(&e->ev0));
   CK(cudaEventCreate(&e->ev1));
@@ -244,7 +262,8 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
   e->pdf[0] = e->alloc<double>(nslots);
   e->pdf[1] = e->alloc<double>(nslots);
   e->info = e->alloc<uint32_t>(S * n_tn);
-  e->nb = e->alloc<uint32_t>(S * 27);
+  const int nbs = d == 3 ? 27 : 9;  // 2D keeps only the dz = 0 slice (cells 9..17)
+  e->nb = e->alloc<uint32_t>(S * nbs);
   e->failed = e->alloc<unsigned long long>(1);
   e->step_base = e->alloc<long long>(1);
   e->domain_err = e->alloc<int>(1);
@@ -264,6 +283,12 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
   CK(cudaMemsetAsync(e->step_base, 0, sizeof(long long), e->stream));
   CK(cudaMemsetAsync(e->pdf[0], 0, nslots * 8, e->stream));
   CK(cudaMemsetAsync(e->pdf[1], 0, nslots * 8, e->stream));
+  if (d == 2) {
+    std::vector<uint32_t> nb2(S * 9);
+    for (uint64_t t = 0; t < S; ++t)
+      for (int k = 0; k < 9; ++k) nb2[t * 9 + k] = nb_local[t * 27 + 9 + k];
+    nb_local.swap(nb2);
+  }
   CK(cudaMemcpyAsync(e->nb, nb_local.data(), nb_local.size() * 4, cudaMemcpyHostToDevice, e->stream));
   {
     uint8_t* types_d = nullptr;
@@ -464,31 +489,29 @@ int splbm_dev_fields(splbm_dev_engine* e, double* rho, double* ux, double* uy, d
     const int* dims = e->tm.dims;
     const std::size_t n = static_cast<std::size_t>(dims[0]) * dims[1] * dims[2];
     // FieldData frame: zeros, mask at non-solid nodes (engine.hpp:516-534)
-    std::vector<double> hr, hx, hy, hz;
+    std::vector<double> own_rho;
+    std::vector<uint8_t> own_mask;
+    if (mass_out && !rho) {
+      own_rho.resize(n);
+      rho = own_rho.data();
+    }
+    if (mass_out && !mask) {
+      own_mask.resize(n);
+      mask = own_mask.data();
+    }
     double* out[4] = {rho, ux, uy, uz};
-    std::vector<double>* own[4] = {&hr, &hx, &hy, &hz};
-    const bool need_mass = mass_out != nullptr;
-    for (int k = 0; k < 4; ++k) {
-      if (!out[k] && (k > 0 || !need_mass)) continue;
-      if (!out[k]) {
-        own[k]->assign(n, 0.0);
-        out[k] = own[k]->data();
-      } else {
-        std::memset(out[k], 0, n * 8);
-      }
-    }
-    std::vector<uint8_t> mloc;
-    if (!mask && need_mass) {
-      mloc.assign(n, 0);
-      mask = mloc.data();
-    }
-    if (mask) std::memset(mask, 0, n);
+    parallel_for(n, [&](std::size_t b, std::size_t en) {
+      for (int c = 0; c < 4; ++c)
+        if (out[c]) std::memset(out[c] + b, 0, (en - b) * 8);
+      if (mask) std::memset(mask + b, 0, en - b);
+    }, 1u << 20);
     CK(cudaMemsetAsync(e->domain_err, 0, sizeof(int), e->stream));
-    const uint64_t first = e->n_low * e->n_tn, total = e->n_own * e->n_tn;
-    std::vector<double> stage(4 * std::min<uint64_t>(kChunkNodes, std::max<uint64_t>(total, 1)));
     const int a = e->a, n_tn = e->n_tn;
-    for (uint64_t k0 = 0; k0 < total; k0 += kChunkNodes) {
-      const uint64_t cnt = std::min(kChunkNodes, total - k0);
+    const uint64_t first = e->n_low * n_tn, total = e->n_own * n_tn;
+    const uint64_t chunk = std::max<uint64_t>(n_tn, (kChunkNodes / n_tn) * n_tn);  // whole tiles
+    double* stage = e->host_stage(4 * std::min(chunk, std::max<uint64_t>(total, 1)));
+    for (uint64_t k0 = 0; k0 < total; k0 += chunk) {
+      const uint64_t cnt = std::min(chunk, total - k0);
       splbm_dev::MomentsArgs ma{};
       ma.pdf = e->pdf[e->read];
       ma.info = e->info;
@@ -502,12 +525,12 @@ int splbm_dev_fields(splbm_dev_engine* e, double* rho, double* ux, double* uy, d
       ma.domain_error = e->domain_err;
       CK(splbm_dev::launch_moments(e->d, e->incompressible != 0, ma, e->stream));
       ++e->launches;
-      CK(cudaMemcpyAsync(stage.data(), e->scratch, 4 * cnt * 8, cudaMemcpyDeviceToHost, e->stream));
+      CK(cudaMemcpyAsync(stage, e->scratch, 4 * cnt * 8, cudaMemcpyDeviceToHost, e->stream));
       CK(cudaStreamSynchronize(e->stream));
+      const uint64_t s0 = (first + k0) / n_tn;  // first stored tile of the chunk
       parallel_for(cnt / n_tn, [&](std::size_t b, std::size_t en) {
         for (std::size_t tl = b; tl < en; ++tl) {
-          const uint64_t s = (first + k0) / n_tn + tl;  // stored tile index
-          const uint64_t g = e->g_own0 + (s - e->n_low);
+          const uint64_t g = e->g_own0 + (s0 + tl - e->n_low);
           const int32_t* o = &e->tm.origins[3 * g];
           const uint8_t* tt = &e->tm.types[g * n_tn];
           for (int p = 0; p < n_tn; ++p) {
@@ -528,7 +551,7 @@ int splbm_dev_fields(splbm_dev_engine* e, double* rho, double* ux, double* uy, d
     if (mass_out) {  // FieldData::total_mass, sequential raster order (fields.hpp:25-31)
       double m = 0.0;
       for (std::size_t i = 0; i < n; ++i)
-        if (mask[i]) m += out[0][i];
+        if (mask[i]) m += rho[i];
       *mass_out = m;
     }
   });

@@ -22,6 +22,12 @@ namespace splbm_dev {
 
 constexpr uint32_t kEmpty = 0xffffffffu;
 constexpr int kThreads = 256;
+// Device neighbour table: the 27 cells of engine.hpp:446-463 in 3D; in 2D only the dz = 0 slice
+// (cells 9..17) is ever addressed, so it is stored compactly with 9 entries per tile.
+template <int D>
+__host__ __device__ constexpr int nb_stride() { return D == 3 ? 27 : 9; }
+template <int D>
+__host__ __device__ constexpr int nb_offset() { return D == 3 ? 0 : 9; }
 #ifndef SPLBM_MINB3
 #define SPLBM_MINB3 4  // resident CTAs per SM the 3D step kernel is register-budgeted for
 #endif
@@ -72,7 +78,7 @@ __global__ void __launch_bounds__(kThreads) t2c_step_kernel(StepArgs args) {
   const int ly = (p / a) % a;
   const int lz = D == 3 ? p / (a * a) : 0;
   const double* own = args.read + t * tile_stride;
-  const uint32_t* nbt = args.nb + t * 27;
+  const uint32_t* nbt = args.nb + t * nb_stride<D>() - nb_offset<D>();
 
   double f[Q];
 #pragma unroll
@@ -128,16 +134,17 @@ __global__ void __launch_bounds__(kThreads, (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2)
   constexpr int NTN = D == 3 ? A * A * A : A * A;
   constexpr int TILES = kThreads / NTN;
   constexpr uint64_t STRIDE = static_cast<uint64_t>(Q) * NTN;
-  __shared__ const double* s_base[TILES][27];
+  constexpr int NBS = nb_stride<D>();
+  __shared__ const double* s_base[TILES][NBS];
 
   const uint64_t n_tiles = args.n_nodes / NTN;
   const uint64_t tile_blk = static_cast<uint64_t>(blockIdx.x) * TILES;
-  for (int k = threadIdx.x; k < TILES * 27; k += kThreads) {
-    const int tl = k / 27, dd = k % 27;
+  for (int k = threadIdx.x; k < TILES * NBS; k += kThreads) {
+    const int tl = k / NBS, dd = k % NBS;
     const uint64_t tt = tile_blk + tl;
     const double* b = nullptr;
     if (tt < n_tiles) {
-      const uint32_t s = __ldg(args.nb + (args.t0 + tt) * 27 + dd);
+      const uint32_t s = __ldg(args.nb + (args.t0 + tt) * NBS + dd);
       b = s == kEmpty ? nullptr : args.read + static_cast<uint64_t>(s) * STRIDE;
     }
     s_base[tl][dd] = b;
@@ -162,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2)
   const int ly = (p >> LOGA) & (A - 1);
   const int lz = D == 3 ? (p >> (2 * LOGA)) : 0;
   const double* own = args.read + t * STRIDE;
-  const double* const* nbp = s_base[tl];
+  const double* const* nbp = s_base[tl] - nb_offset<D>();
 
   double f[Q];
 #pragma unroll
@@ -231,7 +238,7 @@ __global__ void node_info_kernel(NodeInfoArgs args) {
     if (delta == 13) {
       blocked = (args.types[t * n_tn + sp] & 3) == 0;
     } else {
-      const uint32_t s = args.nb[t * 27 + delta];
+      const uint32_t s = args.nb[t * nb_stride<D>() + delta - nb_offset<D>()];
       // a neighbour outside the stored range (slab mode edge) counts as EMPTY
       blocked = s == kEmpty || (args.types[static_cast<uint64_t>(s) * n_tn + sp] & 3) == 0;
     }

@@ -12,7 +12,7 @@ struct StepArgs {
   const double* read;
   double* write;
   const uint32_t* info;  // per stored tile node gather word
-  const uint32_t* nb;    // stored tiles x 27, local indices
+  const uint32_t* nb;    // stored tiles x 27 (3D) / 9 (2D, dz = 0 slice), local indices
   uint64_t t0;           // first stepped tile (stored index)
   uint64_t n_nodes;      // stepped tiles * n_tn
   int a;

@@ -168,12 +168,18 @@ class TileEngineT2C:
         _native.check(self._L.splbm_dev_last_batch_ms(self._h, C.byref(ms)))
         return float(ms.value)
 
-    def fields(self, with_mass: bool = False):
-        """Engine::fields (engine.hpp:371-390): moments of the current post-collision copy."""
+    def fields(self, with_mass: bool = False, out: FieldData | None = None):
+        """Engine::fields (engine.hpp:371-390): moments of the current post-collision copy.
+        `out` (optional) supplies the destination arrays, e.g. page-locked host buffers."""
         nx, ny, nz = self.geometry_dims
         n = nx * ny * nz
-        rho, ux, uy, uz = (np.empty(n) for _ in range(4))
-        mask = np.empty(n, np.uint8)
+        if out is not None:
+            rho, ux, uy, uz, mask = out.rho, out.ux, out.uy, out.uz, out.mask
+            if any(a.size != n or not a.flags.c_contiguous for a in (rho, ux, uy, uz, mask)):
+                raise ConfigError("fields(out=...) arrays must be contiguous raster-sized")
+        else:
+            rho, ux, uy, uz = (np.empty(n) for _ in range(4))
+            mask = np.empty(n, np.uint8)
         mass = C.c_double()
         _native.check(self._L.splbm_dev_fields(self._h, _native.ptr(rho), _native.ptr(ux),
                                                _native.ptr(uy), _native.ptr(uz),

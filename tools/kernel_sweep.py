@@ -29,6 +29,7 @@ def run_one(K=100, W=10):
         "ras256_phi05": lambda: (P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(256, 256, 256), sphere_diameter=40, target_porosity=0.5, seed=7)), 7),
         "full256": lambda: (P.Geometry.filled(3, (256, 256, 256)), 7),
         "cavity2d_4096_a4": lambda: (P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(4096, 4096, 1))), 0),
+        "ras256_phi02": lambda: (P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(256, 256, 256), sphere_diameter=40, target_porosity=0.2, seed=7)), 7),
     }
     for name, mk in cases.items():
         g, per = mk()
