@@ -206,6 +206,12 @@ uint64_t splbm_dev_launch_count(const splbm_dev_engine* e);
 int splbm_dev_halo_bytes(const splbm_dev_engine* e, uint64_t* low_bytes, uint64_t* high_bytes);
 int splbm_dev_halo_recv_bytes(const splbm_dev_engine* e, uint64_t* low_bytes, uint64_t* high_bytes);
 int splbm_dev_halo_pack(splbm_dev_engine* e, void* low_dev, void* high_dev);
+/* Overlapped slab step: part 1 steps the bottom and top owned tile planes into the next copy,
+ * splbm_dev_halo_pack_next packs their faces from that copy (so the exchange can start), part 2
+ * steps the interior planes while the faces are in flight, then swaps the copies and counts the
+ * step. part 1 + part 2 == one splbm_dev_step_async(e, 1). Unpack after part 2. */
+int splbm_dev_step_part(splbm_dev_engine* e, int part);
+int splbm_dev_halo_pack_next(splbm_dev_engine* e, void* low_dev, void* high_dev);
 int splbm_dev_halo_unpack(splbm_dev_engine* e, const void* low_dev, const void* high_dev);
 
 /* ---- self-test ------------------------------------------------------------------------------- */

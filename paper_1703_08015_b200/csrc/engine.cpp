@@ -135,6 +135,39 @@ struct splbm_dev_engine {
     return s;
   }
 
+  // One step's kernel over the stored tile range [t_begin, t_end) from copy rd (no flip).
+  void launch_range(int rd, uint64_t t_begin, uint64_t t_end) {
+    if (t_end <= t_begin) return;
+    splbm_dev::StepArgs s = step_args(rd, 0);
+    s.t0 = t_begin;
+    s.n_nodes = (t_end - t_begin) * n_tn;
+    CK(splbm_dev::launch_step(d, incompressible != 0, s, stream));
+    ++launches;
+  }
+
+  // Slab-overlap parts: 1 = the bottom and top owned planes (their faces are exchanged while
+  // part 2, the interior planes, runs); part 2 then swaps the copies and counts the step.
+  void step_part(int part) {
+    const uint64_t b0 = n_low, b1 = n_low + send_low_tiles;          // bottom plane
+    const uint64_t t0 = n_low + n_own - send_high_tiles, t1 = n_low + n_own;  // top plane
+    const bool merged = b1 >= t0;  // one or two planes: the boundary covers the whole slab
+    if (part == 1) {
+      if (merged) {
+        launch_range(read, b0, t1);
+      } else {
+        launch_range(read, b0, b1);
+        launch_range(read, t0, t1);
+      }
+      return;
+    }
+    if (!merged) launch_range(read, b1, t0);
+    CK(splbm_dev::launch_bump(step_base, 1, stream));
+    ++launches;
+    read = 1 - read;
+    ++step_count;
+    visits += n_own;
+  }
+
   // Enqueue k steps starting from parity rd (direct launches) + the counter bump.
   void enqueue_direct(int rd, int k) {
     for (int r = 0; r < k; ++r) {
@@ -459,6 +492,18 @@ int splbm_dev_step_async(splbm_dev_engine* e, long nsteps) {
   });
 }
 
+int splbm_dev_step_part(splbm_dev_engine* e, int part) {
+  return guarded([&] {
+    checked(e);
+    if (part != 1 && part != 2) throw config_error("step part must be 1 (boundary planes) or 2");
+    if (part == 1 && e->pending_steps == 0) {
+      CK(cudaMemsetAsync(e->failed, 0xff, sizeof(unsigned long long), e->stream));
+    }
+    e->step_part(part);
+    if (part == 2) ++e->pending_steps;
+  });
+}
+
 int splbm_dev_sync(splbm_dev_engine* e, int* ok_out, long* failed_step_out) {
   return guarded([&] {
     checked(e);
@@ -641,6 +686,14 @@ int splbm_dev_halo_pack(splbm_dev_engine* e, void* low_dev, void* high_dev) {
       ++e->launches;
     }
   });
+}
+
+// pack_next: as pack, from the copy the in-flight step is writing (after step part 1).
+int splbm_dev_halo_pack_next(splbm_dev_engine* e, void* low_dev, void* high_dev) {
+  e->read = 1 - e->read;
+  const int rc = splbm_dev_halo_pack(e, low_dev, high_dev);
+  e->read = 1 - e->read;
+  return rc;
 }
 
 // unpack: low_dev (the lower neighbour's high face) -> low halo plane, layer a-1, upward dirs;

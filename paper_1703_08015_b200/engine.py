@@ -234,6 +234,12 @@ class TileEngineT2C:
     def halo_pack(self, low_ptr: int, high_ptr: int) -> None:
         _native.check(self._L.splbm_dev_halo_pack(self._h, low_ptr or None, high_ptr or None))
 
+    def step_part(self, part: int) -> None:
+        _native.check(self._L.splbm_dev_step_part(self._h, int(part)))
+
+    def halo_pack_next(self, low_ptr: int, high_ptr: int) -> None:
+        _native.check(self._L.splbm_dev_halo_pack_next(self._h, low_ptr or None, high_ptr or None))
+
     def halo_unpack(self, low_ptr: int, high_ptr: int) -> None:
         _native.check(self._L.splbm_dev_halo_unpack(self._h, low_ptr or None, high_ptr or None))
 

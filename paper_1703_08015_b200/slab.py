@@ -111,10 +111,11 @@ def neighbours(rank: int, world: int, periodic_axis: bool) -> tuple[int | None, 
 
 
 class HaloExchange:
-    """Per-step face exchange. `comm.exchange(ops)` runs a batch of point-to-point operations
-    [(op, tensor, peer)], op in {"send", "recv"}, and returns when they are enqueued/complete.
-    Two batches (upward then downward) keep the send/recv matching unambiguous even when the
-    lower and upper neighbour are the same rank (two ranks, periodic axis)."""
+    """Per-step face exchange between slab neighbours. `begin(pack)` packs the outgoing faces and
+    starts the transfers, `end(unpack)` completes them and stores the incoming faces; work issued
+    in between (the interior tiles) overlaps the transfers. Two batches (upward then downward)
+    keep the send/recv matching unambiguous even when the lower and upper neighbour are the same
+    rank (two ranks, periodic axis)."""
 
     def __init__(self, rank, world, periodic_axis, sizes, alloc, comm):
         self.lower, self.upper = neighbours(rank, world, periodic_axis)
@@ -124,8 +125,9 @@ class HaloExchange:
         self.send_high = alloc(n["send_high"])
         self.recv_low = alloc(n["recv_low"])
         self.recv_high = alloc(n["recv_high"])
+        self._pending = []
 
-    def exchange(self, pack, unpack):
+    def begin(self, pack):
         pack(self.send_low, self.send_high)
         up, down = [], []
         if self.upper is not None and self.send_high.numel():
@@ -136,39 +138,77 @@ class HaloExchange:
             down.append(("send", self.send_low, self.lower))
         if self.upper is not None and self.recv_high.numel():
             down.append(("recv", self.recv_high, self.upper))
-        for batch in (up, down):
-            if batch:
-                self.comm.exchange(batch)
+        self._pending = [self.comm.start(b) for b in (up, down) if b]
+
+    def end(self, unpack):
+        for h in self._pending:
+            self.comm.finish(h)
+        self._pending = []
         unpack(self.recv_low if self.lower is not None else None,
                self.recv_high if self.upper is not None else None)
 
+    def exchange(self, pack, unpack):
+        self.begin(pack)
+        self.end(unpack)
+
 
 class TorchComm:
-    """torch.distributed point-to-point (NCCL on GPUs, gloo on CPU)."""
+    """torch.distributed point-to-point: NCCL on device buffers, ordered on `stream` (the engine
+    stream), or gloo on CPU tensors. host_staged=True moves device buffers through host memory so
+    the same schedule runs over gloo (multi-process tests on a single GPU)."""
 
-    def __init__(self, stream=None):
+    def __init__(self, stream=None, host_staged=False):
         import torch.distributed as dist
         self.dist = dist
         self.stream = stream
+        self.host_staged = host_staged
 
-    def exchange(self, ops):
+    def start(self, ops):
         import torch
         dist = self.dist
+        if self.host_staged:
+            if self.stream is not None:
+                self.stream.synchronize()
+            else:
+                torch.cuda.synchronize()
+            staged = [(op, t.cpu() if op == "send" else torch.empty(t.shape, dtype=t.dtype), t, peer)
+                      for op, t, peer in ops]
+            works = dist.batch_isend_irecv([
+                dist.P2POp(dist.isend if op == "send" else dist.irecv, h, peer)
+                for op, h, _, peer in staged])
+            return works, staged
         p2p = [dist.P2POp(dist.isend if op == "send" else dist.irecv, t, peer) for op, t, peer in ops]
         if self.stream is not None:
+            with torch.cuda.stream(self.stream):  # NCCL waits for the pack on the engine stream
+                return dist.batch_isend_irecv(p2p), None
+        return dist.batch_isend_irecv(p2p), None
+
+    def finish(self, handle):
+        import torch
+        works, staged = handle
+        if self.stream is not None and not self.host_staged:
             with torch.cuda.stream(self.stream):
-                for w in dist.batch_isend_irecv(p2p):
-                    w.wait()  # enqueues the completion on the engine stream (no host sync)
-        else:
-            for w in dist.batch_isend_irecv(p2p):
-                w.wait()
+                for w in works:
+                    w.wait()  # the engine stream waits for the transfer (no host sync)
+            return
+        for w in works:
+            w.wait()
+        if staged:
+            with torch.cuda.stream(self.stream):
+                for op, h, t, _ in staged:
+                    if op == "recv":
+                        t.copy_(h, non_blocking=False)
+
+    def exchange(self, ops):
+        self.finish(self.start(ops))
 
 
 class SlabRun:
-    """One rank of the multi-GPU slab mode: a slab TileEngineT2C + its NCCL halo exchange."""
+    """One rank of the multi-GPU slab mode: a slab TileEngineT2C + its NCCL halo exchange,
+    overlapped with the interior tiles of every step."""
 
     def __init__(self, g: Geometry, a: int, model, periodic, rank: int, world: int, device: int,
-                 slabs=None):
+                 slabs=None, host_staged: bool = False):
         import torch
         from .engine import TileEngineT2C
         per = Periodicity.of(periodic)
@@ -182,21 +222,27 @@ class SlabRun:
         dev = torch.device("cuda", device)
         self.xchg = HaloExchange(rank, world, axis_periodic, self.engine.halo_bytes(),
                                  lambda n: torch.empty(n, dtype=torch.float64, device=dev),
-                                 TorchComm(self.stream))
+                                 TorchComm(self.stream, host_staged=host_staged))
 
     def _pack(self, lo, hi):
-        self.engine.halo_pack(lo.data_ptr() if lo.numel() else 0, hi.data_ptr() if hi.numel() else 0)
+        self.engine.halo_pack_next(lo.data_ptr() if lo.numel() else 0,
+                                   hi.data_ptr() if hi.numel() else 0)
 
     def _unpack(self, lo, hi):
         self.engine.halo_unpack(lo.data_ptr() if lo is not None and lo.numel() else 0,
                                 hi.data_ptr() if hi is not None and hi.numel() else 0)
 
     def step_async(self, n: int) -> None:
-        """n steps, each followed by the halo exchange; all stream-ordered on the engine stream."""
+        """n steps: boundary planes -> pack -> start exchange -> interior planes (overlapping the
+        transfers) -> complete exchange -> unpack; all ordered on the engine stream."""
+        if self.world == 1:
+            self.engine.step_async(n)
+            return
         for _ in range(n):
-            self.engine.step_async(1)
-            if self.world > 1:
-                self.xchg.exchange(self._pack, self._unpack)
+            self.engine.step_part(1)
+            self.xchg.begin(self._pack)
+            self.engine.step_part(2)
+            self.xchg.end(self._unpack)
 
     def sync(self):
         return self.engine.sync()
@@ -216,6 +262,7 @@ def bench_main(args, P) -> int:
     L = g.dims[2] // 4
     slabs = [(r * L // world, (r + 1) * L // world) for r in range(world)]
     run = SlabRun(g, 4, P.FluidModel(tau=0.8), None, rank, world, local, slabs=slabs)
+    dist.barrier()  # communicators up before the first point-to-point batch
     eng = run.engine
     eng.initialize_uniform()
     run.step_async(args.warmup)

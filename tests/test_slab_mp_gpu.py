@@ -1,0 +1,78 @@
+"""Multi-process slab mode on one B200: 2-3 ranks (processes) share cuda:0 and run SlabRun —
+overlapped boundary/interior step parts, pack_next, the HaloExchange schedule — with the faces
+moved over gloo through host memory (NCCL refuses two ranks on one GPU; the NCCL path differs only
+in the transport). Owned PDFs after K steps equal the single-engine run bit for bit."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+STEPS = 7
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _geom(name):
+    import paper_1703_08015_b200 as P
+    if name == "ras40_periodic":
+        return P.generate(P.GeometryKind.Ras3D, P.GenerateParams(
+            dims=(40, 40, 40), sphere_diameter=12, target_porosity=0.55, seed=5)), 4, 7
+    return P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=(24, 20, 48))), 4, 0
+
+
+def _worker(rank, world, port, name, q):
+    try:
+        import torch.distributed as dist
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_1703_08015_b200 as P
+        from oracle import oracle as O
+        from paper_1703_08015_b200 import slab
+        g, a, per = _geom(name)
+        m = P.FluidModel(tau=0.8)
+        run = slab.SlabRun(g, a, m, per, rank, world, 0, host_staged=True)
+        run.engine.initialize(O.wavy)
+        run.step_async(STEPS)
+        ok, _ = run.sync()
+        whole = P.TileEngineT2C(g, a, m, per)
+        whole.initialize(O.wavy)
+        whole.step_n(STEPS)
+        z0, z1 = run.slabs[rank]
+        lay = slab.slab_layout(g, a, per, z0, z1)
+        st = whole.q * whole.n_tn
+        g0, n = lay["g_own0"], lay["n_own"]
+        mine = run.engine.get_pdf()[lay["n_low"] * st:(lay["n_low"] + n) * st]
+        ref = whole.get_pdf()[g0 * st:(g0 + n) * st]
+        types = whole.tile_grid().types[g0:g0 + n]
+        fluid = np.broadcast_to((types != 0)[:, None, :], (n, whole.q, whole.n_tn)).ravel()
+        same = np.array_equal(mine[fluid].view(np.uint64), ref[fluid].view(np.uint64))
+        dist.destroy_process_group()
+        q.put((rank, bool(ok and same), run.engine.current_step()))
+    except Exception as ex:  # pragma: no cover
+        import traceback
+        q.put((rank, False, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name", ["ras40_periodic", "channel3d"])
+def test_slabrun_processes_match_whole(name, world):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, name, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=600) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    assert all(r[1] for r in res), res
+    assert all(r[2] == STEPS for r in res)
