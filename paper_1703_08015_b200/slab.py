@@ -113,9 +113,11 @@ def neighbours(rank: int, world: int, periodic_axis: bool) -> tuple[int | None, 
 class HaloExchange:
     """Per-step face exchange between slab neighbours. `begin(pack)` packs the outgoing faces and
     starts the transfers, `end(unpack)` completes them and stores the incoming faces; work issued
-    in between (the interior tiles) overlaps the transfers. Two batches (upward then downward)
-    keep the send/recv matching unambiguous even when the lower and upper neighbour are the same
-    rank (two ranks, periodic axis)."""
+    in between (the interior tiles) overlaps the transfers. All four transfers form one batch in
+    the fixed order [send up, recv from below, send down, recv from above]: point-to-point
+    operations between a pair of ranks match in issue order, so even when the lower and upper
+    neighbour are the same rank (two ranks, periodic axis) send-up meets recv-from-below and
+    send-down meets recv-from-above."""
 
     def __init__(self, rank, world, periodic_axis, sizes, alloc, comm):
         self.lower, self.upper = neighbours(rank, world, periodic_axis)
@@ -129,16 +131,16 @@ class HaloExchange:
 
     def begin(self, pack):
         pack(self.send_low, self.send_high)
-        up, down = [], []
+        ops = []
         if self.upper is not None and self.send_high.numel():
-            up.append(("send", self.send_high, self.upper))
+            ops.append(("send", self.send_high, self.upper))
         if self.lower is not None and self.recv_low.numel():
-            up.append(("recv", self.recv_low, self.lower))
+            ops.append(("recv", self.recv_low, self.lower))
         if self.lower is not None and self.send_low.numel():
-            down.append(("send", self.send_low, self.lower))
+            ops.append(("send", self.send_low, self.lower))
         if self.upper is not None and self.recv_high.numel():
-            down.append(("recv", self.recv_high, self.upper))
-        self._pending = [self.comm.start(b) for b in (up, down) if b]
+            ops.append(("recv", self.recv_high, self.upper))
+        self._pending = [self.comm.start(ops)] if ops else []
 
     def end(self, unpack):
         for h in self._pending:
