@@ -41,10 +41,6 @@ constexpr uint64_t kChunkNodes = 1ull << 22;  // init / moments staging (4 x 32 
 #define SPLBM_L2_FETCH 0  // L2 fetch granularity hint in bytes (0 = driver default)
 #endif
 constexpr int kGraphSteps = 32;               // steps per captured graph (even)
-#ifndef SPLBM_MULTISTEP_MAX_NODES
-#define SPLBM_MULTISTEP_MAX_NODES (1 << 18)  // cooperative multi-step below this many tile nodes
-#endif
-constexpr int kMultistepMaxNodes = SPLBM_MULTISTEP_MAX_NODES;
 
 }  // namespace
 
@@ -209,23 +205,6 @@ struct splbm_dev_engine {
 
   void enqueue_steps(long n) {
     long left = n;
-    // small domains: the whole batch in one cooperative launch (grid-wide barrier per step)
-    if (n >= 2 && n_own * n_tn <= static_cast<uint64_t>(kMultistepMaxNodes)) {
-      cudaError_t err = cudaSuccess;
-      const int chunk = static_cast<int>(std::min<long>(n, 1 << 20));
-      if (splbm_dev::launch_multistep(d, incompressible != 0, step_args(read, 0), chunk,
-                                      kMultistepMaxNodes / 256, stream, &err)) {
-        CK(err);
-        ++launches;
-        CK(splbm_dev::launch_bump(step_base, chunk, stream));
-        ++launches;
-        if (chunk & 1) read = 1 - read;
-        step_count += chunk;
-        visits += n_own * static_cast<uint64_t>(chunk);
-        if (chunk < n) enqueue_steps(n - chunk);
-        return;
-      }
-    }
     while (left >= kGraphSteps) {
       CK(cudaGraphLaunch(graph_for(read), stream));
       launches += kGraphSteps + 1;

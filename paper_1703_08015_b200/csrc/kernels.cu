@@ -11,7 +11,6 @@
 // One thread per tile node, 256 threads per CTA, consecutive threads = consecutive p so all
 // q stores of a warp are 256-B coalesced runs; the gather reads the own tile (L1) and the
 // face-adjacent neighbour tiles (L2 hits: neighbours are near in the compact z-major order).
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -21,7 +20,6 @@
 
 namespace splbm_dev {
 
-namespace cg = cooperative_groups;
 constexpr uint32_t kEmpty = 0xffffffffu;
 constexpr int kThreads = 256;
 // Device neighbour table: the 27 cells of engine.hpp:446-463 in 3D; in 2D only the dz = 0 slice
@@ -129,27 +127,18 @@ __global__ void __launch_bounds__(kThreads) t2c_step_kernel(StepArgs args) {
 // the per-direction source address is pure integer arithmetic on compile-time lattice constants
 // plus one shared-memory lookup and two selects — no divergent branches, no dependent global load
 // before the PDF gather.
-template <int D, int LOGA>
-struct Pow2Tiles {
-  static constexpr int A = 1 << LOGA;
-  static constexpr int NTN = D == 3 ? A * A * A : A * A;
-  static constexpr int TILES = kThreads / NTN;
-  static constexpr int NBS = nb_stride<D>();
-};
-
-// One CTA-sized group of tiles (block index `blk`) of one step.
 template <int D, int LOGA, bool INC>
-__device__ __forceinline__ void pow2_step_block(const StepArgs& args, uint64_t blk,
-                                                const double* (*s_base)[Pow2Tiles<D, LOGA>::NBS]) {
+__global__ void __launch_bounds__(kThreads, (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2)) t2c_step_pow2_kernel(StepArgs args) {
   constexpr int Q = Lat<D>::Q;
-  constexpr int A = Pow2Tiles<D, LOGA>::A;
-  constexpr int NTN = Pow2Tiles<D, LOGA>::NTN;
-  constexpr int TILES = Pow2Tiles<D, LOGA>::TILES;
-  constexpr int NBS = Pow2Tiles<D, LOGA>::NBS;
+  constexpr int A = 1 << LOGA;
+  constexpr int NTN = D == 3 ? A * A * A : A * A;
+  constexpr int TILES = kThreads / NTN;
   constexpr uint64_t STRIDE = static_cast<uint64_t>(Q) * NTN;
+  constexpr int NBS = nb_stride<D>();
+  __shared__ const double* s_base[TILES][NBS];
 
   const uint64_t n_tiles = args.n_nodes / NTN;
-  const uint64_t tile_blk = blk * TILES;
+  const uint64_t tile_blk = static_cast<uint64_t>(blockIdx.x) * TILES;
   for (int k = threadIdx.x; k < TILES * NBS; k += kThreads) {
     const int tl = k / NBS, dd = k % NBS;
     const uint64_t tt = tile_blk + tl;
@@ -180,7 +169,7 @@ __device__ __forceinline__ void pow2_step_block(const StepArgs& args, uint64_t b
   const int ly = (p >> LOGA) & (A - 1);
   const int lz = D == 3 ? (p >> (2 * LOGA)) : 0;
   const double* own = args.read + t * STRIDE;
-  const double* const* nbp = s_base[tl];
+  const double* const* nbp = s_base[tl] - nb_offset<D>();
 
   double f[Q];
 #pragma unroll
@@ -191,7 +180,7 @@ __device__ __forceinline__ void pow2_step_block(const StepArgs& args, uint64_t b
     const int dz = (D == 3 && ez<D>(i)) ? (vz >> LOGA) : 0;
     const int sp = (vx & (A - 1)) | ((vy & (A - 1)) << LOGA) | (D == 3 ? ((vz & (A - 1)) << (2 * LOGA)) : 0);
     const int delta = 13 + dx + 3 * dy + 9 * dz;
-    const double* src = (delta == 13 ? own : nbp[delta - nb_offset<D>()]) + (i * NTN + sp);
+    const double* src = (delta == 13 ? own : nbp[delta]) + (i * NTN + sp);
     const double* bb = own + (opp(i) * NTN + p);  // half-way bounce-back (engine.hpp:498-500)
     f[i] = __ldg(((info >> i) & 1u) ? bb : src);
   }
@@ -205,36 +194,6 @@ __device__ __forceinline__ void pow2_step_block(const StepArgs& args, uint64_t b
   if (!good) atomicMin(args.failed, static_cast<unsigned long long>(*args.step_base + args.rel + 1));
 #pragma unroll
   for (int i = 0; i < Q; ++i) st_stream(wr + i * NTN, f[i]);
-}
-
-template <int D, int LOGA, bool INC>
-__global__ void __launch_bounds__(kThreads, (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2)) t2c_step_pow2_kernel(StepArgs args) {
-  __shared__ const double* s_base[Pow2Tiles<D, LOGA>::TILES][Pow2Tiles<D, LOGA>::NBS];
-  pow2_step_block<D, LOGA, INC>(args, blockIdx.x, s_base);
-}
-
-// Small domains are launch-bound (a D2Q9 256^2 step moves 9 MB, ~2 us): one cooperative launch
-// runs `nsteps` steps with a grid-wide barrier between them (CTAs loop over the tile groups).
-template <int D, int LOGA, bool INC>
-__global__ void __launch_bounds__(kThreads, (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2))
-    t2c_multistep_pow2_kernel(StepArgs args, int nsteps) {
-  __shared__ const double* s_base[Pow2Tiles<D, LOGA>::TILES][Pow2Tiles<D, LOGA>::NBS];
-  constexpr int TILES = Pow2Tiles<D, LOGA>::TILES;
-  const uint64_t nblk = (args.n_nodes / Pow2Tiles<D, LOGA>::NTN + TILES - 1) / TILES;
-  cg::grid_group grid = cg::this_grid();
-  const double* r0 = args.read;
-  double* w0 = args.write;
-  for (int s = 0; s < nsteps; ++s) {
-    StepArgs a = args;
-    a.read = (s & 1) ? w0 : r0;
-    a.write = (s & 1) ? const_cast<double*>(r0) : w0;
-    a.rel = s;
-    for (uint64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
-      __syncthreads();  // s_base of the previous group is no longer read
-      pow2_step_block<D, LOGA, INC>(a, blk, s_base);
-    }
-    grid.sync();
-  }
 }
 
 // Advances the step counter the failure stamps are relative to (one per enqueued batch).
@@ -498,53 +457,6 @@ static cudaError_t launch_step_d(const StepArgs& a, cudaStream_t st) {
 cudaError_t launch_step(int d, bool inc, const StepArgs& a, cudaStream_t st) {
   if (d == 2) return inc ? launch_step_d<2, true>(a, st) : launch_step_d<2, false>(a, st);
   return inc ? launch_step_d<3, true>(a, st) : launch_step_d<3, false>(a, st);
-}
-
-// Cooperative multi-step launch for small power-of-two-tile domains; returns false (nothing
-// launched) when the case does not qualify, so the caller falls back to per-step kernels.
-template <int D, int LOGA, bool INC>
-static bool try_multistep(const StepArgs& a, int nsteps, int max_blocks, cudaStream_t st,
-                          cudaError_t* err) {
-  constexpr int NTN = Pow2Tiles<D, LOGA>::NTN;
-  constexpr int TILES = Pow2Tiles<D, LOGA>::TILES;
-  const uint64_t nblk = (a.n_nodes / NTN + TILES - 1) / TILES;
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, t2c_multistep_pow2_kernel<D, LOGA, INC>,
-                                                kThreads, 0);
-  const uint64_t resident = static_cast<uint64_t>(sms) * per_sm;
-  if (nblk == 0 || resident == 0 || nblk > static_cast<uint64_t>(max_blocks) || nblk > resident)
-    return false;
-  StepArgs args = a;
-  void* params[] = {&args, &nsteps};
-  *err = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(t2c_multistep_pow2_kernel<D, LOGA, INC>),
-                                     dim3(static_cast<unsigned>(nblk)), dim3(kThreads), params, 0, st);
-  return true;
-}
-
-template <int D, bool INC>
-static bool multistep_d(const StepArgs& a, int nsteps, int max_blocks, cudaStream_t st,
-                        cudaError_t* err) {
-  if constexpr (D == 3) {
-    if (a.a == 4) return try_multistep<D, 2, INC>(a, nsteps, max_blocks, st, err);
-    if (a.a == 2) return try_multistep<D, 1, INC>(a, nsteps, max_blocks, st, err);
-  } else {
-    if (a.a == 4) return try_multistep<D, 2, INC>(a, nsteps, max_blocks, st, err);
-    if (a.a == 8) return try_multistep<D, 3, INC>(a, nsteps, max_blocks, st, err);
-    if (a.a == 16) return try_multistep<D, 4, INC>(a, nsteps, max_blocks, st, err);
-    if (a.a == 2) return try_multistep<D, 1, INC>(a, nsteps, max_blocks, st, err);
-  }
-  return false;
-}
-
-bool launch_multistep(int d, bool inc, const StepArgs& a, int nsteps, int max_blocks,
-                      cudaStream_t st, cudaError_t* err) {
-  *err = cudaSuccess;
-  if (d == 2) return inc ? multistep_d<2, true>(a, nsteps, max_blocks, st, err)
-                         : multistep_d<2, false>(a, nsteps, max_blocks, st, err);
-  return inc ? multistep_d<3, true>(a, nsteps, max_blocks, st, err)
-             : multistep_d<3, false>(a, nsteps, max_blocks, st, err);
 }
 
 cudaError_t launch_bump(long long* step_base, long long by, cudaStream_t st) {

@@ -78,10 +78,6 @@ struct HaloArgs {
 
 cudaError_t launch_step(int d, bool inc, const StepArgs& a, cudaStream_t st);
 cudaError_t launch_bump(long long* step_base, long long by, cudaStream_t st);
-// nsteps steps in one cooperative launch when the domain fits in one resident wave of at most
-// max_blocks CTAs; returns false if not applicable (nothing launched).
-bool launch_multistep(int d, bool inc, const StepArgs& a, int nsteps, int max_blocks,
-                      cudaStream_t st, cudaError_t* err);
 cudaError_t launch_node_info(int d, const NodeInfoArgs& a, cudaStream_t st);
 cudaError_t launch_init(int d, bool inc, const InitArgs& a, cudaStream_t st);
 cudaError_t launch_moments(int d, bool inc, const MomentsArgs& a, cudaStream_t st);

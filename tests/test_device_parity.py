@@ -144,34 +144,3 @@ def test_errors_match_reference():
         P.TileEngineT2C(g, 1, P.FluidModel(tau=0.8))
     with pytest.raises(P.ConfigError):
         P.TileEngineT2C(P.Geometry.filled(2, (30, 32, 1)), 16, P.FluidModel(tau=0.8), (1, 0, 0))
-
-
-@pytest.mark.parametrize("name", ["cavity2d_64_a4", "cavity2d_64_a16", "ras24_periodic_incompr",
-                                  "periodic_single_tile_3d", "random_solids_a2"])
-def test_multistep_cooperative_path_bitwise(name, oracle):
-    """Small domains run a whole batch in one cooperative launch (grid barrier per step); the
-    result equals the oracle bit for bit and the failure stamp keeps its step number."""
-    factory, a, tau, inc, per, init = CASES[name]
-    g = factory()
-    model = P.FluidModel(P.Compressibility.Incompressible if inc else P.Compressibility.QuasiCompressible,
-                         tau=tau)
-    de = P.TileEngineT2C(g, a, model, per)
-    oe = make_oracle(oracle, g, a, tau, inc, per)
-    init_both(oracle, oe, de, init)
-    launches = de.launch_count()
-    assert de.step_n(57) == (True, 0)
-    assert de.launch_count() - launches <= 3  # one cooperative launch + the counter bump
-    oe.step(57)
-    mask = fluid_slot_mask(oe.tiles["types"], oe.q)
-    assert np.array_equal(de.get_pdf()[mask].view(np.uint64), oe.current_pdf()[mask].view(np.uint64))
-    assert de.current_step() == 57
-
-
-def test_all_solid_geometry_has_no_tiles():
-    g = P.Geometry.filled(3, (16, 16, 16), 0)
-    e = P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8))
-    assert e.info.n_tiles == 0
-    e.initialize_uniform()
-    assert e.step_n(5) == (True, 0)
-    f, mass = e.fields(with_mass=True)
-    assert mass == 0.0 and not f.mask.any() and e.tile_visits() == 0
