@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2)
   const int ly = (p >> LOGA) & (A - 1);
   const int lz = D == 3 ? (p >> (2 * LOGA)) : 0;
   const double* own = args.read + t * STRIDE;
-  const double* const* nbp = s_base[tl] - nb_offset<D>();
+  const double* const* nbp = s_base[tl];
 
   double f[Q];
 #pragma unroll
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2)
     const int dz = (D == 3 && ez<D>(i)) ? (vz >> LOGA) : 0;
     const int sp = (vx & (A - 1)) | ((vy & (A - 1)) << LOGA) | (D == 3 ? ((vz & (A - 1)) << (2 * LOGA)) : 0);
     const int delta = 13 + dx + 3 * dy + 9 * dz;
-    const double* src = (delta == 13 ? own : nbp[delta]) + (i * NTN + sp);
+    const double* src = (delta == 13 ? own : nbp[delta - nb_offset<D>()]) + (i * NTN + sp);
     const double* bb = own + (opp(i) * NTN + p);  // half-way bounce-back (engine.hpp:498-500)
     f[i] = __ldg(((info >> i) & 1u) ? bb : src);
   }

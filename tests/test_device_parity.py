@@ -144,3 +144,13 @@ def test_errors_match_reference():
         P.TileEngineT2C(g, 1, P.FluidModel(tau=0.8))
     with pytest.raises(P.ConfigError):
         P.TileEngineT2C(P.Geometry.filled(2, (30, 32, 1)), 16, P.FluidModel(tau=0.8), (1, 0, 0))
+
+
+def test_all_solid_geometry_has_no_tiles():
+    g = P.Geometry.filled(3, (16, 16, 16), 0)
+    e = P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8))
+    assert e.info.n_tiles == 0
+    e.initialize_uniform()
+    assert e.step_n(5) == (True, 0)
+    f, mass = e.fields(with_mass=True)
+    assert mass == 0.0 and not f.mask.any() and e.tile_visits() == 0
