@@ -214,6 +214,14 @@ int splbm_dev_step_part(splbm_dev_engine* e, int part);
 int splbm_dev_halo_pack_next(splbm_dev_engine* e, void* low_dev, void* high_dev);
 int splbm_dev_halo_unpack(splbm_dev_engine* e, const void* low_dev, const void* high_dev);
 
+/* Native exchange (no per-step host work beyond enqueueing): rank 0 creates an NCCL unique id
+ * (128 bytes) and every rank passes it to splbm_dev_comm_attach with its lower/upper slab
+ * neighbour (-1 at a non-periodic edge). From then on every splbm_dev_step[_async] step runs
+ * boundary planes -> pack -> NCCL send/recv on a side stream -> interior planes -> unpack. */
+int splbm_comm_unique_id(uint8_t* id_out);
+int splbm_dev_comm_attach(splbm_dev_engine* e, const uint8_t* id, int world, int rank,
+                          int lower_rank, int upper_rank);
+
 /* ---- self-test ------------------------------------------------------------------------------- */
 /* Runs the step kernel's velocity division u_k = m_k / rho (collision.hpp:48) on the device for n
  * (m0, m1, m2, rho) tuples; every quotient must equal IEEE division bit for bit. */

@@ -15,8 +15,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsplbm_b200.so")
 BUILD = os.path.join(ROOT, "build", "native")
-SOURCES = ["kernels.cu", "engine.cpp", "tiling.cpp", "geometry.cpp"]
-HEADERS = ["kernels.h", "lattice.cuh", "common.h", "tiling.h"]
+SOURCES = ["kernels.cu", "engine.cpp", "tiling.cpp", "geometry.cpp", "nccl_api.cpp"]
+HEADERS = ["kernels.h", "lattice.cuh", "common.h", "tiling.h", "nccl_api.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
@@ -60,7 +60,7 @@ def build(force: bool = False, verbose: bool = False, defines: list[str] | None 
         subprocess.run(cmd, check=True)
     if force or not _newer(out_lib, objs):
         tmp = out_lib + ".tmp"
-        subprocess.run([nvcc()] + ARCH + ["-shared", "-o", tmp] + objs + ["-lpthread"], check=True)
+        subprocess.run([nvcc()] + ARCH + ["-shared", "-o", tmp] + objs + ["-lpthread", "-ldl"], check=True)
         os.replace(tmp, out_lib)
     return out_lib
 

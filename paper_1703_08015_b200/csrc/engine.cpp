@@ -19,6 +19,7 @@
 
 #include "common.h"
 #include "kernels.h"
+#include "nccl_api.h"
 #include "tiling.h"
 
 using namespace splbm_host;
@@ -76,6 +77,13 @@ struct splbm_dev_engine {
   bool batch_timed = false;
   long pending_steps = 0;
   std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
+  // native slab halo exchange (NCCL point-to-point on a side stream, overlapped with part 2)
+  ncclComm_t comm = nullptr;
+  int lower_rank = -1, upper_rank = -1;
+  double* halo_buf[4] = {nullptr, nullptr, nullptr, nullptr};  // send_low, send_high, recv_low, recv_high
+  uint64_t halo_n[4] = {0, 0, 0, 0};                              // doubles in each
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_packed = nullptr, ev_arrived = nullptr;
   double* pinned = nullptr;  // host staging for fields() (page-locked, grown on demand)
   std::size_t pinned_count = 0;
 
@@ -92,6 +100,12 @@ struct splbm_dev_engine {
 
   ~splbm_dev_engine() {
     if (device >= 0) cudaSetDevice(device);
+    if (comm) nccl().CommDestroy(comm);
+    for (double* b : halo_buf)
+      if (b) cudaFree(b);
+    if (ev_packed) cudaEventDestroy(ev_packed);
+    if (ev_arrived) cudaEventDestroy(ev_arrived);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     for (void* p : {static_cast<void*>(pdf[0]), static_cast<void*>(pdf[1]),
                     static_cast<void*>(info), static_cast<void*>(nb), static_cast<void*>(failed),
@@ -168,6 +182,49 @@ struct splbm_dev_engine {
     visits += n_own;
   }
 
+  // Face pack / unpack on the engine stream (see splbm_dev_halo_pack / _unpack for the layout).
+  void halo_copy(int copy, uint64_t tile0, uint64_t ntiles, int layer, const int* dirs, double* buf,
+                 bool pack) {
+    if (!ntiles || !buf) return;
+    splbm_dev::HaloArgs h{pdf[copy], buf, tile0, ntiles, a, layer, n_halo_dirs, dirs, pack ? 1 : 0};
+    CK(splbm_dev::launch_halo(d, h, stream));
+    ++launches;
+  }
+  void pack_faces(int copy, double* low, double* high) {
+    halo_copy(copy, n_low, send_low_tiles, 0, halo_dirs + n_halo_dirs, low, true);
+    halo_copy(copy, n_low + n_own - send_high_tiles, send_high_tiles, a - 1, halo_dirs, high, true);
+  }
+  void unpack_faces(int copy, double* low, double* high) {
+    halo_copy(copy, 0, n_low, a - 1, halo_dirs, low, false);
+    halo_copy(copy, n_low + n_own, n_high, 0, halo_dirs + n_halo_dirs, high, false);
+  }
+
+  // One step of the multi-GPU slab mode: boundary planes, pack their faces, NCCL send/recv on the
+  // comm stream (one group, order [send up, recv below, send down, recv above] as
+  // slab.HaloExchange), interior planes overlapping the transfer, then unpack into the halo planes.
+  void exchange_step() {
+    step_part(1);
+    const int next = 1 - read;
+    pack_faces(next, lower_rank >= 0 ? halo_buf[0] : nullptr, upper_rank >= 0 ? halo_buf[1] : nullptr);
+    CK(cudaEventRecord(ev_packed, stream));
+    CK(cudaStreamWaitEvent(comm_stream, ev_packed, 0));
+    const NcclApi& N = nccl();
+    nccl_check(N.GroupStart(), "ncclGroupStart");
+    if (upper_rank >= 0 && halo_n[1])
+      nccl_check(N.Send(halo_buf[1], halo_n[1], ncclFloat64, upper_rank, comm, comm_stream), "ncclSend");
+    if (lower_rank >= 0 && halo_n[2])
+      nccl_check(N.Recv(halo_buf[2], halo_n[2], ncclFloat64, lower_rank, comm, comm_stream), "ncclRecv");
+    if (lower_rank >= 0 && halo_n[0])
+      nccl_check(N.Send(halo_buf[0], halo_n[0], ncclFloat64, lower_rank, comm, comm_stream), "ncclSend");
+    if (upper_rank >= 0 && halo_n[3])
+      nccl_check(N.Recv(halo_buf[3], halo_n[3], ncclFloat64, upper_rank, comm, comm_stream), "ncclRecv");
+    nccl_check(N.GroupEnd(), "ncclGroupEnd");
+    CK(cudaEventRecord(ev_arrived, comm_stream));
+    step_part(2);
+    CK(cudaStreamWaitEvent(stream, ev_arrived, 0));
+    unpack_faces(read, lower_rank >= 0 ? halo_buf[2] : nullptr, upper_rank >= 0 ? halo_buf[3] : nullptr);
+  }
+
   // Enqueue k steps starting from parity rd (direct launches) + the counter bump.
   void enqueue_direct(int rd, int k) {
     for (int r = 0; r < k; ++r) {
@@ -204,6 +261,10 @@ struct splbm_dev_engine {
   }
 
   void enqueue_steps(long n) {
+    if (comm) {  // slab mode with a native communicator: every step exchanges faces
+      for (long k = 0; k < n; ++k) exchange_step();
+      return;
+    }
     long left = n;
     while (left >= kGraphSteps) {
       CK(cudaGraphLaunch(graph_for(read), stream));
@@ -483,7 +544,7 @@ int splbm_dev_step_async(splbm_dev_engine* e, long nsteps) {
       CK(cudaMemsetAsync(e->failed, 0xff, sizeof(unsigned long long), e->stream));
     }
     // instantiate the batch graph (host work) before the timing event, not inside the batch
-    if (nsteps >= kGraphSteps) e->graph_for(e->read);
+    if (nsteps >= kGraphSteps && !e->comm) e->graph_for(e->read);
     CK(cudaEventRecord(e->ev0, e->stream));
     e->enqueue_steps(nsteps);
     CK(cudaEventRecord(e->ev1, e->stream));
@@ -671,29 +732,16 @@ int splbm_dev_halo_recv_bytes(const splbm_dev_engine* e, uint64_t* low_bytes, ui
 int splbm_dev_halo_pack(splbm_dev_engine* e, void* low_dev, void* high_dev) {
   return guarded([&] {
     checked(e);
-    const int nd = e->n_halo_dirs;
-    if (low_dev && e->send_low_tiles) {
-      splbm_dev::HaloArgs h{e->pdf[e->read], static_cast<double*>(low_dev), e->n_low,
-                            e->send_low_tiles, e->a, 0, nd, e->halo_dirs + nd, 1};
-      CK(splbm_dev::launch_halo(e->d, h, e->stream));
-      ++e->launches;
-    }
-    if (high_dev && e->send_high_tiles) {
-      splbm_dev::HaloArgs h{e->pdf[e->read], static_cast<double*>(high_dev),
-                            e->n_low + e->n_own - e->send_high_tiles, e->send_high_tiles, e->a,
-                            e->a - 1, nd, e->halo_dirs, 1};
-      CK(splbm_dev::launch_halo(e->d, h, e->stream));
-      ++e->launches;
-    }
+    e->pack_faces(e->read, static_cast<double*>(low_dev), static_cast<double*>(high_dev));
   });
 }
 
 // pack_next: as pack, from the copy the in-flight step is writing (after step part 1).
 int splbm_dev_halo_pack_next(splbm_dev_engine* e, void* low_dev, void* high_dev) {
-  e->read = 1 - e->read;
-  const int rc = splbm_dev_halo_pack(e, low_dev, high_dev);
-  e->read = 1 - e->read;
-  return rc;
+  return guarded([&] {
+    checked(e);
+    e->pack_faces(1 - e->read, static_cast<double*>(low_dev), static_cast<double*>(high_dev));
+  });
 }
 
 // unpack: low_dev (the lower neighbour's high face) -> low halo plane, layer a-1, upward dirs;
@@ -701,40 +749,41 @@ int splbm_dev_halo_pack_next(splbm_dev_engine* e, void* low_dev, void* high_dev)
 int splbm_dev_halo_unpack(splbm_dev_engine* e, const void* low_dev, const void* high_dev) {
   return guarded([&] {
     checked(e);
-    const int nd = e->n_halo_dirs;
-    if (low_dev && e->n_low) {
-      splbm_dev::HaloArgs h{e->pdf[e->read], const_cast<double*>(static_cast<const double*>(low_dev)),
-                            0, e->n_low, e->a, e->a - 1, nd, e->halo_dirs, 0};
-      CK(splbm_dev::launch_halo(e->d, h, e->stream));
-      ++e->launches;
-    }
-    if (high_dev && e->n_high) {
-      splbm_dev::HaloArgs h{e->pdf[e->read], const_cast<double*>(static_cast<const double*>(high_dev)),
-                            e->n_low + e->n_own, e->n_high, e->a, 0, nd, e->halo_dirs + nd, 0};
-      CK(splbm_dev::launch_halo(e->d, h, e->stream));
-      ++e->launches;
-    }
+    e->unpack_faces(e->read, const_cast<double*>(static_cast<const double*>(low_dev)),
+                    const_cast<double*>(static_cast<const double*>(high_dev)));
   });
 }
 
-int splbm_selftest_divide(uint64_t n, const double* m3, const double* rho, double* out3) {
+int splbm_comm_unique_id(uint8_t* id_out) {
   return guarded([&] {
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
-      throw Error(SPLBM_ERR_CUDA, "no CUDA device available");
-    double *dm = nullptr, *dr = nullptr, *dout = nullptr;
-    const std::size_t nb = std::max<uint64_t>(n, 1) * 8;
-    CK(cudaMalloc(&dm, 3 * nb));
-    CK(cudaMalloc(&dr, nb));
-    CK(cudaMalloc(&dout, 3 * nb));
-    cudaError_t err = cudaMemcpy(dm, m3, 3 * n * 8, cudaMemcpyHostToDevice);
-    if (err == cudaSuccess) err = cudaMemcpy(dr, rho, n * 8, cudaMemcpyHostToDevice);
-    if (err == cudaSuccess) err = splbm_dev::launch_divide_selftest(n, dm, dr, dout, nullptr);
-    if (err == cudaSuccess) err = cudaMemcpy(out3, dout, 3 * n * 8, cudaMemcpyDeviceToHost);
-    cudaFree(dm);
-    cudaFree(dr);
-    cudaFree(dout);
-    CK(err);
+    if (!id_out) throw config_error("null argument");
+    ncclUniqueId id;
+    nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(id_out, id.internal, sizeof(id.internal));
+  });
+}
+
+int splbm_dev_comm_attach(splbm_dev_engine* e, const uint8_t* id, int world, int rank,
+                          int lower_rank, int upper_rank) {
+  return guarded([&] {
+    checked(e);
+    if (e->comm) throw config_error("engine already has a communicator");
+    if (!id || world < 1 || rank < 0 || rank >= world || lower_rank >= world || upper_rank >= world)
+      throw config_error("invalid communicator arguments");
+    ncclUniqueId uid;
+    std::memcpy(uid.internal, id, sizeof(uid.internal));
+    const uint64_t face = static_cast<uint64_t>(e->n_tn / e->a) * e->n_halo_dirs;
+    e->halo_n[0] = e->send_low_tiles * face;
+    e->halo_n[1] = e->send_high_tiles * face;
+    e->halo_n[2] = e->n_low * face;
+    e->halo_n[3] = e->n_high * face;
+    for (int k = 0; k < 4; ++k) e->halo_buf[k] = e->alloc<double>(e->halo_n[k]);
+    CK(cudaStreamCreateWithFlags(&e->comm_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&e->ev_packed, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&e->ev_arrived, cudaEventDisableTiming));
+    e->lower_rank = lower_rank;
+    e->upper_rank = upper_rank;
+    nccl_check(nccl().CommInitRank(&e->comm, world, uid, rank), "ncclCommInitRank");
   });
 }
 

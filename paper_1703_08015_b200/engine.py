@@ -234,6 +234,20 @@ class TileEngineT2C:
     def halo_pack(self, low_ptr: int, high_ptr: int) -> None:
         _native.check(self._L.splbm_dev_halo_pack(self._h, low_ptr or None, high_ptr or None))
 
+    def comm_attach(self, uid: bytes, world: int, rank: int, lower: int | None,
+                    upper: int | None) -> None:
+        """Native NCCL halo exchange for the slab mode (splbm_dev_comm_attach)."""
+        buf = C.create_string_buffer(bytes(uid), 128)
+        _native.check(self._L.splbm_dev_comm_attach(self._h, buf, int(world), int(rank),
+                                                    -1 if lower is None else int(lower),
+                                                    -1 if upper is None else int(upper)))
+
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _native.check(_native.lib().splbm_comm_unique_id(buf))
+        return buf.raw
+
     def step_part(self, part: int) -> None:
         _native.check(self._L.splbm_dev_step_part(self._h, int(part)))
 

@@ -210,7 +210,7 @@ class SlabRun:
     overlapped with the interior tiles of every step."""
 
     def __init__(self, g: Geometry, a: int, model, periodic, rank: int, world: int, device: int,
-                 slabs=None, host_staged: bool = False):
+                 slabs=None, host_staged: bool = False, native: bool = False):
         import torch
         from .engine import TileEngineT2C
         per = Periodicity.of(periodic)
@@ -222,9 +222,20 @@ class SlabRun:
         axis_periodic = per.axis(2 if g.d == 3 else 1)
         self.stream = torch.cuda.ExternalStream(self.engine.stream_handle(), device=device)
         dev = torch.device("cuda", device)
-        self.xchg = HaloExchange(rank, world, axis_periodic, self.engine.halo_bytes(),
-                                 lambda n: torch.empty(n, dtype=torch.float64, device=dev),
-                                 TorchComm(self.stream, host_staged=host_staged))
+        self.native = native and world > 1
+        if self.native:
+            # the engine runs the whole step sequence itself: NCCL send/recv from C++ on a side
+            # stream, no per-step Python; rank 0's unique id reaches the others via torch.distributed
+            import torch.distributed as dist
+            uid = [TileEngineT2C.comm_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            lower, upper = neighbours(rank, world, axis_periodic)
+            self.engine.comm_attach(uid[0], world, rank, lower, upper)
+            self.xchg = None
+        else:
+            self.xchg = HaloExchange(rank, world, axis_periodic, self.engine.halo_bytes(),
+                                     lambda n: torch.empty(n, dtype=torch.float64, device=dev),
+                                     TorchComm(self.stream, host_staged=host_staged))
 
     def _pack(self, lo, hi):
         self.engine.halo_pack_next(lo.data_ptr() if lo.numel() else 0,
@@ -237,7 +248,7 @@ class SlabRun:
     def step_async(self, n: int) -> None:
         """n steps: boundary planes -> pack -> start exchange -> interior planes (overlapping the
         transfers) -> complete exchange -> unpack; all ordered on the engine stream."""
-        if self.world == 1:
+        if self.world == 1 or self.native:
             self.engine.step_async(n)
             return
         for _ in range(n):
@@ -263,7 +274,8 @@ def bench_main(args, P) -> int:
     g = P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=(128, 128, 128 * world)))
     L = g.dims[2] // 4
     slabs = [(r * L // world, (r + 1) * L // world) for r in range(world)]
-    run = SlabRun(g, 4, P.FluidModel(tau=0.8), None, rank, world, local, slabs=slabs)
+    run = SlabRun(g, 4, P.FluidModel(tau=0.8), None, rank, world, local, slabs=slabs,
+                  native=os.environ.get("SPLBM_TORCH_COMM") != "1")
     dist.barrier()  # communicators up before the first point-to-point batch
     eng = run.engine
     eng.initialize_uniform()

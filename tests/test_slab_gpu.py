@@ -76,3 +76,19 @@ def test_slab_engines_match_whole(name, world):
         f = e.fields()
         rho += f.rho
     assert np.array_equal(rho, wf.rho)
+
+
+def test_native_comm_attach_single_rank():
+    """The native exchange path (splbm_dev_comm_attach: NCCL communicator, side stream, split
+    boundary/interior step) on a one-rank communicator steps exactly like the plain engine."""
+    from oracle import oracle as O
+    g, a, per = CASES["channel3d"][0](), 4, 0
+    m = P.FluidModel(tau=0.8)
+    e1 = P.TileEngineT2C(g, a, m, per)
+    e2 = P.TileEngineT2C(g, a, m, per)
+    e2.comm_attach(P.TileEngineT2C.comm_unique_id(), 1, 0, None, None)
+    for e in (e1, e2):
+        e.initialize(O.wavy)
+        assert e.step_n(33) == (True, 0)
+    assert np.array_equal(e1.get_pdf(), e2.get_pdf())
+    assert e2.current_step() == 33 and e2.tile_visits() == e1.tile_visits()
