@@ -787,4 +787,25 @@ int splbm_dev_comm_attach(splbm_dev_engine* e, const uint8_t* id, int world, int
   });
 }
 
+int splbm_selftest_divide(uint64_t n, const double* m3, const double* rho, double* out3) {
+  return guarded([&] {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw Error(SPLBM_ERR_CUDA, "no CUDA device available");
+    double *dm = nullptr, *dr = nullptr, *dout = nullptr;
+    const std::size_t nb = std::max<uint64_t>(n, 1) * 8;
+    CK(cudaMalloc(&dm, 3 * nb));
+    CK(cudaMalloc(&dr, nb));
+    CK(cudaMalloc(&dout, 3 * nb));
+    cudaError_t err = cudaMemcpy(dm, m3, 3 * n * 8, cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = cudaMemcpy(dr, rho, n * 8, cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = splbm_dev::launch_divide_selftest(n, dm, dr, dout, nullptr);
+    if (err == cudaSuccess) err = cudaMemcpy(out3, dout, 3 * n * 8, cudaMemcpyDeviceToHost);
+    cudaFree(dm);
+    cudaFree(dr);
+    cudaFree(dout);
+    CK(err);
+  });
+}
+
 }  // extern "C"
