@@ -1,0 +1,68 @@
+"""Regenerates profiles/README.md from profiles/ncu_step_kernel.json, profiles/bench_r1.json and
+profiles/launches_r1.csv."""
+import csv
+import json
+import os
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PR = os.path.join(ROOT, "profiles")
+ALG = {"channel3d_128": 2032128 * 304, "ras256_phi05": 8540134 * 304,
+       "ras256_phi02": 3513249 * 304, "cavity2d_4096_a4": 16764930 * 144}
+
+
+def launches():
+    rows = list(csv.reader(open(os.path.join(PR, "launches_r1.csv"))))
+    hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h = rows[hdr]
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    agg, order = defaultdict(list), []
+    for r in rows[hdr + 1:]:
+        if len(r) > vi:
+            if r[ki] not in agg:
+                order.append(r[ki])
+            agg[r[ki]].append(float(r[vi].replace(",", "")) / 1000.0)
+    tot = sum(sum(v) for v in agg.values())
+    out = ["| kernel | launches | mean us | total us | share |", "|---|---|---|---|---|"]
+    for k in order:
+        v = agg[k]
+        out.append(f"| `{k}` | {len(v)} | {sum(v) / len(v):.1f} | {sum(v):.1f} | {100 * sum(v) / tot:.1f}% |")
+    return out
+
+
+def main():
+    d = json.load(open(os.path.join(PR, "ncu_step_kernel.json")))
+    b = json.load(open(os.path.join(PR, "bench_r1.json")))
+    L = ["# Round-1 profiles (B200, sm_100a)", "",
+         "* `ncu_step_kernel.json`: one `ncu --set full --clock-control none --import-source on -k regex:t2c_step -s 3 -c 1 python tools/profile_case.py <case> 5` capture per workload, summarised by `tools/ncu_summary.py`.",
+         "* `launches_r1.csv`: `ncu --metrics gpu__time_duration.sum --clock-control none -c 200 python bench.py --steps 50 --warmup 3 --no-sweep --no-cpu` (cold-cache, serialised per-launch times: compare shares, not absolutes).",
+         "* `bench_r1.json`: the `python bench.py` line of the same code.", "",
+         "## Step kernel per launch (ncu)", "",
+         "| workload | kernel | us | DRAM read MB | DRAM write MB | DRAM / algorithmic | DRAM % of peak | issue active % | warps active % | regs | top stalls |",
+         "|---|---|---|---|---|---|---|---|---|---|---|"]
+    for k, r in d.items():
+        st = ", ".join(f"{n} {v}%" for n, v in list(r["top_stalls_pct"].items())[:3])
+        L.append(f"| {k} | `{r['kernel'].split('(')[0]}` | {r['duration_us']:.1f} | {r['dram_read_bytes'] / 1e6:.0f} | "
+                 f"{r['dram_write_bytes'] / 1e6:.0f} | {r['dram_bytes_per_launch'] / ALG[k]:.3f} | {r['dram_pct_peak']:.1f} | "
+                 f"{r['issue_active_pct']:.1f} | {r['warps_active_pct']:.1f} | {r['registers']:.0f} | {st} |")
+    L += ["", "Dense cases read DRAM/algorithmic slightly below 1: part of the written copy is still dirty in L2 when a "
+          "single profiled kernel ends; in steady state those writes reach DRAM during the next step. Sparse media read "
+          "whole 32-B sectors of partially solid rows: for RAS 256^3 phi 0.21 the geometric minimum is 1.18x the fluid "
+          "bytes (computed from the tile map), measured 1.28x.", "",
+          "## Launch list (bench command)", ""] + launches()
+    L += ["", "## Bench line (device-timed batches, steady state)", "",
+          f"* configs[1] channel 128^3: **{b['value']} MLUPS**, {b['ms_per_step'] * 1e3:.1f} us/step, {b['roofline']['achieved']} GB/s "
+          f"algorithmic = **{b['roofline']['frac']} of the measured copy peak** ({b['roofline']['peak']} GB/s); clocks {b['clocks']}",
+          f"* e2e, public API with host buffers (pinned NodeInit H2D, 1000 steps, fields D2H): {b['e2e']['value']} MLUPS",
+          f"* CPU reference T2C engine, {b['cpu_baseline']['cores']} host threads: {b['cpu_baseline']['value']} MLUPS", "",
+          "| phi | phi_t | MLUPS | GB/s algorithmic | frac of copy peak | BU of 8 TB/s |", "|---|---|---|---|---|---|"]
+    for r in b["porosity_sweep"]:
+        L.append(f"| {r['phi']} | {r['phi_t']} | {r['mlups']} | {r['achieved_gbs']} | {r['frac_of_measured_peak']} | {r['bu_of_8tbs']} |")
+    L += ["", "| other config | us/step | MLUPS | GB/s algorithmic | frac |", "|---|---|---|---|---|"]
+    for r in b["other_configs"]:
+        L.append(f"| {r['config']} | {r['us_per_step']} | {r['mlups']} | {r['achieved_gbs']} | {r['frac_of_measured_peak']} |")
+    open(os.path.join(PR, "README.md"), "w").write("\n".join(L) + "\n")
+
+
+if __name__ == "__main__":
+    main()
