@@ -347,6 +347,42 @@ def run_ours(args):
     return 0
 
 
+def run_big(args):
+    """--config ras1024: BASELINE configs[4] on ONE B200 (the 1-GPU point of the 1024^3 curve):
+    RAS 1024^3, d=40, seed 7, periodic, tiles 4^3, porosity --phi (only phi <~ 0.35 fits with two
+    PDF copies in 180 GB)."""
+    import paper_1703_08015_b200 as P
+    peak, peak_kind = measured_peaks()
+    t0 = time.time()
+    g = P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(1024, 1024, 1024), sphere_diameter=40,
+                                                          target_porosity=args.phi, seed=7))
+    t_gen = time.time() - t0
+    t0 = time.time()
+    eng = P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8), (1, 1, 1))
+    t_build = time.time() - t0
+    eng.initialize_uniform(1.0, (0.01, 0.005, 0.0))
+    ms, launches, clocks = time_steps(eng, args.steps, args.warmup)
+    nf = eng.fluid_nodes()
+    mlups = nf * args.steps / (ms * 1e-3) / 1e6
+    gbs = mlups * 1e6 * B_NODE[3] / 1e9
+    red = eng.reduce()
+    print(json.dumps({
+        "metric": "MLUPS (D3Q19 fp64 BGK) vs porosity; % of HBM peak GB/s; at 1/2/4/8 B200",
+        "value": round(mlups, 1), "unit": "MLUPS", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"configs[4] RAS 1024^3 d=40 seed 7 periodic, phi target {args.phi}",
+                   "phi": round(P.porosity(g).phi, 4), "phi_t": round(eng.info.phi_t, 4),
+                   "tiles": int(eng.info.n_tiles), "fluid_nodes": nf,
+                   "device_gb": round(eng.info.device_bytes / 1e9, 1)},
+        "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(gbs / peak, 4), "peak_source": peak_kind},
+        "gpu_launches": int(launches), "clocks": clocks, "mass": red["mass"],
+        "non_finite": red["non_finite"], "host_seconds": {"generate": round(t_gen, 1),
+                                                         "engine_build": round(t_build, 1)}}))
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -355,11 +391,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--config", default="default", choices=["default", "ras1024"])
+    ap.add_argument("--phi", type=float, default=0.2)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.config == "ras1024":
+        return run_big(args)
     return run_ours(args)
 
 

@@ -66,6 +66,9 @@ CASES = {
     "channel3d_32": (lambda: P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=(32, 20, 20))), 4, 0.8, False, 0, "uniform"),
     "channel3d_32_incompr": (lambda: P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=(30, 18, 21))), 4, 0.8, True, 0, "uniform"),
     "ras48_periodic_a4": (lambda: P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(48, 48, 48), sphere_diameter=10, target_porosity=0.8, seed=42)), 4, 0.7, False, 7, "wavy"),
+    "cavity3d_a8_generic": (lambda: P.generate(P.GeometryKind.Cavity3D, P.GenerateParams(dims=(20, 17, 19))), 8, 0.8, False, 0, "uniform"),
+    "random_solids_a5_generic": (lambda: random_solids((23, 14, 11), seed=5, frac=0.25), 5, 0.9, True, 0, "wavy"),
+    "full2d_periodic_a8": (lambda: P.Geometry.filled(2, (40, 24, 1)), 8, 0.7, False, 3, "wavy"),
     "vessel_256": (lambda: P.generate(P.GeometryKind.Vessel2D, P.GenerateParams(dims=(256, 256, 1), target_porosity=0.3, seed=3)), 4, 0.8, False, 0, "uniform"),
 }
 
