@@ -1,0 +1,64 @@
+"""CLI subcommands in the reference's key=value format and exit codes (test_cli.cpp analogue)."""
+import io
+import subprocess
+import sys
+
+import pytest
+
+import paper_1703_08015_b200 as P
+from paper_1703_08015_b200 import cli
+
+
+def run(argv):
+    out = io.StringIO()
+    rc = cli.main(argv, out=out)
+    kv = dict(line.split("=", 1) for line in out.getvalue().splitlines() if "=" in line)
+    return rc, kv
+
+
+def test_generate_and_reload(tmp_path):
+    path = str(tmp_path / "ras.splb")
+    rc, kv = run(["generate", path, "--set", "geometry.kind=ras3d", "--set", "geometry.dims=32 32 32",
+                  "--set", "geometry.diameter=8", "--set", "geometry.porosity=0.7",
+                  "--set", "geometry.seed=3"])
+    assert rc == 0 and kv["nodes"] == "32768" and kv["output"] == path
+    g = P.load_geometry_file(path)
+    assert abs(float(kv["phi"]) - P.porosity(g).phi) < 1e-12
+
+
+def test_stats_matches_library(tmp_path):
+    cfgf = tmp_path / "c.cfg"
+    cfgf.write_text("geometry.kind = cavity2d\ngeometry.dims = 33 32\nsim.tile = 16  # reference default\n")
+    rc, kv = run(["stats", "-c", str(cfgf)])
+    assert rc == 0
+    g = P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(33, 32, 1)))
+    assert float(kv["phi_t"]) == pytest.approx(P.tile_stats(P.build_tile_grid(g, 16)).phi_t, abs=1e-12)
+    assert kv["n_tiles"] == "6" and "t2c.delta_b" in kv and "t2c.delta_b_bt" in kv
+
+
+def test_exit_codes():
+    assert run(["stats"])[0] == cli.EXIT_CONFIG  # no geometry
+    assert run(["stats", "--set", "geometry.kind=nope"])[0] == cli.EXIT_CONFIG
+    assert run(["run", "--set", "geometry.kind=cavity2d", "--set", "geometry.dims=16 16",
+                "--set", "sim.collision=mrt"])[0] == cli.EXIT_CONFIG
+
+
+def test_module_entry_point():
+    r = subprocess.run([sys.executable, "-m", "paper_1703_08015_b200", "stats", "--set",
+                        "geometry.kind=channel3d", "--set", "geometry.dims=16 12 12"],
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "phi_t=" in r.stdout
+
+
+@pytest.mark.gpu
+def test_run_and_bench_on_device():
+    rc, kv = run(["run", "--set", "geometry.kind=cavity2d", "--set", "geometry.dims=64 64",
+                  "--set", "sim.steps=100", "--set", "sim.tile=16"])
+    assert rc == 0 and kv["steps"] == "100" and float(kv["mlups"]) > 0
+    assert int(kv["tile_visits"]) == 100 * 16
+    rc, kv = run(["bench", "--set", "geometry.kind=channel3d", "--set", "geometry.dims=64 32 32",
+                  "--set", "bench.steps=40", "--set", "bench.mem_bandwidth=6.537e12",
+                  "--set", "bench.models=bgk-quasi bgk-incompressible"])
+    assert rc == 0 and float(kv["bench.t2c-b200.bgk-quasi.mlups"]) > 0
+    mlups = float(kv["bench.t2c-b200.bgk-incompressible.mlups"])
+    assert float(kv["bench.t2c-b200.bgk-incompressible.bu"]) == pytest.approx(mlups * 1e6 * 304 / 6.537e12, rel=1e-5)
