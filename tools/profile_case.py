@@ -2,7 +2,9 @@
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 import paper_1703_08015_b200 as P  # noqa: E402
 
 CASES = {
@@ -10,6 +12,10 @@ CASES = {
     "ras256_phi02": lambda: (P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(256, 256, 256), sphere_diameter=40, target_porosity=0.2, seed=7)), 4, 7),
     "ras256_phi05": lambda: (P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(256, 256, 256), sphere_diameter=40, target_porosity=0.5, seed=7)), 4, 7),
     "cavity2d_4096_a4": lambda: (P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(4096, 4096, 1))), 4, 0),
+    "ras48_periodic": lambda: (P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(48, 48, 48), sphere_diameter=12, target_porosity=0.5, seed=2)), 4, 7),
+    "channel3d_small": lambda: (P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=(30, 18, 21))), 4, 0),
+    "cavity2d_64_a16": lambda: (P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(64, 64, 1))), 16, 0),
+    "random_a3": lambda: (__import__("cases").random_solids((23, 14, 11), seed=5, frac=0.25), 3, 0),
     "vessel4096_a4": lambda: (P.generate(P.GeometryKind.Vessel2D, P.GenerateParams(dims=(4096, 4096, 1), target_porosity=0.2, seed=1)), 4, 0),
 }
 
@@ -20,4 +26,6 @@ if __name__ == "__main__":
     e = P.TileEngineT2C(g, a, P.FluidModel(tau=0.8), per)
     e.initialize_uniform(1.0, (0.01, 0.0, 0.0))
     ok, _ = e.step_n(steps)
+    e.fields()
+    e.reduce()
     print(name, "ok" if ok else "FAILED", "fluid nodes", e.fluid_nodes(), "tiles", e.info.n_tiles)
