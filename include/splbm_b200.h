@@ -222,6 +222,16 @@ int splbm_comm_unique_id(uint8_t* id_out);
 int splbm_dev_comm_attach(splbm_dev_engine* e, const uint8_t* id, int world, int rank,
                           int lower_rank, int upper_rank);
 
+/* Fused NVLink exchange: the boundary-plane step kernel stores its face values straight into the
+ * neighbours' halo tiles (peer memory over NVLink; CUDA IPC across processes), ordered by 64-bit
+ * flags with GPU-side stream waits/writes — no pack, no unpack, no host synchronisation. Every rank
+ * exports its blob (SPLBM_IPC_BLOB_BYTES bytes), the blobs reach the neighbours out of band, then
+ * each rank attaches its lower/upper neighbour's blob (NULL at a non-periodic edge). All ranks
+ * must initialize before any rank steps. */
+#define SPLBM_IPC_BLOB_BYTES 512
+int splbm_dev_ipc_blob(splbm_dev_engine* e, uint8_t* blob_out);
+int splbm_dev_p2p_attach(splbm_dev_engine* e, const uint8_t* lower_blob, const uint8_t* upper_blob);
+
 /* ---- self-test ------------------------------------------------------------------------------- */
 /* Runs the step kernel's velocity division u_k = m_k / rho (collision.hpp:48) on the device for n
  * (m0, m1, m2, rho) tuples; every quotient must equal IEEE division bit for bit. */

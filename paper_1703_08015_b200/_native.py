@@ -99,6 +99,8 @@ SIGNATURES = {
     "splbm_dev_halo_unpack": ([_vp, C.c_void_p, C.c_void_p], C.c_int),
     "splbm_dev_step_part": ([_vp, C.c_int], C.c_int),
     "splbm_comm_unique_id": ([C.c_void_p], C.c_int),
+    "splbm_dev_ipc_blob": ([_vp, C.c_void_p], C.c_int),
+    "splbm_dev_p2p_attach": ([_vp, C.c_void_p, C.c_void_p], C.c_int),
     "splbm_dev_comm_attach": ([_vp, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int], C.c_int),
     "splbm_dev_halo_pack_next": ([_vp, C.c_void_p, C.c_void_p], C.c_int),
     "splbm_selftest_divide": ([C.c_uint64, _dp, _dp, _dp], C.c_int),

@@ -6,7 +6,9 @@
 // and allocates the two PDF copies. step() enqueues fused step kernels on the engine stream
 // (batches are replayed from cached CUDA graphs) and reads back one 8-byte failure stamp per
 // batch. fields() computes moments on the device and scatters them to the raster on the host.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <climits>
@@ -36,6 +38,35 @@ void cuda_check(cudaError_t e, const char* what) {
     throw Error(SPLBM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 #define CK(x) cuda_check((x), #x)
+
+void cu_check(CUresult r, const char* what) {
+  if (r != CUDA_SUCCESS) throw Error(SPLBM_ERR_CUDA, std::string(what) + " failed (CUresult " + std::to_string(static_cast<int>(r)) + ")");
+}
+
+// Driver stream memory operations (GPU-side waits/writes on 64-bit flags), resolved through the
+// runtime's driver entry point so the library needs no link-time libcuda dependency.
+struct StreamMemOps {
+  CUresult (*wait)(CUstream, CUdeviceptr, cuuint64_t, unsigned int) = nullptr;
+  CUresult (*write)(CUstream, CUdeviceptr, cuuint64_t, unsigned int) = nullptr;
+};
+
+const StreamMemOps& stream_mem_ops() {
+  static StreamMemOps ops;
+  static bool done = false;
+  if (!done) {
+    cudaDriverEntryPointQueryResult q1, q2;
+    void* w = nullptr;
+    void* v = nullptr;
+    CK(cudaGetDriverEntryPoint("cuStreamWaitValue64", &w, cudaEnableDefault, &q1));
+    CK(cudaGetDriverEntryPoint("cuStreamWriteValue64", &v, cudaEnableDefault, &q2));
+    if (!w || !v || q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess)
+      throw Error(SPLBM_ERR_CUDA, "stream memory operations unavailable");
+    ops.wait = reinterpret_cast<decltype(ops.wait)>(w);
+    ops.write = reinterpret_cast<decltype(ops.write)>(v);
+    done = true;
+  }
+  return ops;
+}
 
 constexpr uint64_t kChunkNodes = 1ull << 22;  // init / moments staging (4 x 32 MB)
 #ifndef SPLBM_L2_FETCH
@@ -84,6 +115,16 @@ struct splbm_dev_engine {
   uint64_t halo_n[4] = {0, 0, 0, 0};                              // doubles in each
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_packed = nullptr, ev_arrived = nullptr;
+  // fused NVLink peer-store halo exchange (splbm_dev_p2p_attach)
+  bool p2p = false, peer_part1 = false;
+  unsigned long long* flags = nullptr;  // [0] faces from below arrived, [1] from above (step seq)
+  double* peer_pdf_up[2] = {nullptr, nullptr};
+  double* peer_pdf_down[2] = {nullptr, nullptr};
+  unsigned long long* peer_flags_up = nullptr;
+  unsigned long long* peer_flags_down = nullptr;
+  uint64_t peer_down_halo0 = 0;  // first high-halo tile of the lower neighbour
+  unsigned long long comm_seq = 0;
+  std::vector<void*> ipc_opened;
   double* pinned = nullptr;  // host staging for fields() (page-locked, grown on demand)
   std::size_t pinned_count = 0;
 
@@ -100,6 +141,9 @@ struct splbm_dev_engine {
 
   ~splbm_dev_engine() {
     if (device >= 0) cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
+    if (flags) cudaFree(flags);
     if (comm) nccl().CommDestroy(comm);
     for (double* b : halo_buf)
       if (b) cudaFree(b);
@@ -146,6 +190,13 @@ struct splbm_dev_engine {
     s.failed = failed;
     s.step_base = step_base;
     s.rel = rel;
+    if (peer_part1) {
+      s.peer_up = peer_pdf_up[1 - rd];
+      s.peer_down = peer_pdf_down[1 - rd] ? peer_pdf_down[1 - rd] + peer_down_halo0 * tile_stride() : nullptr;
+      s.top_begin = n_low + n_own - send_high_tiles;
+      s.bot_begin = n_low;
+      s.bot_end = n_low + send_low_tiles;
+    }
     return s;
   }
 
@@ -225,6 +276,28 @@ struct splbm_dev_engine {
     unpack_faces(read, lower_rank >= 0 ? halo_buf[2] : nullptr, upper_rank >= 0 ? halo_buf[3] : nullptr);
   }
 
+  // One slab step with the faces stored by the boundary-plane kernel straight into the neighbours'
+  // halo tiles (NVLink peer stores). Stream-ordered flags: before the boundary planes of step
+  // seq+1 wait until both neighbours finished their boundary planes of step seq (so my halos hold
+  // their faces and they no longer read the halo copy I am about to overwrite); afterwards publish
+  // seq+1 into the neighbours' flags.
+  void p2p_step() {
+    const StreamMemOps& ops = stream_mem_ops();
+    if (peer_pdf_down[0])
+      cu_check(ops.wait(stream, reinterpret_cast<CUdeviceptr>(&flags[0]), comm_seq, CU_STREAM_WAIT_VALUE_GEQ), "cuStreamWaitValue64");
+    if (peer_pdf_up[0])
+      cu_check(ops.wait(stream, reinterpret_cast<CUdeviceptr>(&flags[1]), comm_seq, CU_STREAM_WAIT_VALUE_GEQ), "cuStreamWaitValue64");
+    peer_part1 = true;
+    step_part(1);
+    peer_part1 = false;
+    ++comm_seq;
+    if (peer_pdf_up[0])  // the upper rank's "from below" flag
+      cu_check(ops.write(stream, reinterpret_cast<CUdeviceptr>(&peer_flags_up[0]), comm_seq, CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue64");
+    if (peer_pdf_down[0])  // the lower rank's "from above" flag
+      cu_check(ops.write(stream, reinterpret_cast<CUdeviceptr>(&peer_flags_down[1]), comm_seq, CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue64");
+    step_part(2);
+  }
+
   // Enqueue k steps starting from parity rd (direct launches) + the counter bump.
   void enqueue_direct(int rd, int k) {
     for (int r = 0; r < k; ++r) {
@@ -263,6 +336,10 @@ struct splbm_dev_engine {
   void enqueue_steps(long n) {
     if (comm) {  // slab mode with a native communicator: every step exchanges faces
       for (long k = 0; k < n; ++k) exchange_step();
+      return;
+    }
+    if (p2p) {  // slab mode with NVLink peer stores
+      for (long k = 0; k < n; ++k) p2p_step();
       return;
     }
     long left = n;
@@ -544,7 +621,7 @@ int splbm_dev_step_async(splbm_dev_engine* e, long nsteps) {
       CK(cudaMemsetAsync(e->failed, 0xff, sizeof(unsigned long long), e->stream));
     }
     // instantiate the batch graph (host work) before the timing event, not inside the batch
-    if (nsteps >= kGraphSteps && !e->comm) e->graph_for(e->read);
+    if (nsteps >= kGraphSteps && !e->comm && !e->p2p) e->graph_for(e->read);
     CK(cudaEventRecord(e->ev0, e->stream));
     e->enqueue_steps(nsteps);
     CK(cudaEventRecord(e->ev1, e->stream));
@@ -751,6 +828,91 @@ int splbm_dev_halo_unpack(splbm_dev_engine* e, const void* low_dev, const void* 
     checked(e);
     e->unpack_faces(e->read, const_cast<double*>(static_cast<const double*>(low_dev)),
                     const_cast<double*>(static_cast<const double*>(high_dev)));
+  });
+}
+
+// IPC blob of a slab engine: what a neighbour needs to store faces into this engine's halos.
+struct IpcBlob {
+  uint32_t magic, version;
+  int32_t pid, device;
+  cudaIpcMemHandle_t pdf[2], flags;
+  uint64_t raw_pdf[2], raw_flags;  // same-process peers use the pointers directly
+  uint64_t n_low, n_own, n_high, send_low_tiles, send_high_tiles, tile_stride;
+};
+static_assert(sizeof(IpcBlob) <= SPLBM_IPC_BLOB_BYTES, "blob too large");
+
+int splbm_dev_ipc_blob(splbm_dev_engine* e, uint8_t* out) {
+  return guarded([&] {
+    checked(e);
+    if (!out) throw config_error("null argument");
+    if (!e->flags) {
+      e->flags = e->alloc<unsigned long long>(2);
+      CK(cudaMemset(e->flags, 0, 2 * sizeof(unsigned long long)));
+    }
+    IpcBlob b{};
+    b.magic = 0x53504c42u;  // "SPLB"
+    b.version = 1;
+    b.pid = static_cast<int32_t>(getpid());
+    b.device = e->device;
+    for (int k = 0; k < 2; ++k) {
+      CK(cudaIpcGetMemHandle(&b.pdf[k], e->pdf[k]));
+      b.raw_pdf[k] = reinterpret_cast<uint64_t>(e->pdf[k]);
+    }
+    CK(cudaIpcGetMemHandle(&b.flags, e->flags));
+    b.raw_flags = reinterpret_cast<uint64_t>(e->flags);
+    b.n_low = e->n_low;
+    b.n_own = e->n_own;
+    b.n_high = e->n_high;
+    b.send_low_tiles = e->send_low_tiles;
+    b.send_high_tiles = e->send_high_tiles;
+    b.tile_stride = e->tile_stride();
+    std::memset(out, 0, SPLBM_IPC_BLOB_BYTES);
+    std::memcpy(out, &b, sizeof(b));
+  });
+}
+
+int splbm_dev_p2p_attach(splbm_dev_engine* e, const uint8_t* lower_blob, const uint8_t* upper_blob) {
+  return guarded([&] {
+    checked(e);
+    if (e->p2p || e->comm) throw config_error("engine already has a halo transport");
+    if (!e->flags) throw config_error("call splbm_dev_ipc_blob before attaching");
+    if (e->a != 4 && e->a != 2 && !(e->d == 2 && (e->a == 8 || e->a == 16)))
+      throw config_error("peer-store halos need a power-of-two tile kernel (a = 2, 4; 2D a <= 16)");
+    auto open = [&](const IpcBlob& b, double** pdf, unsigned long long** fl) {
+      if (b.magic != 0x53504c42u || b.version != 1 || b.tile_stride != e->tile_stride())
+        throw config_error("incompatible peer blob");
+      if (b.pid == static_cast<int32_t>(getpid())) {
+        pdf[0] = reinterpret_cast<double*>(b.raw_pdf[0]);
+        pdf[1] = reinterpret_cast<double*>(b.raw_pdf[1]);
+        *fl = reinterpret_cast<unsigned long long*>(b.raw_flags);
+        return;
+      }
+      for (int k = 0; k < 2; ++k) {
+        void* p = nullptr;
+        CK(cudaIpcOpenMemHandle(&p, b.pdf[k], cudaIpcMemLazyEnablePeerAccess));
+        e->ipc_opened.push_back(p);
+        pdf[k] = static_cast<double*>(p);
+      }
+      void* p = nullptr;
+      CK(cudaIpcOpenMemHandle(&p, b.flags, cudaIpcMemLazyEnablePeerAccess));
+      e->ipc_opened.push_back(p);
+      *fl = static_cast<unsigned long long*>(p);
+    };
+    if (lower_blob) {
+      IpcBlob b;
+      std::memcpy(&b, lower_blob, sizeof(b));
+      if (b.n_high != e->send_low_tiles) throw config_error("lower neighbour's halo does not match my bottom plane");
+      open(b, e->peer_pdf_down, &e->peer_flags_down);
+      e->peer_down_halo0 = b.n_low + b.n_own;
+    }
+    if (upper_blob) {
+      IpcBlob b;
+      std::memcpy(&b, upper_blob, sizeof(b));
+      if (b.n_low != e->send_high_tiles) throw config_error("upper neighbour's halo does not match my top plane");
+      open(b, e->peer_pdf_up, &e->peer_flags_up);
+    }
+    stream_mem_ops();
+    e->p2p = true;
   });
 }
 

@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kThreads) t2c_step_kernel(StepArgs args) {
 // the per-direction source address is pure integer arithmetic on compile-time lattice constants
 // plus one shared-memory lookup and two selects — no divergent branches, no dependent global load
 // before the PDF gather.
-template <int D, int LOGA, bool INC>
+template <int D, int LOGA, bool INC, bool PEER>
 __global__ void __launch_bounds__(kThreads, (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2)) t2c_step_pow2_kernel(StepArgs args) {
   constexpr int Q = Lat<D>::Q;
   constexpr int A = 1 << LOGA;
@@ -203,6 +203,23 @@ __global__ void __launch_bounds__(kThreads, (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2)
   if (!good) atomicMin(args.failed, static_cast<unsigned long long>(*args.step_base + args.rel + 1));
 #pragma unroll
   for (int i = 0; i < Q; ++i) st_stream(wr + i * NTN, f[i]);
+
+  // Slab faces straight into the neighbours' halo tiles over NVLink (fused with the step): the
+  // neighbour gathers exactly these slots (layer a-1 / 0, directions crossing the face).
+  if constexpr (!PEER) return;
+  const int lslab = D == 3 ? lz : ly;
+  if (args.peer_up && t >= args.top_begin && lslab == A - 1) {
+    double* dst = args.peer_up + (t - args.top_begin) * STRIDE + p;
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+      if ((D == 3 ? ez<D>(i) : ey<D>(i)) > 0) dst[i * NTN] = f[i];
+  }
+  if (args.peer_down && t >= args.bot_begin && t < args.bot_end && lslab == 0) {
+    double* dst = args.peer_down + (t - args.bot_begin) * STRIDE + p;
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+      if ((D == 3 ? ez<D>(i) : ey<D>(i)) < 0) dst[i * NTN] = f[i];
+  }
 }
 
 // Advances the step counter the failure stamps are relative to (one per enqueued batch).
@@ -433,6 +450,12 @@ __global__ void divide_selftest_kernel(uint64_t n, const double* m, const double
 // Launchers (host side of this translation unit)
 template <int D, int LOGA, bool INC>
 static void launch_pow2(const StepArgs& a, cudaStream_t st) {
+  if (a.peer_up || a.peer_down) {  // slab boundary planes with NVLink peer stores
+    constexpr int NTN_ = D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA));
+    const unsigned b = static_cast<unsigned>((a.n_nodes / NTN_ + kThreads / NTN_ - 1) / (kThreads / NTN_));
+    t2c_step_pow2_kernel<D, LOGA, INC, true><<<b, kThreads, 0, st>>>(a);
+    return;
+  }
   constexpr int NTN = D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA));
   constexpr int TILES = kThreads / NTN;
   const uint64_t tiles = a.n_nodes / NTN;
@@ -441,7 +464,7 @@ static void launch_pow2(const StepArgs& a, cudaStream_t st) {
   // Overlap the next step's launch and static-table prologue with this step's tail; below a few
   // waves (launch-latency-bound domains) the plain launch measured faster.
   if (blocks < 4u * 148u) {
-    t2c_step_pow2_kernel<D, LOGA, INC><<<blocks, kThreads, 0, st>>>(a);
+    t2c_step_pow2_kernel<D, LOGA, INC, false><<<blocks, kThreads, 0, st>>>(a);
     return;
   }
   cudaLaunchConfig_t cfg = {};
@@ -453,9 +476,9 @@ static void launch_pow2(const StepArgs& a, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, t2c_step_pow2_kernel<D, LOGA, INC>, a);
+  cudaLaunchKernelEx(&cfg, t2c_step_pow2_kernel<D, LOGA, INC, false>, a);
 #else
-  t2c_step_pow2_kernel<D, LOGA, INC><<<blocks, kThreads, 0, st>>>(a);
+  t2c_step_pow2_kernel<D, LOGA, INC, false><<<blocks, kThreads, 0, st>>>(a);
 #endif
 }
 

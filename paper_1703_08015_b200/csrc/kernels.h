@@ -21,6 +21,13 @@ struct StepArgs {
   unsigned long long* failed;  // min failing step number (ULLONG_MAX = none)
   const long long* step_base;  // steps completed before this batch
   int rel;                     // step index within the batch
+  // Slab mode, NVLink peer stores (power-of-two tile kernel only): the face layer of my top
+  // plane tiles [top_begin, ...) is also stored, for the directions leaving upwards, into the
+  // upper neighbour's next copy at its low halo tiles (peer_up = that copy's first halo tile);
+  // likewise the bottom plane [bot_begin, bot_end) into the lower neighbour's high halo tiles.
+  double* peer_up;
+  double* peer_down;
+  uint64_t top_begin, bot_begin, bot_end;
 };
 
 struct NodeInfoArgs {

@@ -242,6 +242,18 @@ class TileEngineT2C:
                                                     -1 if lower is None else int(lower),
                                                     -1 if upper is None else int(upper)))
 
+    def ipc_blob(self) -> bytes:
+        """What a slab neighbour needs to store faces into this engine (splbm_dev_ipc_blob)."""
+        buf = C.create_string_buffer(512)
+        _native.check(self._L.splbm_dev_ipc_blob(self._h, buf))
+        return buf.raw
+
+    def p2p_attach(self, lower_blob: bytes | None, upper_blob: bytes | None) -> None:
+        """Fused NVLink peer-store halo exchange with the slab neighbours (splbm_dev_p2p_attach)."""
+        lo = C.create_string_buffer(bytes(lower_blob), 512) if lower_blob else None
+        hi = C.create_string_buffer(bytes(upper_blob), 512) if upper_blob else None
+        _native.check(self._L.splbm_dev_p2p_attach(self._h, lo, hi))
+
     @staticmethod
     def comm_unique_id() -> bytes:
         buf = C.create_string_buffer(128)

@@ -210,7 +210,8 @@ class SlabRun:
     overlapped with the interior tiles of every step."""
 
     def __init__(self, g: Geometry, a: int, model, periodic, rank: int, world: int, device: int,
-                 slabs=None, host_staged: bool = False, native: bool = False):
+                 slabs=None, host_staged: bool = False, native: bool = False,
+                 transport: str | None = None):
         import torch
         from .engine import TileEngineT2C
         per = Periodicity.of(periodic)
@@ -222,17 +223,26 @@ class SlabRun:
         axis_periodic = per.axis(2 if g.d == 3 else 1)
         self.stream = torch.cuda.ExternalStream(self.engine.stream_handle(), device=device)
         dev = torch.device("cuda", device)
-        self.native = native and world > 1
-        if self.native:
+        # transport: "p2p" (fused NVLink peer stores), "nccl" (native NCCL), "torch" (HaloExchange)
+        transport = transport or ("nccl" if native else "torch")
+        self.transport = transport if world > 1 else "none"
+        self.native = self.transport in ("nccl", "p2p")
+        lower, upper = neighbours(rank, world, axis_periodic)
+        self.xchg = None
+        if self.transport == "p2p":
+            import torch.distributed as dist
+            blobs = [None] * world
+            dist.all_gather_object(blobs, self.engine.ipc_blob())
+            self.engine.p2p_attach(blobs[lower] if lower is not None else None,
+                                   blobs[upper] if upper is not None else None)
+        elif self.transport == "nccl":
             # the engine runs the whole step sequence itself: NCCL send/recv from C++ on a side
             # stream, no per-step Python; rank 0's unique id reaches the others via torch.distributed
             import torch.distributed as dist
             uid = [TileEngineT2C.comm_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(uid, src=0)
-            lower, upper = neighbours(rank, world, axis_periodic)
             self.engine.comm_attach(uid[0], world, rank, lower, upper)
-            self.xchg = None
-        else:
+        elif self.transport == "torch":
             self.xchg = HaloExchange(rank, world, axis_periodic, self.engine.halo_bytes(),
                                      lambda n: torch.empty(n, dtype=torch.float64, device=dev),
                                      TorchComm(self.stream, host_staged=host_staged))
@@ -244,6 +254,17 @@ class SlabRun:
     def _unpack(self, lo, hi):
         self.engine.halo_unpack(lo.data_ptr() if lo is not None and lo.numel() else 0,
                                 hi.data_ptr() if hi is not None and hi.numel() else 0)
+
+    def initialize(self, init=None) -> None:
+        """Initialise every rank, then a barrier: a neighbour's first step may already store its
+        faces into this rank's halo tiles, which initialisation must not overwrite afterwards."""
+        import torch.distributed as dist
+        if init is None:
+            self.engine.initialize_uniform()
+        else:
+            self.engine.initialize(init)
+        if self.world > 1:
+            dist.barrier()
 
     def step_async(self, n: int) -> None:
         """n steps: boundary planes -> pack -> start exchange -> interior planes (overlapping the
@@ -275,10 +296,10 @@ def bench_main(args, P) -> int:
     L = g.dims[2] // 4
     slabs = [(r * L // world, (r + 1) * L // world) for r in range(world)]
     run = SlabRun(g, 4, P.FluidModel(tau=0.8), None, rank, world, local, slabs=slabs,
-                  native=os.environ.get("SPLBM_TORCH_COMM") != "1")
-    dist.barrier()  # communicators up before the first point-to-point batch
+                  transport=os.environ.get("SPLBM_SLAB_TRANSPORT", "p2p"))
+    dist.barrier()  # transports up before the first step
     eng = run.engine
-    eng.initialize_uniform()
+    run.initialize()
     run.step_async(args.warmup)
     run.sync()
     start = torch.cuda.Event(enable_timing=True)

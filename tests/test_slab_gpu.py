@@ -92,3 +92,40 @@ def test_native_comm_attach_single_rank():
         assert e.step_n(33) == (True, 0)
     assert np.array_equal(e1.get_pdf(), e2.get_pdf())
     assert e2.current_step() == 33 and e2.tile_visits() == e1.tile_visits()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_p2p_peer_store_slabs_match_whole(name, world):
+    """Fused exchange: the boundary-plane kernel stores its faces straight into the neighbours'
+    halo tiles, ordered by GPU-side flag waits/writes (same-process peers on one GPU; across
+    processes the blob carries CUDA IPC handles). Bitwise equal to the single engine."""
+    from oracle import oracle as O
+    factory, a, per = CASES[name]
+    g = factory()
+    m = P.FluidModel(tau=0.8)
+    whole = P.TileEngineT2C(g, a, m, per)
+    whole.initialize(O.wavy)
+    slabs = slab.plan_slabs(slab.plane_tile_counts(g, a, per), world)
+    ranks = [P.TileEngineT2C(g, a, m, per, slab=s) for s in slabs]
+    blobs = [e.ipc_blob() for e in ranks]
+    ax_per = P.Periodicity.of(per).axis(2 if g.d == 3 else 1)
+    for r, e in enumerate(ranks):
+        lo, hi = slab.neighbours(r, world, ax_per)
+        e.p2p_attach(blobs[lo] if lo is not None else None, blobs[hi] if hi is not None else None)
+        e.initialize(O.wavy)
+    K = 11
+    for e in ranks:          # all ranks' steps enqueued; GPU-side flags order them
+        e.step_async(K)
+    for e in ranks:
+        assert e.sync() == (True, 0)
+    assert whole.step_n(K)[0]
+    tg = whole.tile_grid()
+    st = whole.q * whole.n_tn
+    wp = whole.get_pdf()
+    for r, e in enumerate(ranks):
+        lay = slab.slab_layout(g, a, per, *slabs[r])
+        g0, n = lay["g_own0"], lay["n_own"]
+        mine = e.get_pdf()[lay["n_low"] * st:(lay["n_low"] + n) * st]
+        fluid = np.broadcast_to((tg.types[g0:g0 + n] != 0)[:, None, :], (n, whole.q, whole.n_tn)).ravel()
+        assert np.array_equal(mine[fluid].view(np.uint64), wp[g0 * st:(g0 + n) * st][fluid].view(np.uint64))

@@ -1,7 +1,8 @@
-"""Multi-process slab mode on one B200: 2-3 ranks (processes) share cuda:0 and run SlabRun —
-overlapped boundary/interior step parts, pack_next, the HaloExchange schedule — with the faces
-moved over gloo through host memory (NCCL refuses two ranks on one GPU; the NCCL path differs only
-in the transport). Owned PDFs after K steps equal the single-engine run bit for bit."""
+"""Multi-process slab mode on one B200: 2-3 ranks (processes) share cuda:0 and run SlabRun with
+(a) the fused peer-store exchange across processes (CUDA IPC handles, GPU-side flag waits), and
+(b) the torch HaloExchange schedule with faces over gloo through host memory (NCCL refuses two
+ranks on one GPU; the native NCCL path shares that schedule). Owned PDFs after K steps equal the
+single-engine run bit for bit."""
 import os
 import socket
 
@@ -28,7 +29,7 @@ def _geom(name):
     return P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=(24, 20, 48))), 4, 0
 
 
-def _worker(rank, world, port, name, q):
+def _worker(rank, world, port, name, transport, q):
     try:
         import torch.distributed as dist
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -38,8 +39,11 @@ def _worker(rank, world, port, name, q):
         from paper_1703_08015_b200 import slab
         g, a, per = _geom(name)
         m = P.FluidModel(tau=0.8)
-        run = slab.SlabRun(g, a, m, per, rank, world, 0, host_staged=True)
-        run.engine.initialize(O.wavy)
+        if transport == "p2p":  # CUDA IPC peer stores between the processes
+            run = slab.SlabRun(g, a, m, per, rank, world, 0, transport="p2p")
+        else:  # torch HaloExchange over gloo through host memory
+            run = slab.SlabRun(g, a, m, per, rank, world, 0, host_staged=True)
+        run.initialize(O.wavy)
         run.step_async(STEPS)
         ok, _ = run.sync()
         whole = P.TileEngineT2C(g, a, m, per)
@@ -61,14 +65,15 @@ def _worker(rank, world, port, name, q):
         q.put((rank, False, traceback.format_exc()))
 
 
+@pytest.mark.parametrize("transport", ["torch", "p2p"])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("name", ["ras40_periodic", "channel3d"])
-def test_slabrun_processes_match_whole(name, world):
+def test_slabrun_processes_match_whole(name, world, transport):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, name, q)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, name, transport, q)) for r in range(world)]
     for p in ps:
         p.start()
     res = [q.get(timeout=600) for _ in ps]
