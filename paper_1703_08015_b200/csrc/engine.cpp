@@ -184,6 +184,8 @@ struct splbm_dev_engine {
     s.nb = nb;
     s.t0 = n_low;
     s.n_nodes = n_own * n_tn;
+    s.skip_at = UINT64_MAX;
+    s.skip_by = 0;
     s.a = a;
     s.inv_tau = inv_tau;
     s.bc = bc;
@@ -219,6 +221,14 @@ struct splbm_dev_engine {
     if (part == 1) {
       if (merged) {
         launch_range(read, b0, t1);
+      } else if (b1 > b0 && t1 > t0) {  // both planes in one launch, jumping the interior
+        splbm_dev::StepArgs s = step_args(read, 0);
+        s.t0 = b0;
+        s.n_nodes = (send_low_tiles + send_high_tiles) * n_tn;
+        s.skip_at = send_low_tiles;
+        s.skip_by = t0 - b1;
+        CK(splbm_dev::launch_step(d, incompressible != 0, s, stream));
+        ++launches;
       } else {
         launch_range(read, b0, b1);
         launch_range(read, t0, t1);

@@ -63,7 +63,9 @@ __global__ void __launch_bounds__(kThreads) t2c_step_kernel(StepArgs args) {
   const int n_tn = a * a * az;
   const uint64_t g = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
   if (g >= args.n_nodes) return;
-  const uint64_t t = args.t0 + g / static_cast<uint64_t>(n_tn);
+  uint64_t tord = g / static_cast<uint64_t>(n_tn);
+  if (tord >= args.skip_at) tord += args.skip_by;
+  const uint64_t t = args.t0 + tord;
   const int p = static_cast<int>(g % static_cast<uint64_t>(n_tn));
   const uint64_t node = t * n_tn + p;
   const uint32_t info = __ldg(args.info + node);
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2)
     const uint64_t tt = tile_blk + tl;
     const double* b = nullptr;
     if (tt < n_tiles) {
-      const uint32_t s = __ldg(args.nb + (args.t0 + tt) * NBS + dd);
+      const uint32_t s = __ldg(args.nb + (args.t0 + tt + (tt >= args.skip_at ? args.skip_by : 0)) * NBS + dd);
       b = s == kEmpty ? nullptr : args.read + static_cast<uint64_t>(s) * STRIDE;
     }
     s_base[tl][dd] = b;
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2)
   const int p = threadIdx.x % NTN;
   const uint64_t tloc = tile_blk + tl;
   const bool live = tloc < n_tiles;
-  const uint64_t t = args.t0 + tloc;
+  const uint64_t t = args.t0 + tloc + (tloc >= args.skip_at ? args.skip_by : 0);
   const uint32_t info = live ? __ldg(args.info + t * NTN + p) : 0u;
   __syncthreads();
 #if SPLBM_PDL

@@ -15,6 +15,8 @@ struct StepArgs {
   const uint32_t* nb;    // stored tiles x 27 (3D) / 9 (2D, dz = 0 slice), local indices
   uint64_t t0;           // first stepped tile (stored index)
   uint64_t n_nodes;      // stepped tiles * n_tn
+  uint64_t skip_at;      // stepped-tile ordinal from which `skip_by` tiles are jumped (two ranges
+  uint64_t skip_by;      // in one launch: a slab's bottom and top planes); skip_by = 0 = one range
   int a;
   double inv_tau;
   BcParams bc;

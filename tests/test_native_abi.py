@@ -21,6 +21,7 @@ def declared_functions():
 
 def test_every_declared_symbol_is_exported_and_bound():
     L = _native.lib()
+    assert L.missing_symbols == []
     names = declared_functions()
     assert len(names) >= 30
     for n in names:
