@@ -164,23 +164,34 @@ def porosity_sweep(P, K, W, peak):
 
 def other_configs(P, K, W, peak):
     """The other BASELINE configs on one GPU: configs[0] (D2Q9 cavity 256^2, 1000 steps, a=4 and
-    the reference 2D default a=16) and configs[3] (D2Q9 4096^2 seeded vessel tree, a=4)."""
+    the reference 2D default a=16), configs[3] (D2Q9 4096^2 seeded vessel tree, a=4), and the
+    paper's Table 2 collision variants on the configs[1] channel (BGK incompressible, MRT)."""
     rows = []
-    cases = [("configs[0] D2Q9 cavity 256^2 a=4, 1000 steps",
-              lambda: P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(256, 256, 1))), 4, 1000),
+    inc = P.FluidModel(P.Compressibility.Incompressible, tau=0.8)
+    mrt = P.FluidModel(collision=P.CollisionKind.MRT, tau=0.8)
+    mrt_inc = P.FluidModel(P.Compressibility.Incompressible, P.CollisionKind.MRT, tau=0.8)
+    chan = lambda: channel_geometry(P, (128, 128, 128))
+    cases = [("configs[1] channel 128^3, BGK incompressible (paper Table 2 headline model)",
+              chan, 4, K, inc),
+             ("configs[1] channel 128^3, MRT quasi-compressible", chan, 4, K, mrt),
+             ("configs[1] channel 128^3, MRT incompressible", chan, 4, K, mrt_inc),
+             ("configs[0] D2Q9 cavity 256^2 a=4, 1000 steps",
+              lambda: P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(256, 256, 1))), 4, 1000,
+              None),
              ("configs[0] D2Q9 cavity 256^2 a=16, 1000 steps",
-              lambda: P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(256, 256, 1))), 16, 1000),
+              lambda: P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(256, 256, 1))), 16,
+              1000, None),
              ("configs[3] D2Q9 vessel tree 4096^2 a=4 (seed 1, phi~0.23)",
               lambda: P.generate(P.GeometryKind.Vessel2D, P.GenerateParams(
-                  dims=(4096, 4096, 1), target_porosity=0.2, seed=1)), 4, K)]
-    for name, mk, a, steps in cases:
+                  dims=(4096, 4096, 1), target_porosity=0.2, seed=1)), 4, K, None)]
+    for name, mk, a, steps, model in cases:
         g = mk()
-        eng = P.TileEngineT2C(g, a, P.FluidModel(tau=0.8))
+        eng = P.TileEngineT2C(g, a, model or P.FluidModel(tau=0.8))
         eng.initialize_uniform()
         ms, _, _ = time_steps(eng, steps, W)
         nf = eng.fluid_nodes()
         mlups = nf * steps / (ms * 1e-3) / 1e6
-        gbs = mlups * 1e6 * B_NODE[2] / 1e9
+        gbs = mlups * 1e6 * B_NODE[g.d] / 1e9
         rows.append({"config": name, "steps": steps, "fluid_nodes": nf,
                      "phi_t": round(eng.info.phi_t, 4), "us_per_step": round(ms / steps * 1e3, 2),
                      "mlups": round(mlups, 1), "achieved_gbs": round(gbs, 1),

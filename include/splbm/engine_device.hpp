@@ -46,8 +46,6 @@ class TileEngineT2CDevice : public Engine<double> {
   TileEngineT2CDevice(const Geometry& g, int a, const FluidModel& model, Periodicity periodic = {},
                       ThreadPool* /*pool*/ = nullptr, int device = 0)
       : d_(g.d), dims_(g.dims), types_(g.types) {
-    if (model.collision != CollisionKind::BGK)
-      throw ConfigError("the B200 T2C path implements BGK collisions only");
     splbm_dev_desc desc{};
     desc.d = g.d;
     for (int k = 0; k < 3; ++k) desc.dims[k] = g.dims[k];
@@ -59,6 +57,10 @@ class TileEngineT2CDevice : public Engine<double> {
     desc.incompressible = model.compressibility == Compressibility::Incompressible;
     desc.periodic = (periodic.x ? 1 : 0) | (periodic.y ? 2 : 0) | (periodic.z ? 4 : 0);
     desc.device = device;
+    desc.collision = model.collision == CollisionKind::MRT ? 1 : 0;
+    desc.mrt_rates = model.mrt_rates.empty() ? nullptr : model.mrt_rates.data();
+    if (desc.mrt_rates && static_cast<int>(model.mrt_rates.size()) != (g.d == 2 ? 9 : 19))
+      throw ConfigError("mrt_rates must have one entry per moment");
     device_detail::check(splbm_dev_create(&desc, &e_));
     device_detail::check(splbm_dev_get_info(e_, &info_));
     tile_.resize(info_.n_tiles_stored);

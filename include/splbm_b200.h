@@ -126,6 +126,10 @@ typedef struct {
    * Multi-GPU slab mode; the engine then stores its own planes plus one halo plane
    * on each side and exchanges face PDFs through splbm_dev_halo_* each step. */
   int slab_z0, slab_z1;
+  /* CollisionKind (lattice.hpp:54): 0 BGK, 1 MRT with K = M^-1 S M (collision.cpp:86-113);
+   * mrt_rates = q relaxation rates or NULL for default_mrt_rates (collision.cpp:76-84). */
+  int collision;
+  const double* mrt_rates;
 } splbm_dev_desc;
 
 typedef struct {
@@ -231,6 +235,10 @@ int splbm_dev_comm_attach(splbm_dev_engine* e, const uint8_t* id, int world, int
 #define SPLBM_IPC_BLOB_BYTES 512
 int splbm_dev_ipc_blob(splbm_dev_engine* e, uint8_t* blob_out);
 int splbm_dev_p2p_attach(splbm_dev_engine* e, const uint8_t* lower_blob, const uint8_t* upper_blob);
+
+/* The MRT operator matrix the device applies (q x q row-major), bit-identical to the reference's
+ * CollisionOperator<double> (collision.cpp:86-113). */
+int splbm_mrt_kernel(int d, double tau, const double* rates, double* K_out);
 
 /* ---- self-test ------------------------------------------------------------------------------- */
 /* Runs the step kernel's velocity division u_k = m_k / rho (collision.hpp:48) on the device for n

@@ -45,7 +45,8 @@ def lib():
     L.oracle_t2c_initialize.argtypes = [C.c_int, C.c_int64, C.c_int, C.c_int, _dp, _dp, _dp, _dp,
                                         _dp, _dp]
     L.oracle_t2c_step.argtypes = [C.c_int, C.c_int, C.c_int64, _u8, _u32, _u8, _dp, _dp,
-                                  C.c_double, C.c_int, _dp, C.c_double, C.c_int]
+                                  C.c_double, C.c_int, _dp, C.c_double, C.c_int, C.c_void_p]
+    L.oracle_mrt_kernel.argtypes = [C.c_int, C.c_double, C.c_void_p, _dp]
     L.oracle_t2c_step.restype = C.c_int
     L.oracle_fields.argtypes = [C.c_int, C.c_int, C.c_int64, _i32, _u8, _i32, _dp, C.c_int, _dp,
                                 _dp, _dp, _dp, _u8]
@@ -127,6 +128,15 @@ def wavy(x, y, z):
     return out
 
 
+def mrt_kernel(d, tau, rates=None):
+    """K = M^-1 S M of CollisionOperator (collision.cpp:86-113), restated in C."""
+    q = 9 if d == 2 else 19
+    out = np.empty(q * q)
+    r = None if rates is None else np.ascontiguousarray(rates, np.float64)
+    lib().oracle_mrt_kernel(d, tau, None if r is None else r.ctypes.data, out)
+    return out.reshape(q, q)
+
+
 def tile_node_coords(origins, a, d):
     """node_coords(tile, p) for every tile node (engine.hpp:401-407) -> x, y, z [T*n_tn]."""
     n_tn = a * a * (a if d == 3 else 1)
@@ -139,10 +149,11 @@ def tile_node_coords(origins, a, d):
 
 
 class OracleT2C:
-    """TileEngineT2C<double> restated in C (engine.hpp:311-551), BGK only."""
+    """TileEngineT2C<double> restated in C (engine.hpp:311-551), BGK or MRT."""
 
     def __init__(self, types, d, dims, a=4, tau=0.8, incompressible=False, periodic=0,
-                 bc_velocity=(0.0, 0.0, 0.0), bc_density=1.0, threads=1):
+                 bc_velocity=(0.0, 0.0, 0.0), bc_density=1.0, threads=1, mrt=False,
+                 mrt_rates=None):
         if not tau > 0.5:
             raise ValueError("relaxation time tau must be > 0.5")
         self.d, self.a = d, a
@@ -154,6 +165,7 @@ class OracleT2C:
         self.bc_u = np.asarray(bc_velocity, np.float64)
         self.bc_rho = float(bc_density)
         self.threads = threads
+        self.K = np.ascontiguousarray(mrt_kernel(d, tau, mrt_rates)).ravel() if mrt else None
         self.tiles = build_tiles(types, d, self.dims, a, self.periodic)
         self.T = self.tiles["origins"].shape[0]
         self.n_tn = self.tiles["n_tn"]
@@ -194,7 +206,8 @@ class OracleT2C:
             ok = lib().oracle_t2c_step(self.d, self.a, self.T, self.ttypes, self.nb, self.bcdeg,
                                        self.pdf[self.read], self.pdf[1 - self.read],
                                        self.inv_tau, self.incompressible, self.bc_u,
-                                       self.bc_rho, self.threads)
+                                       self.bc_rho, self.threads,
+                                       None if self.K is None else self.K.ctypes.data)
             self.read = 1 - self.read
             self.step_count += 1
             if not ok:

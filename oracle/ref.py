@@ -84,6 +84,7 @@ def lib(fast: bool = False) -> C.CDLL:
     L.ref_bandwidth_utilization.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double,
                                             C.POINTER(C.c_double)]
     L.ref_hardware_threads.restype = C.c_int
+    L.ref_mrt_kernel.argtypes = [C.c_int, C.c_double, C.c_void_p, C.c_int, _dp]
     _libs[key] = L
     return L
 
@@ -304,6 +305,17 @@ def bandwidth_utilization(d, mlups, b_peak, s_d=8.0):
     out = C.c_double()
     _check(L, L.ref_bandwidth_utilization(d, s_d, mlups, b_peak, C.byref(out)))
     return out.value
+
+
+def mrt_kernel(d, tau, rates=None):
+    """CollisionOperator<double>::kernel_ of the reference (collision.cpp:86-113)."""
+    L = lib()
+    q = 9 if d == 2 else 19
+    out = np.empty(q * q)
+    r = None if rates is None else np.ascontiguousarray(rates, np.float64)
+    _check(L, L.ref_mrt_kernel(d, tau, None if r is None else r.ctypes.data,
+                               0 if r is None else r.size, out))
+    return out.reshape(q, q)
 
 
 def hardware_threads() -> int:

@@ -36,6 +36,11 @@ struct T2CRead {
   using type = int TileEngineT2C<double>::*;
   friend type get(T2CRead);
 };
+struct MrtKernel {
+  using type = std::vector<double> CollisionOperator<double>::*;
+  friend type get(MrtKernel);
+};
+template struct Rob<MrtKernel, &CollisionOperator<double>::kernel_>;
 template struct Rob<T2CPdf, &TileEngineT2C<double>::pdf_>;
 template struct Rob<T2CRead, &TileEngineT2C<double>::read_>;
 
@@ -364,6 +369,17 @@ int ref_bandwidth_utilization(int d, double s_d, double mlups, double b_peak, do
     p.lat = &lattice_descriptor(d == 2 ? Arrangement::D2Q9 : Arrangement::D3Q19);
     p.s_d = s_d;
     *out = bandwidth_utilization(mlups, p, b_peak);
+  })
+}
+
+// The MRT operator matrix K = M^-1 S M of CollisionOperator<double> (collision.cpp:86-113).
+int ref_mrt_kernel(int d, double tau, const double* rates, int n_rates, double* K) {
+  GUARD({
+    FluidModel m = model_of(tau, 0, 1);
+    if (rates) m.mrt_rates.assign(rates, rates + n_rates);
+    const CollisionOperator<double> op(detail::solver_lattice(d), m);
+    const auto& k = op.*get(MrtKernel());
+    std::memcpy(K, k.data(), k.size() * sizeof(double));
   })
 }
 

@@ -219,6 +219,33 @@ static int collide_bgk(const lattice_t* L, int incompressible, double inv_tau, d
   return isfinite(rho) && isfinite(m[0]) && isfinite(m[1]) && isfinite(m[2]);
 }
 
+/* CollisionOperator::operator() MRT branch: collision.hpp:54-63 */
+static int collide_mrt(const lattice_t* L, int incompressible, const double* K, double* f) {
+  double rho = 0.0, m[3] = {0.0, 0.0, 0.0};
+  for (int i = 0; i < L->q; ++i) {
+    rho += f[i];
+    m[0] += (double)L->e[i][0] * f[i];
+    m[1] += (double)L->e[i][1] * f[i];
+    m[2] += (double)L->e[i][2] * f[i];
+  }
+  if (!incompressible) {
+    if (!(rho > 0.0) || !isfinite(rho)) return 0;
+    m[0] /= rho;
+    m[1] /= rho;
+    m[2] /= rho;
+  }
+  double feq[19], delta[19];
+  equilibrium(L, incompressible, rho, m, feq);
+  for (int i = 0; i < L->q; ++i) delta[i] = feq[i] - f[i];
+  const double* row = K;
+  for (int i = 0; i < L->q; ++i, row += L->q) {
+    double acc = 0.0;
+    for (int j = 0; j < L->q; ++j) acc += row[j] * delta[j];
+    f[i] += acc;
+  }
+  return isfinite(rho) && isfinite(m[0]) && isfinite(m[1]) && isfinite(m[2]);
+}
+
 /* apply_boundary<T>: engine.hpp:32-65 */
 static int apply_boundary(const lattice_t* L, int incompressible, const double* bc_u,
                           double bc_rho, int type, double* f, int rho_underdetermined) {
@@ -294,6 +321,7 @@ typedef struct {
   double bc_rho;
   const uint8_t* delta;
   const uint32_t* src;
+  const double* K; /* MRT operator or NULL (BGK) */
   int64_t t_begin, t_end;
   int ok;
 } step_ctx_t;
@@ -326,7 +354,8 @@ static void* sweep_range(void* arg) {
         }
         fin[i] = blocked ? own_pdf[(size_t)L->opp[i] * n_tn + p] : src_pdf[(size_t)i * n_tn + sp];
       }
-      const int good = type == 1 ? collide_bgk(L, c->incompressible, c->inv_tau, fin)
+      const int good = type == 1 ? (c->K ? collide_mrt(L, c->incompressible, c->K, fin)
+                                         : collide_bgk(L, c->incompressible, c->inv_tau, fin))
                                  : apply_boundary(L, c->incompressible, c->bc_u, c->bc_rho, type,
                                                   fin, c->bcdeg[(size_t)t * n_tn + p] != 0);
       ok &= good;
@@ -365,7 +394,8 @@ static void run_chunks(step_ctx_t* ctx, int nthreads) {
  * flag per tile node (bc_degenerate(t,p), engine.hpp:409-417). Returns the step's ok flag. */
 int oracle_t2c_step(int d, int a, int64_t T, const uint8_t* ttypes, const uint32_t* nb,
                     const uint8_t* bcdeg, const double* read, double* write, double inv_tau,
-                    int incompressible, const double* bc_u, double bc_rho, int nthreads) {
+                    int incompressible, const double* bc_u, double bc_rho, int nthreads,
+                    const double* K) {
   lattice_t L;
   lattice_init(&L, d);
   const int q = L.q;
@@ -391,7 +421,7 @@ int oracle_t2c_step(int d, int a, int64_t T, const uint8_t* ttypes, const uint32
       src[i * n_tn + p] = (uint32_t)(l[0] + a * (l[1] + a * l[2]));
     }
   step_ctx_t ctx = {&L, a, n_tn, T, ttypes, nb, bcdeg, read, write, inv_tau, incompressible,
-                    bc_u, bc_rho, delta, src, 0, 0, 1};
+                    bc_u, bc_rho, delta, src, K, 0, 0, 1};
   run_chunks(&ctx, nthreads);
   const int ok = ctx.ok;
   free(delta);
@@ -506,4 +536,87 @@ void oracle_wavy(size_t n, const int32_t* x, const int32_t* y, const int32_t* z,
     uy[i] = 0.01 * cos(0.17 * Y + 0.29 * Z);
     uz[i] = 0.01 * sin(0.13 * Z + 0.41 * X);
   }
+}
+
+/* ---- MRT (collision.cpp:11-113, collision.hpp:54-63) ---------------------------------------- */
+/* Moment basis rows evaluated on the direction vectors (collision.cpp:11-60). */
+static void mrt_basis(const lattice_t* L, double* m /* q*q, row-major */) {
+  const int q = L->q;
+  for (int i = 0; i < q; ++i) {
+    const double ex = L->e[i][0], ey = L->e[i][1], ez = L->e[i][2];
+    if (L->d == 2) {
+      const double e2 = ex * ex + ey * ey;
+      const double r[9] = {1.0,
+                           -4.0 + 3.0 * e2,
+                           4.0 - 10.5 * e2 + 4.5 * e2 * e2,
+                           ex,
+                           (-5.0 + 3.0 * e2) * ex,
+                           ey,
+                           (-5.0 + 3.0 * e2) * ey,
+                           ex * ex - ey * ey,
+                           ex * ey};
+      for (int k = 0; k < 9; ++k) m[k * q + i] = r[k];
+    } else {
+      const double e2 = ex * ex + ey * ey + ez * ez;
+      const double r[19] = {1.0,
+                            19.0 * e2 - 30.0,
+                            0.5 * (21.0 * e2 * e2 - 53.0 * e2 + 24.0),
+                            ex,
+                            (5.0 * e2 - 9.0) * ex,
+                            ey,
+                            (5.0 * e2 - 9.0) * ey,
+                            ez,
+                            (5.0 * e2 - 9.0) * ez,
+                            3.0 * ex * ex - e2,
+                            (3.0 * e2 - 5.0) * (3.0 * ex * ex - e2),
+                            ey * ey - ez * ez,
+                            (3.0 * e2 - 5.0) * (ey * ey - ez * ez),
+                            ex * ey,
+                            ey * ez,
+                            ex * ez,
+                            (ey * ey - ez * ez) * ex,
+                            (ez * ez - ex * ex) * ey,
+                            (ex * ex - ey * ey) * ez};
+      for (int k = 0; k < 19; ++k) m[k * q + i] = r[k];
+    }
+  }
+}
+
+/* K = M^-1 S M with M^-1 = M^T diag(1/|row|^2) (collision.cpp:86-113); the dense products run in
+ * the shim's order (acc += a(i,k) * b(k,j), k ascending). rates: q entries or NULL for the default
+ * (0 for the conserved moments, 1/tau otherwise; collision.cpp:76-84). */
+int oracle_mrt_kernel(int d, double tau, const double* rates_in, double* K) {
+  lattice_t L;
+  lattice_init(&L, d);
+  const int q = L.q;
+  double m[361], rn2[19], minv[361], s[361], p1[361], rates[19];
+  mrt_basis(&L, m);
+  for (int i = 0; i < q; ++i) rates[i] = rates_in ? rates_in[i] : 1.0 / tau;
+  if (!rates_in) {
+    const int cons2[3] = {0, 3, 5}, cons3[4] = {0, 3, 5, 7};
+    const int* c = d == 2 ? cons2 : cons3;
+    for (int k = 0; k < (d == 2 ? 3 : 4); ++k) rates[c[k]] = 0.0;
+  }
+  for (int i = 0; i < q; ++i) { /* (m * m^T).diagonal() */
+    double acc = 0.0;
+    for (int k = 0; k < q; ++k) acc += m[i * q + k] * m[i * q + k];
+    rn2[i] = acc;
+  }
+  for (int i = 0; i < q; ++i)
+    for (int j = 0; j < q; ++j) minv[i * q + j] = m[j * q + i] * (1.0 / rn2[j]);
+  for (int i = 0; i < q; ++i)
+    for (int j = 0; j < q; ++j) s[i * q + j] = i == j ? rates[i] : 0.0;
+  for (int i = 0; i < q; ++i)
+    for (int j = 0; j < q; ++j) {
+      double acc = 0.0;
+      for (int k = 0; k < q; ++k) acc += minv[i * q + k] * s[k * q + j];
+      p1[i * q + j] = acc;
+    }
+  for (int i = 0; i < q; ++i)
+    for (int j = 0; j < q; ++j) {
+      double acc = 0.0;
+      for (int k = 0; k < q; ++k) acc += p1[i * q + k] * m[k * q + j];
+      K[i * q + j] = acc;
+    }
+  return q;
 }

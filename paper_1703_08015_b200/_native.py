@@ -33,7 +33,8 @@ class DevDesc(C.Structure):
     _fields_ = [("d", C.c_int), ("dims", C.c_int * 3), ("types", C.c_void_p),
                 ("bc_velocity", C.c_double * 3), ("bc_density", C.c_double), ("tile", C.c_int),
                 ("tau", C.c_double), ("incompressible", C.c_int), ("periodic", C.c_int),
-                ("device", C.c_int), ("slab_z0", C.c_int), ("slab_z1", C.c_int)]
+                ("device", C.c_int), ("slab_z0", C.c_int), ("slab_z1", C.c_int),
+                ("collision", C.c_int), ("mrt_rates", C.c_void_p)]
 
 
 class DevInfo(C.Structure):
@@ -104,6 +105,7 @@ SIGNATURES = {
     "splbm_dev_comm_attach": ([_vp, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int], C.c_int),
     "splbm_dev_halo_pack_next": ([_vp, C.c_void_p, C.c_void_p], C.c_int),
     "splbm_selftest_divide": ([C.c_uint64, _dp, _dp, _dp], C.c_int),
+    "splbm_mrt_kernel": ([C.c_int, C.c_double, C.c_void_p, _dp], C.c_int),
 }
 
 

@@ -15,8 +15,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsplbm_b200.so")
 BUILD = os.path.join(ROOT, "build", "native")
-SOURCES = ["kernels.cu", "engine.cpp", "tiling.cpp", "geometry.cpp", "nccl_api.cpp"]
-HEADERS = ["kernels.h", "lattice.cuh", "common.h", "tiling.h", "nccl_api.h"]
+SOURCES = ["kernels.cu", "engine.cpp", "tiling.cpp", "geometry.cpp", "nccl_api.cpp", "mrt.cpp"]
+HEADERS = ["kernels.h", "lattice.cuh", "common.h", "tiling.h", "nccl_api.h", "mrt.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",

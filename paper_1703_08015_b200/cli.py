@@ -15,7 +15,7 @@ from . import engine as E
 from . import geometry as G
 from . import overhead as O
 from .errors import ConfigError, Error, NumericalError
-from .lattice import Compressibility, FluidModel, solver_lattice
+from .lattice import CollisionKind, Compressibility, FluidModel, solver_lattice
 from .tiling import Periodicity, build_tile_grid, tile_stats
 
 EXIT_OK, EXIT_CONFIG, EXIT_NUMERICAL = 0, 2, 3
@@ -104,8 +104,9 @@ def build_geometry(cfg: Config) -> G.Geometry:  # splbm.cpp:91-116
 
 
 def build_model(cfg: Config) -> FluidModel:  # splbm.cpp:118-134
-    if cfg.get("sim.collision", "bgk") != "bgk":
-        raise ConfigError("the B200 engine implements sim.collision = bgk")
+    coll = cfg.get("sim.collision", "bgk")
+    if coll not in ("bgk", "mrt"):
+        raise ConfigError("sim.collision must be bgk or mrt")
     comp = cfg.get("sim.compressibility", "quasi")
     if comp in ("quasi", "quasi-compressible"):
         c = Compressibility.QuasiCompressible
@@ -113,7 +114,8 @@ def build_model(cfg: Config) -> FluidModel:  # splbm.cpp:118-134
         c = Compressibility.Incompressible
     else:
         raise ConfigError("sim.compressibility must be quasi or incompressible")
-    return FluidModel(c, tau=cfg.get_float("sim.tau", 0.8))
+    return FluidModel(c, CollisionKind.MRT if coll == "mrt" else CollisionKind.BGK,
+                      tau=cfg.get_float("sim.tau", 0.8))
 
 
 def build_sim(cfg: Config) -> E.SimConfig:  # splbm.cpp:136-150

@@ -55,7 +55,7 @@ __device__ __forceinline__ void st_stream(double* p, double v) {
 // ---------------------------------------------------------------------------------------------
 // The fused gather-propagation + BGK/boundary + store step (engine.hpp:466-514, collision.hpp:35-65,
 // engine.hpp:32-65). A > 0 is a compile-time tile edge; A == 0 reads a_rt.
-template <int D, int A, bool INC>
+template <int D, int A, bool INC, bool MRT>
 __global__ void __launch_bounds__(kThreads) t2c_step_kernel(StepArgs args) {
   constexpr int Q = Lat<D>::Q;
   const int a = A > 0 ? A : args.a;
@@ -117,7 +117,10 @@ __global__ void __launch_bounds__(kThreads) t2c_step_kernel(StepArgs args) {
 
   bool good;
   if (type == 1) {
-    good = collide_bgk<D, INC>(f, args.inv_tau);
+    if constexpr (MRT)
+      good = collide_mrt<D, INC>(f, args.mrt_K);
+    else
+      good = collide_bgk<D, INC>(f, args.inv_tau);
   } else {
     good = apply_boundary<D, INC>(f, type, (info >> 26) & 1u, args.bc);
   }
@@ -132,8 +135,9 @@ __global__ void __launch_bounds__(kThreads) t2c_step_kernel(StepArgs args) {
 // the per-direction source address is pure integer arithmetic on compile-time lattice constants
 // plus one shared-memory lookup and two selects — no divergent branches, no dependent global load
 // before the PDF gather.
-template <int D, int LOGA, bool INC, bool PEER>
-__global__ void __launch_bounds__(kThreads, (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2)) t2c_step_pow2_kernel(StepArgs args) {
+template <int D, int LOGA, bool INC, bool PEER, bool MRT>
+__global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2))
+    t2c_step_pow2_kernel(StepArgs args) {
   constexpr int Q = Lat<D>::Q;
   constexpr int A = 1 << LOGA;
   constexpr int NTN = D == 3 ? A * A * A : A * A;
@@ -198,7 +202,10 @@ __global__ void __launch_bounds__(kThreads, (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2)
 
   bool good;
   if (type == 1) {
-    good = collide_bgk<D, INC>(f, args.inv_tau);
+    if constexpr (MRT)
+      good = collide_mrt<D, INC>(f, args.mrt_K);
+    else
+      good = collide_bgk<D, INC>(f, args.inv_tau);
   } else {
     good = apply_boundary<D, INC>(f, type, (info >> 26) & 1u, args.bc);
   }
@@ -452,36 +459,44 @@ __global__ void divide_selftest_kernel(uint64_t n, const double* m, const double
 // Launchers (host side of this translation unit)
 template <int D, int LOGA, bool INC>
 static void launch_pow2(const StepArgs& a, cudaStream_t st) {
-  if (a.peer_up || a.peer_down) {  // slab boundary planes with NVLink peer stores
-    constexpr int NTN_ = D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA));
-    const unsigned b = static_cast<unsigned>((a.n_nodes / NTN_ + kThreads / NTN_ - 1) / (kThreads / NTN_));
-    t2c_step_pow2_kernel<D, LOGA, INC, true><<<b, kThreads, 0, st>>>(a);
-    return;
-  }
   constexpr int NTN = D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA));
   constexpr int TILES = kThreads / NTN;
   const uint64_t tiles = a.n_nodes / NTN;
   const unsigned blocks = static_cast<unsigned>((tiles + TILES - 1) / TILES);
+  if (a.mrt_K) {
+    t2c_step_pow2_kernel<D, LOGA, INC, false, true><<<blocks, kThreads, 0, st>>>(a);
+    return;
+  }
+  if (a.peer_up || a.peer_down) {  // slab boundary planes with NVLink peer stores
+    t2c_step_pow2_kernel<D, LOGA, INC, true, false><<<blocks, kThreads, 0, st>>>(a);
+    return;
+  }
 #if SPLBM_PDL
   // Overlap the next step's launch and static-table prologue with this step's tail; below a few
   // waves (launch-latency-bound domains) the plain launch measured faster.
-  if (blocks < 4u * 148u) {
-    t2c_step_pow2_kernel<D, LOGA, INC, false><<<blocks, kThreads, 0, st>>>(a);
+  if (blocks >= 4u * 148u) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, t2c_step_pow2_kernel<D, LOGA, INC, false, false>, a);
     return;
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(blocks);
-  cfg.blockDim = dim3(kThreads);
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, t2c_step_pow2_kernel<D, LOGA, INC, false>, a);
-#else
-  t2c_step_pow2_kernel<D, LOGA, INC, false><<<blocks, kThreads, 0, st>>>(a);
 #endif
+  t2c_step_pow2_kernel<D, LOGA, INC, false, false><<<blocks, kThreads, 0, st>>>(a);
+}
+
+template <int D, int A, bool INC>
+static void launch_generic(const StepArgs& a, unsigned blocks, cudaStream_t st) {
+  if (a.mrt_K)
+    t2c_step_kernel<D, A, INC, true><<<blocks, kThreads, 0, st>>>(a);
+  else
+    t2c_step_kernel<D, A, INC, false><<<blocks, kThreads, 0, st>>>(a);
 }
 
 template <int D, bool INC>
@@ -492,8 +507,8 @@ static cudaError_t launch_step_d(const StepArgs& a, cudaStream_t st) {
     switch (a.a) {
       case 2: launch_pow2<D, 1, INC>(a, st); break;
       case 4: launch_pow2<D, 2, INC>(a, st); break;
-      case 8: t2c_step_kernel<D, 8, INC><<<blocks, kThreads, 0, st>>>(a); break;
-      default: t2c_step_kernel<D, 0, INC><<<blocks, kThreads, 0, st>>>(a); break;
+      case 8: launch_generic<D, 8, INC>(a, blocks, st); break;
+      default: launch_generic<D, 0, INC>(a, blocks, st); break;
     }
   } else {
     switch (a.a) {
@@ -501,7 +516,7 @@ static cudaError_t launch_step_d(const StepArgs& a, cudaStream_t st) {
       case 4: launch_pow2<D, 2, INC>(a, st); break;
       case 8: launch_pow2<D, 3, INC>(a, st); break;
       case 16: launch_pow2<D, 4, INC>(a, st); break;
-      default: t2c_step_kernel<D, 0, INC><<<blocks, kThreads, 0, st>>>(a); break;
+      default: launch_generic<D, 0, INC>(a, blocks, st); break;
     }
   }
   return cudaGetLastError();

@@ -19,6 +19,7 @@ struct StepArgs {
   uint64_t skip_by;      // in one launch: a slab's bottom and top planes); skip_by = 0 = one range
   int a;
   double inv_tau;
+  const double* mrt_K;  // MRT operator (q x q, device memory); nullptr = BGK
   BcParams bc;
   unsigned long long* failed;  // min failing step number (ULLONG_MAX = none)
   const long long* step_base;  // steps completed before this batch

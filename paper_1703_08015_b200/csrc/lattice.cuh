@@ -198,6 +198,34 @@ __device__ __forceinline__ bool collide_bgk(double* f, double inv_tau) {
   return finite(rho) && finite(u0) && finite(u1) && finite(u2);
 }
 
+// CollisionOperator<T>::operator() MRT branch (collision.hpp:54-63): the same moments and
+// equilibrium as BGK, then f_i += sum_j K_ij (feq_j - f_j) with the q x q operator K = M^-1 S M
+// (row-major in global memory; every thread reads the same entry, a broadcast).
+template <int D, bool INC>
+__device__ __forceinline__ bool collide_mrt(double* f, const double* __restrict__ K) {
+  constexpr int Q = Lat<D>::Q;
+  const double rho = density<D>(f);
+  double u0 = momentum<D, 0>(f);
+  double u1 = momentum<D, 1>(f);
+  double u2 = momentum<D, 2>(f);
+  if (!INC) {
+    if (!(rho > 0.0) || !finite(rho)) return false;
+    divide3(u0, u1, u2, rho);
+  }
+  const double uu = sqnorm(u0, u1, u2);
+  double delta[Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) delta[i] = dsub(feq<D, INC>(i, rho, u0, u1, u2, uu), f[i]);
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < Q; ++j) acc = dadd(acc, dmul(__ldg(K + i * Q + j), delta[j]));
+    f[i] = dadd(f[i], acc);
+  }
+  return finite(rho) && finite(u0) && finite(u1) && finite(u2);
+}
+
 struct BcParams {
   double u0, u1, u2;
   double rho;

@@ -43,9 +43,13 @@ class TileEngineT2C:
 
     def __init__(self, g: Geometry, a: int, model: FluidModel, periodic=None, device: int = 0,
                  slab: tuple | None = None):
-        if model.collision != CollisionKind.BGK:
-            raise ConfigError("the device T2C path implements BGK collisions only")
         L = _native.lib()
+        q = 9 if g.d == 2 else 19
+        rates = None
+        if model.collision == CollisionKind.MRT and model.mrt_rates:
+            if len(model.mrt_rates) != q:  # collision.cpp:100-103
+                raise ConfigError(f"mrt_rates must have one entry per moment ({q})")
+            rates = np.ascontiguousarray(model.mrt_rates, np.float64)
         per = Periodicity.of(periodic)
         types = np.ascontiguousarray(g.types, np.uint8)
         desc = _native.DevDesc()
@@ -60,6 +64,8 @@ class TileEngineT2C:
         desc.periodic = per.mask()
         desc.device = int(device)
         desc.slab_z0, desc.slab_z1 = (int(slab[0]), int(slab[1])) if slab else (0, 0)
+        desc.collision = int(model.collision)
+        desc.mrt_rates = rates.ctypes.data_as(C.c_void_p) if rates is not None else None
         h = C.c_void_p()
         _native.check(L.splbm_dev_create(C.byref(desc), C.byref(h)))
         self._h = h

@@ -63,6 +63,17 @@ def lattice_descriptor(arr: Arrangement) -> LatticeDescriptor:
     return _CACHE[Arrangement(arr)]
 
 
+def mrt_kernel(d: int, tau: float, rates=None):
+    """The MRT operator matrix K (q x q) the device applies (splbm_mrt_kernel)."""
+    import numpy as np
+    from . import _native
+    q = 9 if d == 2 else 19
+    out = np.empty(q * q)
+    r = None if rates is None else np.ascontiguousarray(rates, np.float64)
+    _native.check(_native.lib().splbm_mrt_kernel(d, float(tau), None if r is None else r.ctypes.data, out))
+    return out.reshape(q, q)
+
+
 def solver_lattice(d: int) -> LatticeDescriptor:  # engine.hpp:104-106
     return lattice_descriptor(Arrangement.D2Q9 if d == 2 else Arrangement.D3Q19)
 
@@ -74,7 +85,7 @@ class Compressibility(enum.IntEnum):  # lattice.hpp:53
 
 class CollisionKind(enum.IntEnum):  # lattice.hpp:54
     BGK = 0
-    MRT = 1  # not on the north-star path (fp64 BGK); the device engine rejects it
+    MRT = 1  # K = M^-1 S M (collision.cpp:86-113), SURVEY f4
 
 
 @dataclass

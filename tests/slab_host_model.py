@@ -49,7 +49,7 @@ class HostSlabRank:
         ok = self.O.lib().oracle_t2c_step(self.d, self.a, self.S, self.ttypes, self.nb, self.bcdeg,
                                           self.pdf[self.read], self.pdf[1 - self.read], self.inv_tau,
                                           self.inc, np.asarray(self.g.bc.velocity, np.float64),
-                                          self.g.bc.density, 1)
+                                          self.g.bc.density, 1, None)
         self.read = 1 - self.read
         return ok
 

@@ -40,7 +40,7 @@ def test_exit_codes():
     assert run(["stats"])[0] == cli.EXIT_CONFIG  # no geometry
     assert run(["stats", "--set", "geometry.kind=nope"])[0] == cli.EXIT_CONFIG
     assert run(["run", "--set", "geometry.kind=cavity2d", "--set", "geometry.dims=16 16",
-                "--set", "sim.collision=mrt"])[0] == cli.EXIT_CONFIG
+                "--set", "sim.collision=trt"])[0] == cli.EXIT_CONFIG
 
 
 def test_module_entry_point():

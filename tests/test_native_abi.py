@@ -51,7 +51,7 @@ def test_config_errors_before_device():
     with pytest.raises(P.ConfigError):
         P.TileEngineT2C(g, 4, P.FluidModel(tau=0.4))
     with pytest.raises(P.ConfigError):
-        P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8, collision=P.CollisionKind.MRT))
+        P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8, collision=P.CollisionKind.MRT, mrt_rates=[1.0] * 5))
 
 
 def test_status_mapping():
