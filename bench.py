@@ -350,6 +350,7 @@ def run_ours(args):
     del eng
     if not args.no_sweep:
         line["porosity_sweep"] = porosity_sweep(P, min(K, 50), max(W, 3), peak)
+    if not args.no_other:
         line["other_configs"] = other_configs(P, min(K, 50), max(W, 3), peak)
     line["e2e"] = e2e_public_api(P, g, 1000)
     if not args.no_cpu:
@@ -402,6 +403,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-other", action="store_true")
     ap.add_argument("--config", default="default", choices=["default", "ras1024"])
     ap.add_argument("--phi", type=float, default=0.2)
     args = ap.parse_args()

@@ -100,7 +100,7 @@ struct splbm_dev_engine {
   int* halo_dirs = nullptr;  // [0..4] ez=+1 set, [5..9] ez=-1 set (or 3+3 in 2D)
   int n_halo_dirs = 0;
   double* scratch = nullptr;
-  double* mrt_K = nullptr;  // MRT operator (nullptr = BGK)
+  std::vector<double> mrt_K;  // MRT operator (host copy; passed to the kernels by value), empty = BGK
   uint64_t device_bytes = 0;
   int read = 0;
   long step_count = 0;
@@ -156,8 +156,7 @@ struct splbm_dev_engine {
     for (void* p : {static_cast<void*>(pdf[0]), static_cast<void*>(pdf[1]),
                     static_cast<void*>(info), static_cast<void*>(nb), static_cast<void*>(failed),
                     static_cast<void*>(step_base), static_cast<void*>(domain_err),
-                    static_cast<void*>(halo_dirs), static_cast<void*>(scratch),
-                    static_cast<void*>(mrt_K)})
+                    static_cast<void*>(halo_dirs), static_cast<void*>(scratch)})
       if (p) cudaFree(p);
     if (pinned) cudaFreeHost(pinned);
     if (ev0) cudaEventDestroy(ev0);
@@ -191,7 +190,7 @@ struct splbm_dev_engine {
     s.skip_by = 0;
     s.a = a;
     s.inv_tau = inv_tau;
-    s.mrt_K = mrt_K;
+    s.mrt_K = mrt_K.empty() ? nullptr : mrt_K.data();
     s.bc = bc;
     s.failed = failed;
     s.step_base = step_base;
@@ -454,9 +453,7 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
   e->domain_err = e->alloc<int>(1);
   e->scratch = e->alloc<double>(4 * std::min<uint64_t>(kChunkNodes, std::max<uint64_t>(S * n_tn, 1)));
   if (desc->collision == 1) {  // MRT
-    const std::vector<double> K = mrt_kernel(d, desc->tau, desc->mrt_rates);
-    e->mrt_K = e->alloc<double>(K.size());
-    CK(cudaMemcpy(e->mrt_K, K.data(), K.size() * sizeof(double), cudaMemcpyHostToDevice));
+    e->mrt_K = mrt_kernel(d, desc->tau, desc->mrt_rates);
   } else if (desc->collision != 0) {
     throw config_error("unknown collision kind");
   }
@@ -896,7 +893,7 @@ int splbm_dev_p2p_attach(splbm_dev_engine* e, const uint8_t* lower_blob, const u
   return guarded([&] {
     checked(e);
     if (e->p2p || e->comm) throw config_error("engine already has a halo transport");
-    if (e->mrt_K) throw config_error("peer-store halos are built for the BGK kernels");
+    if (!e->mrt_K.empty()) throw config_error("peer-store halos are built for the BGK kernels");
     if (!e->flags) throw config_error("call splbm_dev_ipc_blob before attaching");
     if (e->a != 4 && e->a != 2 && !(e->d == 2 && (e->a == 8 || e->a == 16)))
       throw config_error("peer-store halos need a power-of-two tile kernel (a = 2, 4; 2D a <= 16)");

@@ -56,7 +56,8 @@ __device__ __forceinline__ void st_stream(double* p, double v) {
 // The fused gather-propagation + BGK/boundary + store step (engine.hpp:466-514, collision.hpp:35-65,
 // engine.hpp:32-65). A > 0 is a compile-time tile edge; A == 0 reads a_rt.
 template <int D, int A, bool INC, bool MRT>
-__global__ void __launch_bounds__(kThreads) t2c_step_kernel(StepArgs args) {
+__global__ void __launch_bounds__(kThreads)
+    t2c_step_kernel(StepArgs args, const __grid_constant__ MrtMatrix<MRT ? Lat<D>::Q : 1> mrt) {
   constexpr int Q = Lat<D>::Q;
   const int a = A > 0 ? A : args.a;
   const int az = D == 3 ? a : 1;
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(kThreads) t2c_step_kernel(StepArgs args) {
   bool good;
   if (type == 1) {
     if constexpr (MRT)
-      good = collide_mrt<D, INC>(f, args.mrt_K);
+      good = collide_mrt<D, INC>(f, mrt.K);
     else
       good = collide_bgk<D, INC>(f, args.inv_tau);
   } else {
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(kThreads) t2c_step_kernel(StepArgs args) {
 // before the PDF gather.
 template <int D, int LOGA, bool INC, bool PEER, bool MRT>
 __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2))
-    t2c_step_pow2_kernel(StepArgs args) {
+    t2c_step_pow2_kernel(StepArgs args, const __grid_constant__ MrtMatrix<MRT ? Lat<D>::Q : 1> mrt) {
   constexpr int Q = Lat<D>::Q;
   constexpr int A = 1 << LOGA;
   constexpr int NTN = D == 3 ? A * A * A : A * A;
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SP
   bool good;
   if (type == 1) {
     if constexpr (MRT)
-      good = collide_mrt<D, INC>(f, args.mrt_K);
+      good = collide_mrt<D, INC>(f, mrt.K);
     else
       good = collide_bgk<D, INC>(f, args.inv_tau);
   } else {
@@ -457,18 +458,27 @@ __global__ void divide_selftest_kernel(uint64_t n, const double* m, const double
 
 // ---------------------------------------------------------------------------------------------
 // Launchers (host side of this translation unit)
+template <int Q>
+static MrtMatrix<Q> mrt_param(const double* K) {
+  MrtMatrix<Q> m;
+  for (int i = 0; i < Q * Q; ++i) m.K[i] = K[i];
+  return m;
+}
+
 template <int D, int LOGA, bool INC>
 static void launch_pow2(const StepArgs& a, cudaStream_t st) {
   constexpr int NTN = D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA));
   constexpr int TILES = kThreads / NTN;
   const uint64_t tiles = a.n_nodes / NTN;
   const unsigned blocks = static_cast<unsigned>((tiles + TILES - 1) / TILES);
+  const MrtMatrix<1> none{};
   if (a.mrt_K) {
-    t2c_step_pow2_kernel<D, LOGA, INC, false, true><<<blocks, kThreads, 0, st>>>(a);
+    t2c_step_pow2_kernel<D, LOGA, INC, false, true>
+        <<<blocks, kThreads, 0, st>>>(a, mrt_param<Lat<D>::Q>(a.mrt_K));
     return;
   }
   if (a.peer_up || a.peer_down) {  // slab boundary planes with NVLink peer stores
-    t2c_step_pow2_kernel<D, LOGA, INC, true, false><<<blocks, kThreads, 0, st>>>(a);
+    t2c_step_pow2_kernel<D, LOGA, INC, true, false><<<blocks, kThreads, 0, st>>>(a, none);
     return;
   }
 #if SPLBM_PDL
@@ -484,19 +494,19 @@ static void launch_pow2(const StepArgs& a, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, t2c_step_pow2_kernel<D, LOGA, INC, false, false>, a);
+    cudaLaunchKernelEx(&cfg, t2c_step_pow2_kernel<D, LOGA, INC, false, false>, a, none);
     return;
   }
 #endif
-  t2c_step_pow2_kernel<D, LOGA, INC, false, false><<<blocks, kThreads, 0, st>>>(a);
+  t2c_step_pow2_kernel<D, LOGA, INC, false, false><<<blocks, kThreads, 0, st>>>(a, none);
 }
 
 template <int D, int A, bool INC>
 static void launch_generic(const StepArgs& a, unsigned blocks, cudaStream_t st) {
   if (a.mrt_K)
-    t2c_step_kernel<D, A, INC, true><<<blocks, kThreads, 0, st>>>(a);
+    t2c_step_kernel<D, A, INC, true><<<blocks, kThreads, 0, st>>>(a, mrt_param<Lat<D>::Q>(a.mrt_K));
   else
-    t2c_step_kernel<D, A, INC, false><<<blocks, kThreads, 0, st>>>(a);
+    t2c_step_kernel<D, A, INC, false><<<blocks, kThreads, 0, st>>>(a, MrtMatrix<1>{});
 }
 
 template <int D, bool INC>

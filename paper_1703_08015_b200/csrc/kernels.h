@@ -19,7 +19,7 @@ struct StepArgs {
   uint64_t skip_by;      // in one launch: a slab's bottom and top planes); skip_by = 0 = one range
   int a;
   double inv_tau;
-  const double* mrt_K;  // MRT operator (q x q, device memory); nullptr = BGK
+  const double* mrt_K;  // MRT operator (q x q, HOST memory, copied into the launch); nullptr = BGK
   BcParams bc;
   unsigned long long* failed;  // min failing step number (ULLONG_MAX = none)
   const long long* step_base;  // steps completed before this batch
@@ -31,6 +31,13 @@ struct StepArgs {
   double* peer_up;
   double* peer_down;
   uint64_t top_begin, bot_begin, bot_end;
+};
+
+// The MRT operator as a kernel parameter (constant bank): the unrolled K_ij * delta_j products
+// read it as immediate constant operands instead of 361 loads per node.
+template <int Q>
+struct MrtMatrix {
+  double K[Q * Q];
 };
 
 struct NodeInfoArgs {

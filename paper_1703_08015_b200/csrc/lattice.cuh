@@ -200,9 +200,9 @@ __device__ __forceinline__ bool collide_bgk(double* f, double inv_tau) {
 
 // CollisionOperator<T>::operator() MRT branch (collision.hpp:54-63): the same moments and
 // equilibrium as BGK, then f_i += sum_j K_ij (feq_j - f_j) with the q x q operator K = M^-1 S M
-// (row-major in global memory; every thread reads the same entry, a broadcast).
+// (row-major, a __grid_constant__ kernel parameter: the constants feed the DMULs directly).
 template <int D, bool INC>
-__device__ __forceinline__ bool collide_mrt(double* f, const double* __restrict__ K) {
+__device__ __forceinline__ bool collide_mrt(double* f, const double* K) {
   constexpr int Q = Lat<D>::Q;
   const double rho = density<D>(f);
   double u0 = momentum<D, 0>(f);
@@ -220,7 +220,7 @@ __device__ __forceinline__ bool collide_mrt(double* f, const double* __restrict_
   for (int i = 0; i < Q; ++i) {
     double acc = 0.0;
 #pragma unroll
-    for (int j = 0; j < Q; ++j) acc = dadd(acc, dmul(__ldg(K + i * Q + j), delta[j]));
+    for (int j = 0; j < Q; ++j) acc = dadd(acc, dmul(K[i * Q + j], delta[j]));
     f[i] = dadd(f[i], acc);
   }
   return finite(rho) && finite(u0) && finite(u1) && finite(u2);
