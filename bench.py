@@ -175,6 +175,8 @@ def other_configs(P, K, W, peak):
               chan, 4, K, inc),
              ("configs[1] channel 128^3, MRT quasi-compressible", chan, 4, K, mrt),
              ("configs[1] channel 128^3, MRT incompressible", chan, 4, K, mrt_inc),
+             ("configs[1] channel 128^3, single-copy (AA) propagation, half the HBM", chan, 4, K,
+              "single_copy"),
              ("configs[0] D2Q9 cavity 256^2 a=4, 1000 steps",
               lambda: P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(256, 256, 1))), 4, 1000,
               None),
@@ -186,7 +188,9 @@ def other_configs(P, K, W, peak):
                   dims=(4096, 4096, 1), target_porosity=0.2, seed=1)), 4, K, None)]
     for name, mk, a, steps, model in cases:
         g = mk()
-        eng = P.TileEngineT2C(g, a, model or P.FluidModel(tau=0.8))
+        single = model == "single_copy"
+        eng = P.TileEngineT2C(g, a, P.FluidModel(tau=0.8) if single or model is None else model,
+                              single_copy=single)
         eng.initialize_uniform()
         ms, _, _ = time_steps(eng, steps, W)
         nf = eng.fluid_nodes()
@@ -362,7 +366,7 @@ def run_ours(args):
 def run_big(args):
     """--config ras1024: BASELINE configs[4] on ONE B200 (the 1-GPU point of the 1024^3 curve):
     RAS 1024^3, d=40, seed 7, periodic, tiles 4^3, porosity --phi (only phi <~ 0.35 fits with two
-    PDF copies in 180 GB)."""
+    PDF copies in 180 GB; --single-copy, the in-place AA propagation, fits phi up to ~0.8)."""
     import paper_1703_08015_b200 as P
     peak, peak_kind = measured_peaks()
     t0 = time.time()
@@ -370,7 +374,7 @@ def run_big(args):
                                                           target_porosity=args.phi, seed=7))
     t_gen = time.time() - t0
     t0 = time.time()
-    eng = P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8), (1, 1, 1))
+    eng = P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8), (1, 1, 1), single_copy=args.single_copy)
     t_build = time.time() - t0
     eng.initialize_uniform(1.0, (0.01, 0.005, 0.0))
     ms, launches, clocks = time_steps(eng, args.steps, args.warmup)
@@ -383,7 +387,8 @@ def run_big(args):
         "value": round(mlups, 1), "unit": "MLUPS", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"configs[4] RAS 1024^3 d=40 seed 7 periodic, phi target {args.phi}",
+        "config": {"workload": f"configs[4] RAS 1024^3 d=40 seed 7 periodic, phi target {args.phi}"
+                               + (", single-copy (AA) propagation" if args.single_copy else ""),
                    "phi": round(P.porosity(g).phi, 4), "phi_t": round(eng.info.phi_t, 4),
                    "tiles": int(eng.info.n_tiles), "fluid_nodes": nf,
                    "device_gb": round(eng.info.device_bytes / 1e9, 1)},
@@ -406,6 +411,8 @@ def main():
     ap.add_argument("--no-other", action="store_true")
     ap.add_argument("--config", default="default", choices=["default", "ras1024"])
     ap.add_argument("--phi", type=float, default=0.2)
+    ap.add_argument("--single-copy", action="store_true",
+                    help="ras1024: in-place AA propagation (one PDF array)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

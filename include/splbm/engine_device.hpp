@@ -43,8 +43,9 @@ class TileEngineT2CDevice : public Engine<double> {
  public:
   // TileEngineT2C(g, a, model, periodic, pool) — the pool is accepted for signature parity; the
   // step runs on the GPU (`device` selects it).
+  // single_copy selects the in-place AA propagation (half the HBM, same results).
   TileEngineT2CDevice(const Geometry& g, int a, const FluidModel& model, Periodicity periodic = {},
-                      ThreadPool* /*pool*/ = nullptr, int device = 0)
+                      ThreadPool* /*pool*/ = nullptr, int device = 0, bool single_copy = false)
       : d_(g.d), dims_(g.dims), types_(g.types) {
     splbm_dev_desc desc{};
     desc.d = g.d;
@@ -59,6 +60,7 @@ class TileEngineT2CDevice : public Engine<double> {
     desc.device = device;
     desc.collision = model.collision == CollisionKind::MRT ? 1 : 0;
     desc.mrt_rates = model.mrt_rates.empty() ? nullptr : model.mrt_rates.data();
+    desc.single_copy = single_copy ? 1 : 0;
     if (desc.mrt_rates && static_cast<int>(model.mrt_rates.size()) != (g.d == 2 ? 9 : 19))
       throw ConfigError("mrt_rates must have one entry per moment");
     device_detail::check(splbm_dev_create(&desc, &e_));

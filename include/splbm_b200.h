@@ -130,6 +130,10 @@ typedef struct {
    * mrt_rates = q relaxation rates or NULL for default_mrt_rates (collision.cpp:76-84). */
   int collision;
   const double* mrt_rates;
+  /* Propagation storage (no reference counterpart): 0 = two PDF copies swapped per
+   * step (the reference T2C scheme, engine.hpp:354-369); 1 = one copy updated in place with the
+   * AA access pattern (half the HBM, bit-identical results; power-of-two tiles, no slab). */
+  int single_copy;
 } splbm_dev_desc;
 
 typedef struct {

@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -102,6 +103,10 @@ struct splbm_dev_engine {
   double* scratch = nullptr;
   std::vector<double> mrt_K;  // MRT operator (host copy; passed to the kernels by value), empty = BGK
   uint64_t device_bytes = 0;
+  uint32_t l2pf = 0;  // step kernel L2 prefetch distance in CTAs (StepArgs::l2pf)
+  // single-copy (AA) propagation: one PDF array (pdf[0]); `read` is then the state parity
+  // (0 natural layout, 1 swapped, see t2c_aa_kernel)
+  bool aa = false;
   int read = 0;
   long step_count = 0;
   uint64_t visits = 0;
@@ -177,11 +182,14 @@ struct splbm_dev_engine {
   }
 
   uint64_t tile_stride() const { return static_cast<uint64_t>(q) * n_tn; }
+  double* cur_pdf() const { return aa ? pdf[0] : pdf[read]; }
+  splbm_dev::StateView view() const { return {nb, a, aa && read == 1 ? 1 : 0}; }
 
   splbm_dev::StepArgs step_args(int rd, int rel) const {
     splbm_dev::StepArgs s{};
-    s.read = pdf[rd];
-    s.write = pdf[1 - rd];
+    s.read = aa ? pdf[0] : pdf[rd];
+    s.write = aa ? pdf[0] : pdf[1 - rd];
+    s.aa = aa ? 1 + rd : 0;
     s.info = info;
     s.nb = nb;
     s.t0 = n_low;
@@ -195,6 +203,7 @@ struct splbm_dev_engine {
     s.failed = failed;
     s.step_base = step_base;
     s.rel = rel;
+    s.l2pf = l2pf;
     if (peer_part1) {
       s.peer_up = peer_pdf_up[1 - rd];
       s.peer_down = peer_pdf_down[1 - rd] ? peer_pdf_down[1 - rd] + peer_down_halo0 * tile_stride() : nullptr;
@@ -218,6 +227,7 @@ struct splbm_dev_engine {
   // Slab-overlap parts: 1 = the bottom and top owned planes (their faces are exchanged while
   // part 2, the interior planes, runs); part 2 then swaps the copies and counts the step.
   void step_part(int part) {
+    if (aa) throw config_error("the slab step parts need the two-copy scheme");
     const uint64_t b0 = n_low, b1 = n_low + send_low_tiles;          // bottom plane
     const uint64_t t0 = n_low + n_own - send_high_tiles, t1 = n_low + n_own;  // top plane
     const bool merged = b1 >= t0;  // one or two planes: the boundary covers the whole slab
@@ -249,6 +259,7 @@ struct splbm_dev_engine {
   // Face pack / unpack on the engine stream (see splbm_dev_halo_pack / _unpack for the layout).
   void halo_copy(int copy, uint64_t tile0, uint64_t ntiles, int layer, const int* dirs, double* buf,
                  bool pack) {
+    if (aa) throw config_error("slab halo exchange needs the two-copy scheme");
     if (!ntiles || !buf) return;
     splbm_dev::HaloArgs h{pdf[copy], buf, tile0, ntiles, a, layer, n_halo_dirs, dirs, pack ? 1 : 0};
     CK(splbm_dev::launch_halo(d, h, stream));
@@ -396,6 +407,13 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
   if (d == 2 && desc->dims[2] != 1 && desc->dims[2] != 0)
     throw config_error("2D geometry requires nz = 1");
 
+  if (desc->single_copy) {  // single PDF array, AA access pattern
+    const bool pow2 = e->a == 2 || e->a == 4 || (d == 2 && (e->a == 8 || e->a == 16));
+    if (!pow2) throw config_error("single-copy propagation needs a power-of-two tile (a = 2, 4; 2D a <= 16)");
+    if (desc->slab_z0 != 0 || desc->slab_z1 != 0)
+      throw config_error("single-copy propagation is a single-GPU mode (no slab)");
+    e->aa = true;
+  }
   e->tm = build_tile_map(desc->types, d, dims, e->a, e->periodic);
   TileMap& tm = e->tm;
   e->n_tn = tm.n_tn;
@@ -439,19 +457,28 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
   if (e->device < 0 || e->device >= ndev) throw config_error("invalid CUDA device ordinal");
   CK(cudaSetDevice(e->device));
   if (SPLBM_L2_FETCH > 0) CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, SPLBM_L2_FETCH));
+  {
+    // L2 prefetch distance of the step kernel: half a wave in 3D (4 resident CTAs per SM), two
+    // thirds in 2D (6 per SM); farther ahead the prefetched blocks are evicted before use
+    // (measured). SPLBM_L2PF overrides it (0 = off) for tuning sweeps.
+    int sms = 148;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device));
+    e->l2pf = static_cast<uint32_t>(sms * (d == 3 ? 2 : 4));
+    if (const char* v = std::getenv("SPLBM_L2PF")) e->l2pf = static_cast<uint32_t>(std::atoi(v));
+  }
   CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   CK(cudaEventCreate(&e->ev0));
   CK(cudaEventCreate(&e->ev1));
   const uint64_t nslots = S * e->tile_stride();
   e->pdf[0] = e->alloc<double>(nslots);
-  e->pdf[1] = e->alloc<double>(nslots);
+  if (!e->aa) e->pdf[1] = e->alloc<double>(nslots);
   e->info = e->alloc<uint32_t>(S * n_tn);
   const int nbs = d == 3 ? 27 : 9;  // 2D keeps only the dz = 0 slice (cells 9..17)
   e->nb = e->alloc<uint32_t>(S * nbs);
   e->failed = e->alloc<unsigned long long>(1);
   e->step_base = e->alloc<long long>(1);
   e->domain_err = e->alloc<int>(1);
-  e->scratch = e->alloc<double>(4 * std::min<uint64_t>(kChunkNodes, std::max<uint64_t>(S * n_tn, 1)));
+  e->scratch = e->alloc<double>(std::max<uint64_t>(4 * std::min<uint64_t>(kChunkNodes, std::max<uint64_t>(S * n_tn, 1)), e->tile_stride()));
   if (desc->collision == 1) {  // MRT
     e->mrt_K = mrt_kernel(d, desc->tau, desc->mrt_rates);
   } else if (desc->collision != 0) {
@@ -471,7 +498,7 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
   }
   CK(cudaMemsetAsync(e->step_base, 0, sizeof(long long), e->stream));
   CK(cudaMemsetAsync(e->pdf[0], 0, nslots * 8, e->stream));
-  CK(cudaMemsetAsync(e->pdf[1], 0, nslots * 8, e->stream));
+  if (e->pdf[1]) CK(cudaMemsetAsync(e->pdf[1], 0, nslots * 8, e->stream));
   if (d == 2) {
     std::vector<uint32_t> nb2(S * 9);
     for (uint64_t t = 0; t < S; ++t)
@@ -585,7 +612,7 @@ static int initialize_impl(splbm_dev_engine* e, const double* rho, const double*
       const uint64_t cnt = std::min(kChunkNodes, total - node0);
       splbm_dev::InitArgs ia{};
       ia.pdf0 = e->pdf[0];
-      ia.pdf1 = e->pdf[1];
+      ia.pdf1 = e->pdf[1];  // nullptr in single-copy mode
       ia.node0 = node0;
       ia.count = cnt;
       ia.n_tn = e->n_tn;
@@ -714,7 +741,8 @@ int splbm_dev_fields(splbm_dev_engine* e, double* rho, double* ux, double* uy, d
     for (uint64_t k0 = 0; k0 < total; k0 += chunk) {
       const uint64_t cnt = std::min(chunk, total - k0);
       splbm_dev::MomentsArgs ma{};
-      ma.pdf = e->pdf[e->read];
+      ma.pdf = e->cur_pdf();
+      ma.view = e->view();
       ma.info = e->info;
       ma.rho = e->scratch;
       ma.ux = e->scratch + cnt;
@@ -763,8 +791,8 @@ int splbm_dev_reduce(splbm_dev_engine* e, double out[3]) {
     checked(e);
     const int blocks = 1184;  // 8 x 148 SMs, fixed so the summation order is fixed
     double* dev = e->alloc<double>(3 * blocks + 3);
-    splbm_dev::ReduceArgs ra{e->pdf[e->read], e->info, e->n_low * e->n_tn, e->n_own * e->n_tn,
-                             e->n_tn, dev};
+    splbm_dev::ReduceArgs ra{e->cur_pdf(), e->info, e->view(), e->n_low * e->n_tn,
+                             e->n_own * e->n_tn, e->n_tn, dev};
     cudaError_t err = splbm_dev::launch_reduce(e->d, e->incompressible != 0, ra, blocks,
                                                dev + 3 * blocks, e->stream);
     e->launches += 2;
@@ -780,8 +808,21 @@ int splbm_dev_reduce(splbm_dev_engine* e, double out[3]) {
 int splbm_dev_get_pdf(splbm_dev_engine* e, double* f_out) {
   return guarded([&] {
     checked(e);
-    CK(cudaMemcpyAsync(f_out, e->pdf[e->read], e->n_stored * e->tile_stride() * 8,
-                       cudaMemcpyDeviceToHost, e->stream));
+    const uint64_t stride = e->tile_stride();
+    if (!e->view().swapped) {
+      CK(cudaMemcpyAsync(f_out, e->cur_pdf(), e->n_stored * stride * 8, cudaMemcpyDeviceToHost,
+                         e->stream));
+    } else {  // swapped single-copy state: natural layout through the staging buffer, by tiles
+      const uint64_t per = std::max<uint64_t>(1, 4 * std::min<uint64_t>(kChunkNodes, std::max<uint64_t>(e->n_stored * e->n_tn, 1)) / stride);
+      for (uint64_t t0 = 0; t0 < e->n_stored; t0 += per) {
+        const uint64_t nt = std::min(per, e->n_stored - t0);
+        CK(splbm_dev::launch_unswap(e->d, e->cur_pdf(), e->info, e->view(), e->n_tn, t0, nt,
+                                    e->scratch, e->stream));
+        ++e->launches;
+        CK(cudaMemcpyAsync(f_out + t0 * stride, e->scratch, nt * stride * 8, cudaMemcpyDeviceToHost,
+                           e->stream));
+      }
+    }
     CK(cudaStreamSynchronize(e->stream));
   });
 }
@@ -789,7 +830,8 @@ int splbm_dev_get_pdf(splbm_dev_engine* e, double* f_out) {
 int splbm_dev_set_pdf(splbm_dev_engine* e, const double* f) {
   return guarded([&] {
     checked(e);
-    CK(cudaMemcpyAsync(e->pdf[e->read], f, e->n_stored * e->tile_stride() * 8,
+    if (e->aa) e->read = 0;  // a natural-layout state
+    CK(cudaMemcpyAsync(e->cur_pdf(), f, e->n_stored * e->tile_stride() * 8,
                        cudaMemcpyHostToDevice, e->stream));
     CK(cudaStreamSynchronize(e->stream));
   });
@@ -893,6 +935,7 @@ int splbm_dev_p2p_attach(splbm_dev_engine* e, const uint8_t* lower_blob, const u
   return guarded([&] {
     checked(e);
     if (e->p2p || e->comm) throw config_error("engine already has a halo transport");
+    if (e->aa) throw config_error("slab halo exchange needs the two-copy scheme");
     if (!e->mrt_K.empty()) throw config_error("peer-store halos are built for the BGK kernels");
     if (!e->flags) throw config_error("call splbm_dev_ipc_blob before attaching");
     if (e->a != 4 && e->a != 2 && !(e->d == 2 && (e->a == 8 || e->a == 16)))
@@ -949,6 +992,7 @@ int splbm_dev_comm_attach(splbm_dev_engine* e, const uint8_t* id, int world, int
   return guarded([&] {
     checked(e);
     if (e->comm) throw config_error("engine already has a communicator");
+    if (e->aa) throw config_error("slab halo exchange needs the two-copy scheme");
     if (!id || world < 1 || rank < 0 || rank >= world || lower_rank >= world || upper_rank >= world)
       throw config_error("invalid communicator arguments");
     ncclUniqueId uid;

@@ -52,6 +52,48 @@ __device__ __forceinline__ void st_stream(double* p, double v) {
 #endif
 }
 
+// L2 prefetch of a future CTA's read blocks (the CTA StepArgs::l2pf CTAs ahead, about half a
+// wave): one bulk request per tile block (Q*NTN doubles, contiguous) holds no registers, so more
+// DRAM reads are in flight than the gather alone keeps. Whole blocks measured faster than
+// per-direction or non-solid-row requests even on sparse media.
+template <int Q, int NTN, int TILES>
+__device__ __forceinline__ void l2_prefetch_blocks(const double* pdf, uint64_t tile, bool valid) {
+  if (threadIdx.x < TILES && valid)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pdf + tile * Q * NTN),
+                 "r"(static_cast<uint32_t>(Q * NTN * sizeof(double))) : "memory");
+}
+
+// Slot the natural-state gather of direction i reads for node (t, p) (engine.hpp:485-501): the
+// source x - e_i in its tile, or the own opposite slot when the direction is blocked. Generic
+// tile edge; the neighbour tile comes from the stored nb table.
+template <int D>
+__device__ __forceinline__ uint64_t gather_slot(const uint32_t* nb, uint32_t info, int a, int n_tn,
+                                                uint64_t t, int p, int i) {
+  constexpr uint64_t Q = Lat<D>::Q;
+  if ((info >> i) & 1u) return (t * Q + opp(i)) * n_tn + p;
+  int sx = p % a - ex<D>(i), sy = (p / a) % a - ey<D>(i), sz = (D == 3 ? p / (a * a) : 0) - ez<D>(i);
+  int dx = 0, dy = 0, dz = 0;
+  if (sx < 0) { dx = -1; sx += a; } else if (sx >= a) { dx = 1; sx -= a; }
+  if (sy < 0) { dy = -1; sy += a; } else if (sy >= a) { dy = 1; sy -= a; }
+  if (D == 3) {
+    if (sz < 0) { dz = -1; sz += a; } else if (sz >= a) { dz = 1; sz -= a; }
+  }
+  const int delta = (dx + 1) + 3 * ((dy + 1) + 3 * (dz + 1));
+  const uint64_t u = delta == 13 ? t : nb[t * nb_stride<D>() + delta - nb_offset<D>()];
+  return (u * Q + i) * n_tn + (sx + a * (sy + a * sz));
+}
+
+// The post-collision PDFs S[x][.] of node (t, p) in the current state (StateView).
+template <int D>
+__device__ __forceinline__ void load_state(const double* pdf, uint32_t info, const StateView& v,
+                                           int n_tn, uint64_t t, int p, double* f) {
+  constexpr int Q = Lat<D>::Q;
+#pragma unroll
+  for (int i = 0; i < Q; ++i)
+    f[i] = v.swapped ? pdf[gather_slot<D>(v.nb, info, v.a, n_tn, t, p, opp(i))]
+                     : pdf[(t * Q + i) * static_cast<uint64_t>(n_tn) + p];
+}
+
 // ---------------------------------------------------------------------------------------------
 // The fused gather-propagation + BGK/boundary + store step (engine.hpp:466-514, collision.hpp:35-65,
 // engine.hpp:32-65). A > 0 is a compile-time tile edge; A == 0 reads a_rt.
@@ -165,6 +207,7 @@ __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SP
   const bool live = tloc < n_tiles;
   const uint64_t t = args.t0 + tloc + (tloc >= args.skip_at ? args.skip_by : 0);
   const uint32_t info = live ? __ldg(args.info + t * NTN + p) : 0u;
+  const uint64_t pf = tile_blk + static_cast<uint64_t>(args.l2pf) * TILES + threadIdx.x;
   __syncthreads();
 #if SPLBM_PDL
   // Everything above reads only static tables (nb, info); the PDFs of the previous step are
@@ -172,6 +215,8 @@ __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SP
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
+  l2_prefetch_blocks<Q, NTN, TILES>(args.read, args.t0 + pf + (pf >= args.skip_at ? args.skip_by : 0),
+                                    args.l2pf && pf < n_tiles);
   const int type = (info >> 24) & 3;
   double* wr = args.write + t * STRIDE + p;
   if (type == 0) {
@@ -230,6 +275,97 @@ __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SP
     for (int i = 0; i < Q; ++i)
       if ((D == 3 ? ez<D>(i) : ey<D>(i)) < 0) dst[i * NTN] = f[i];
   }
+}
+
+// Single-copy propagation (the AA access pattern on the reference's tile layout). One
+// PDF array, updated in place; results are bit-identical to the two-copy T2C step because every
+// node applies the same arithmetic to the same incoming values. With addr(i) = the slot the
+// natural gather of direction i reads (source x - e_i, or the own opposite slot if blocked):
+//   PHASE 1 (natural state):  f_i = *addr(i); collide; *addr(opp(i)) = f*_i   -> swapped state
+//   PHASE 2 (swapped state):  f_i = own[opp(i)];  collide; own[i] = f*_i       -> natural state
+// Each node reads and writes exactly the slots of its own set, so the in-place update is race
+// free; phase 2 touches only the node's own slots (no neighbour tables, no cross-tile reads).
+template <int D, int LOGA, bool INC, bool MRT, int PHASE>
+__global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2))
+    t2c_aa_kernel(StepArgs args, const __grid_constant__ MrtMatrix<MRT ? Lat<D>::Q : 1> mrt) {
+  constexpr int Q = Lat<D>::Q;
+  constexpr int A = 1 << LOGA;
+  constexpr int NTN = D == 3 ? A * A * A : A * A;
+  constexpr int TILES = kThreads / NTN;
+  constexpr uint64_t STRIDE = static_cast<uint64_t>(Q) * NTN;
+  constexpr int NBS = nb_stride<D>();
+  __shared__ double* s_base[PHASE == 1 ? TILES : 1][NBS];
+
+  double* const pdf = args.write;
+  const uint64_t n_tiles = args.n_nodes / NTN;
+  const uint64_t tile_blk = static_cast<uint64_t>(blockIdx.x) * TILES;
+  if constexpr (PHASE == 1) {
+    for (int k = threadIdx.x; k < TILES * NBS; k += kThreads) {
+      const int tl = k / NBS, dd = k % NBS;
+      const uint64_t tt = tile_blk + tl;
+      double* b = nullptr;
+      if (tt < n_tiles) {
+        const uint32_t s = __ldg(args.nb + (args.t0 + tt) * NBS + dd);
+        b = s == kEmpty ? nullptr : pdf + static_cast<uint64_t>(s) * STRIDE;
+      }
+      s_base[tl][dd] = b;
+    }
+  }
+  const int tl = threadIdx.x / NTN;
+  const int p = threadIdx.x % NTN;
+  const uint64_t tloc = tile_blk + tl;
+  const uint64_t t = args.t0 + tloc;
+  const uint32_t info = tloc < n_tiles ? __ldg(args.info + t * NTN + p) : 0u;
+  if constexpr (PHASE == 1) __syncthreads();
+#if SPLBM_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+  {
+    const uint64_t pf = tile_blk + static_cast<uint64_t>(args.l2pf) * TILES + threadIdx.x;
+    l2_prefetch_blocks<Q, NTN, TILES>(pdf, args.t0 + pf, args.l2pf && pf < n_tiles);
+  }
+  const int type = (info >> 24) & 3;
+  double* own = pdf + t * STRIDE;
+  if (type == 0) {  // solid slots are never read: whole store sectors (see file header)
+    if (info & (1u << 27)) {
+#pragma unroll
+      for (int i = 0; i < Q; ++i) st_stream(own + i * NTN + p, 0.0);
+    }
+    return;
+  }
+  const int lx = p & (A - 1);
+  const int ly = (p >> LOGA) & (A - 1);
+  const int lz = D == 3 ? (p >> (2 * LOGA)) : 0;
+  double* const* nbp = s_base[PHASE == 1 ? tl : 0];
+  auto addr = [&](int i) -> double* {  // PHASE 1 only
+    const int vx = lx - ex<D>(i), vy = ly - ey<D>(i), vz = lz - ez<D>(i);
+    const int dx = ex<D>(i) ? (vx >> LOGA) : 0;
+    const int dy = ey<D>(i) ? (vy >> LOGA) : 0;
+    const int dz = (D == 3 && ez<D>(i)) ? (vz >> LOGA) : 0;
+    const int sp = (vx & (A - 1)) | ((vy & (A - 1)) << LOGA) | (D == 3 ? ((vz & (A - 1)) << (2 * LOGA)) : 0);
+    const int delta = 13 + dx + 3 * dy + 9 * dz;
+    double* src = (delta == 13 ? own : nbp[delta - nb_offset<D>()]) + (i * NTN + sp);
+    double* bb = own + (opp(i) * NTN + p);
+    return ((info >> i) & 1u) ? bb : src;
+  };
+
+  double f[Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) f[i] = __ldg(PHASE == 1 ? addr(i) : own + (opp(i) * NTN + p));
+
+  bool good;
+  if (type == 1) {
+    if constexpr (MRT)
+      good = collide_mrt<D, INC>(f, mrt.K);
+    else
+      good = collide_bgk<D, INC>(f, args.inv_tau);
+  } else {
+    good = apply_boundary<D, INC>(f, type, (info >> 26) & 1u, args.bc);
+  }
+  if (!good) atomicMin(args.failed, static_cast<unsigned long long>(*args.step_base + args.rel + 1));
+#pragma unroll
+  for (int i = 0; i < Q; ++i) st_stream(PHASE == 1 ? addr(opp(i)) : own + (i * NTN + p), f[i]);
 }
 
 // Advances the step counter the failure stamps are relative to (one per enqueued batch).
@@ -312,7 +448,7 @@ __global__ void init_kernel(InitArgs args) {
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
     args.pdf0[base + static_cast<uint64_t>(i) * args.n_tn] = f[i];
-    args.pdf1[base + static_cast<uint64_t>(i) * args.n_tn] = f[i];
+    if (args.pdf1) args.pdf1[base + static_cast<uint64_t>(i) * args.n_tn] = f[i];
   }
 }
 
@@ -330,9 +466,7 @@ __global__ void moments_kernel(MomentsArgs args) {
   double r = 0.0, m0 = 0.0, m1 = 0.0, m2 = 0.0;
   if (type != 0) {
     double f[Q];
-    const double* src = args.pdf + t * static_cast<uint64_t>(Q) * args.n_tn + p;
-#pragma unroll
-    for (int i = 0; i < Q; ++i) f[i] = src[static_cast<uint64_t>(i) * args.n_tn];
+    load_state<D>(args.pdf, args.info[node], args.view, args.n_tn, t, p, f);
     r = density<D>(f);
     m0 = momentum<D, 0>(f);
     m1 = momentum<D, 1>(f);
@@ -369,9 +503,7 @@ __global__ void __launch_bounds__(kThreads) reduce_partial_kernel(ReduceArgs arg
     const uint64_t t = node / args.n_tn;
     const int p = static_cast<int>(node % args.n_tn);
     double f[Q];
-    const double* src = args.pdf + t * static_cast<uint64_t>(Q) * args.n_tn + p;
-#pragma unroll
-    for (int i = 0; i < Q; ++i) f[i] = src[static_cast<uint64_t>(i) * args.n_tn];
+    load_state<D>(args.pdf, args.info[node], args.view, args.n_tn, t, p, f);
     const double r = density<D>(f);
     double u0 = momentum<D, 0>(f), u1 = momentum<D, 1>(f), u2 = momentum<D, 2>(f);
     if (!INC && r != 0.0) {
@@ -445,6 +577,28 @@ __global__ void halo_copy_kernel(HaloArgs args) {
     args.pdf[slot] = args.buf[k];
 }
 
+// Natural-layout copy of a tile range of the current state (parity dumps of a swapped AA state).
+template <int D>
+__global__ void unswap_kernel(const double* pdf, const uint32_t* info, StateView v, int n_tn,
+                              uint64_t tile0, uint64_t n_tiles, double* out) {
+  constexpr int Q = Lat<D>::Q;
+  const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n_tiles * n_tn) return;
+  const uint64_t t = tile0 + k / n_tn;
+  const int p = static_cast<int>(k % n_tn);
+  const uint32_t w = info[t * n_tn + p];
+  double f[Q];
+  if (((w >> 24) & 3) == 0) {  // solid slots are not part of the state: copied as stored
+#pragma unroll
+    for (int i = 0; i < Q; ++i) f[i] = pdf[(t * Q + i) * static_cast<uint64_t>(n_tn) + p];
+  } else {
+    load_state<D>(pdf, w, v, n_tn, t, p, f);
+  }
+  double* o = out + (k / n_tn) * Q * n_tn + p;
+#pragma unroll
+  for (int i = 0; i < Q; ++i) o[static_cast<uint64_t>(i) * n_tn] = f[i];
+}
+
 // Self-test of the shared-reciprocal division against IEEE division (tests/test_device_division.py).
 __global__ void divide_selftest_kernel(uint64_t n, const double* m, const double* rho, double* out) {
   const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -465,22 +619,8 @@ static MrtMatrix<Q> mrt_param(const double* K) {
   return m;
 }
 
-template <int D, int LOGA, bool INC>
-static void launch_pow2(const StepArgs& a, cudaStream_t st) {
-  constexpr int NTN = D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA));
-  constexpr int TILES = kThreads / NTN;
-  const uint64_t tiles = a.n_nodes / NTN;
-  const unsigned blocks = static_cast<unsigned>((tiles + TILES - 1) / TILES);
-  const MrtMatrix<1> none{};
-  if (a.mrt_K) {
-    t2c_step_pow2_kernel<D, LOGA, INC, false, true>
-        <<<blocks, kThreads, 0, st>>>(a, mrt_param<Lat<D>::Q>(a.mrt_K));
-    return;
-  }
-  if (a.peer_up || a.peer_down) {  // slab boundary planes with NVLink peer stores
-    t2c_step_pow2_kernel<D, LOGA, INC, true, false><<<blocks, kThreads, 0, st>>>(a, none);
-    return;
-  }
+template <class Kern, class M>
+static void launch_maybe_pdl(Kern kern, unsigned blocks, cudaStream_t st, const StepArgs& a, const M& m) {
 #if SPLBM_PDL
   // Overlap the next step's launch and static-table prologue with this step's tail; below a few
   // waves (launch-latency-bound domains) the plain launch measured faster.
@@ -494,15 +634,48 @@ static void launch_pow2(const StepArgs& a, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, t2c_step_pow2_kernel<D, LOGA, INC, false, false>, a, none);
+    cudaLaunchKernelEx(&cfg, kern, a, m);
     return;
   }
 #endif
-  t2c_step_pow2_kernel<D, LOGA, INC, false, false><<<blocks, kThreads, 0, st>>>(a, none);
+  kern<<<blocks, kThreads, 0, st>>>(a, m);
+}
+
+template <int D, int LOGA, bool INC, int PHASE>
+static void launch_aa(const StepArgs& a, unsigned blocks, cudaStream_t st) {
+  if (a.mrt_K)
+    launch_maybe_pdl(t2c_aa_kernel<D, LOGA, INC, true, PHASE>, blocks, st, a, mrt_param<Lat<D>::Q>(a.mrt_K));
+  else
+    launch_maybe_pdl(t2c_aa_kernel<D, LOGA, INC, false, PHASE>, blocks, st, a, MrtMatrix<1>{});
+}
+
+template <int D, int LOGA, bool INC>
+static void launch_pow2(const StepArgs& a, cudaStream_t st) {
+  constexpr int NTN = D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA));
+  constexpr int TILES = kThreads / NTN;
+  const uint64_t tiles = a.n_nodes / NTN;
+  const unsigned blocks = static_cast<unsigned>((tiles + TILES - 1) / TILES);
+  const MrtMatrix<1> none{};
+  if (a.aa) {
+    if (a.aa == 1) launch_aa<D, LOGA, INC, 1>(a, blocks, st);
+    else launch_aa<D, LOGA, INC, 2>(a, blocks, st);
+    return;
+  }
+  if (a.mrt_K) {
+    t2c_step_pow2_kernel<D, LOGA, INC, false, true>
+        <<<blocks, kThreads, 0, st>>>(a, mrt_param<Lat<D>::Q>(a.mrt_K));
+    return;
+  }
+  if (a.peer_up || a.peer_down) {  // slab boundary planes with NVLink peer stores
+    t2c_step_pow2_kernel<D, LOGA, INC, true, false><<<blocks, kThreads, 0, st>>>(a, none);
+    return;
+  }
+  launch_maybe_pdl(t2c_step_pow2_kernel<D, LOGA, INC, false, false>, blocks, st, a, none);
 }
 
 template <int D, int A, bool INC>
 static void launch_generic(const StepArgs& a, unsigned blocks, cudaStream_t st) {
+  if (a.aa) return;  // the engine rejects single-copy mode for non-power-of-two tiles
   if (a.mrt_K)
     t2c_step_kernel<D, A, INC, true><<<blocks, kThreads, 0, st>>>(a, mrt_param<Lat<D>::Q>(a.mrt_K));
   else
@@ -590,6 +763,18 @@ cudaError_t launch_reduce(int d, bool inc, const ReduceArgs& a, int blocks, doub
     else reduce_partial_kernel<3, false><<<blocks, kThreads, 0, st>>>(a);
   }
   reduce_final_kernel<<<1, 32, 0, st>>>(a.partial, blocks, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unswap(int d, const double* pdf, const uint32_t* info, StateView v, int n_tn,
+                          uint64_t tile0, uint64_t n_tiles, double* out, cudaStream_t st) {
+  const uint64_t n = n_tiles * n_tn;
+  const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
+  if (blocks == 0) return cudaSuccess;
+  if (d == 2)
+    unswap_kernel<2><<<blocks, 256, 0, st>>>(pdf, info, v, n_tn, tile0, n_tiles, out);
+  else
+    unswap_kernel<3><<<blocks, 256, 0, st>>>(pdf, info, v, n_tn, tile0, n_tiles, out);
   return cudaGetLastError();
 }
 

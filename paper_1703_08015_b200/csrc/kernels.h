@@ -24,6 +24,12 @@ struct StepArgs {
   unsigned long long* failed;  // min failing step number (ULLONG_MAX = none)
   const long long* step_base;  // steps completed before this batch
   int rel;                     // step index within the batch
+  uint32_t l2pf;               // pow2 kernel: bulk-prefetch the read blocks of the CTA this many
+                               // CTAs ahead into L2 (0 = off)
+  // Single-copy (AA) propagation, read == write: 0 = two copies (the reference T2C scheme);
+  // 1 = the step from the natural state (gather from x - e_i, scatter to x + e_i);
+  // 2 = the step from the swapped state (own node only: read slot opp(i), write slot i).
+  int aa;
   // Slab mode, NVLink peer stores (power-of-two tile kernel only): the face layer of my top
   // plane tiles [top_begin, ...) is also stored, for the directions leaving upwards, into the
   // upper neighbour's next copy at its low halo tiles (peer_up = that copy's first halo tile);
@@ -62,9 +68,19 @@ struct InitArgs {
   int* domain_error;
 };
 
+// Where the post-collision value S[x][i] of the current state lives (single copy):
+// two-copy / natural state -> slot (t, i, p); swapped state (after an odd number of AA steps) ->
+// the slot the natural-state gather of direction opp(i) reads (x + e_i, or own slot i if blocked).
+struct StateView {
+  const uint32_t* nb;  // stored tiles x 27 (3D) / 9 (2D); only read when swapped
+  int a;
+  int swapped;
+};
+
 struct MomentsArgs {
   const double* pdf;
   const uint32_t* info;
+  StateView view;
   double* rho;
   double* ux;
   double* uy;
@@ -77,6 +93,7 @@ struct MomentsArgs {
 struct ReduceArgs {
   const double* pdf;
   const uint32_t* info;
+  StateView view;
   uint64_t node0, n_nodes;
   int n_tn;
   double* partial;  // 3 per block
@@ -101,6 +118,9 @@ cudaError_t launch_moments(int d, bool inc, const MomentsArgs& a, cudaStream_t s
 cudaError_t launch_reduce(int d, bool inc, const ReduceArgs& a, int blocks, double* out,
                           cudaStream_t st);
 cudaError_t launch_halo(int d, const HaloArgs& a, cudaStream_t st);
+// Natural-layout copy of tiles [tile0, tile0 + n_tiles) of a (possibly swapped) state into out.
+cudaError_t launch_unswap(int d, const double* pdf, const uint32_t* info, StateView v, int n_tn,
+                          uint64_t tile0, uint64_t n_tiles, double* out, cudaStream_t st);
 cudaError_t launch_divide_selftest(uint64_t n, const double* m, const double* rho, double* out,
                                    cudaStream_t st);
 

@@ -37,12 +37,13 @@ class TileEngineT2C:
     """TileEngineT2C<double> (engine.hpp:311-551) on one B200.
 
     Constructor mirrors `TileEngineT2C(const Geometry&, int a, const FluidModel&, Periodicity)`
-    (engine.hpp:314-315); `device` selects the GPU and `slab=(z0, z1)` the owned tile planes of
-    the multi-GPU slab mode.
+    (engine.hpp:314-315); `device` selects the GPU, `slab=(z0, z1)` the owned tile planes of
+    the multi-GPU slab mode and `single_copy=True` the in-place AA propagation
+    (one PDF array instead of two, bit-identical results).
     """
 
     def __init__(self, g: Geometry, a: int, model: FluidModel, periodic=None, device: int = 0,
-                 slab: tuple | None = None):
+                 slab: tuple | None = None, single_copy: bool = False):
         L = _native.lib()
         q = 9 if g.d == 2 else 19
         rates = None
@@ -66,6 +67,7 @@ class TileEngineT2C:
         desc.slab_z0, desc.slab_z1 = (int(slab[0]), int(slab[1])) if slab else (0, 0)
         desc.collision = int(model.collision)
         desc.mrt_rates = rates.ctypes.data_as(C.c_void_p) if rates is not None else None
+        desc.single_copy = int(bool(single_copy))
         h = C.c_void_p()
         _native.check(L.splbm_dev_create(C.byref(desc), C.byref(h)))
         self._h = h
@@ -74,6 +76,7 @@ class TileEngineT2C:
         self.d = g.d
         self.model = model
         self.periodic = per
+        self.single_copy = bool(single_copy)
         info = _native.DevInfo()
         _native.check(L.splbm_dev_get_info(h, C.byref(info)))
         self.info = info

@@ -34,7 +34,8 @@ def run_one(K=100, W=10):
     }
     for name, mk in cases.items():
         g, per = mk()
-        e = P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8), per)
+        e = P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8), per,
+                            single_copy=os.environ.get("SPLBM_SINGLE_COPY") == "1")
         e.initialize_uniform(1.0, (0.01, 0.0, 0.0))
         k = 1000 if "256_a4" in name else K
         e.step_n(max(W, 64))
@@ -58,6 +59,15 @@ if __name__ == "__main__":
         out = {}
         for name in VARIANTS:
             env = dict(os.environ, SPLBM_LIB=os.path.join(VAR, f"lib_{name}.so"))
+            r = subprocess.run([sys.executable, __file__, "--one"], env=env, capture_output=True,
+                               text=True)
+            out[name] = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else r.stderr[-2000:]
+            print(name, out[name], flush=True)
+        print(json.dumps(out))
+    elif sys.argv[1] == "--run-env":  # runtime variants of the in-tree library: {name: {VAR: value}}
+        out = {}
+        for name, extra in json.loads(sys.argv[2]).items():
+            env = dict(os.environ, **{k: str(v) for k, v in extra.items()})
             r = subprocess.run([sys.executable, __file__, "--one"], env=env, capture_output=True,
                                text=True)
             out[name] = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else r.stderr[-2000:]

@@ -23,7 +23,8 @@ if __name__ == "__main__":
     name = sys.argv[1]
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 6
     g, a, per = CASES[name]()
-    e = P.TileEngineT2C(g, a, P.FluidModel(tau=0.8), per)
+    e = P.TileEngineT2C(g, a, P.FluidModel(tau=0.8), per,
+                        single_copy=os.environ.get("SPLBM_SINGLE_COPY") == "1")
     e.initialize_uniform(1.0, (0.01, 0.0, 0.0))
     ok, _ = e.step_n(steps)
     e.fields()
