@@ -164,6 +164,29 @@ __device__ __forceinline__ double feq(int i, double rho, double u0, double u1, d
   return INC ? dmul(w, dadd(rho, shape)) : dmul(dmul(w, rho), dadd(1.0, shape));
 }
 
+// The equilibria of an opposite pair (i, opp(i) = i + 1, i odd) at once. Negation is exact and
+// round-to-nearest is sign-symmetric, so with cu' = -cu: cu'*3 = -(cu*3), cu'*cu' = cu*cu and
+// (-(cu*3)) + q = q - cu*3 — the pair shares e.u, cu*3 and (cu*cu)*4.5 and each value is still
+// bit-identical to feq() (the reference's per-direction formula, lattice.hpp:78-89).
+template <int D, bool INC>
+__device__ __forceinline__ void feq_pair(int i, double rho, double u0, double u1, double u2,
+                                         double uu15, double& fp, double& fm) {
+  const double cu = edotu<D>(i, u0, u1, u2);
+  const double c3 = dmul(cu, 3.0);
+  const double q = dmul(dmul(cu, cu), 4.5);
+  const double sp = dsub(dadd(c3, q), uu15);
+  const double sm = dsub(dsub(q, c3), uu15);
+  const double w = Lat<D>::w(i);
+  if (INC) {
+    fp = dmul(w, dadd(rho, sp));
+    fm = dmul(w, dadd(rho, sm));
+  } else {
+    const double wr = dmul(w, rho);
+    fp = dmul(wr, dadd(1.0, sp));
+    fm = dmul(wr, dadd(1.0, sm));
+  }
+}
+
 __device__ __forceinline__ double sqnorm(double u0, double u1, double u2) {
   return dadd(dadd(dmul(u0, u0), dmul(u1, u1)), dmul(u2, u2));
 }
@@ -172,8 +195,10 @@ template <int D, bool INC>
 __device__ __forceinline__ void equilibrium(double rho, double u0, double u1, double u2,
                                             double* out) {
   const double uu = sqnorm(u0, u1, u2);
+  const double uu15 = dmul(uu, 1.5);
+  out[0] = feq<D, INC>(0, rho, u0, u1, u2, uu);
 #pragma unroll
-  for (int i = 0; i < Lat<D>::Q; ++i) out[i] = feq<D, INC>(i, rho, u0, u1, u2, uu);
+  for (int i = 1; i < Lat<D>::Q; i += 2) feq_pair<D, INC>(i, rho, u0, u1, u2, uu15, out[i], out[i + 1]);
 }
 
 // CollisionOperator<T>::operator() BGK branch (collision.hpp:35-65). Returns
@@ -190,10 +215,14 @@ __device__ __forceinline__ bool collide_bgk(double* f, double inv_tau) {
     divide3(u0, u1, u2, rho);
   }
   const double uu = sqnorm(u0, u1, u2);
+  const double uu15 = dmul(uu, 1.5);
+  f[0] = dadd(f[0], dmul(inv_tau, dsub(feq<D, INC>(0, rho, u0, u1, u2, uu), f[0])));
 #pragma unroll
-  for (int i = 0; i < Lat<D>::Q; ++i) {
-    const double fe = feq<D, INC>(i, rho, u0, u1, u2, uu);
-    f[i] = dadd(f[i], dmul(inv_tau, dsub(fe, f[i])));
+  for (int i = 1; i < Lat<D>::Q; i += 2) {
+    double fp, fm;
+    feq_pair<D, INC>(i, rho, u0, u1, u2, uu15, fp, fm);
+    f[i] = dadd(f[i], dmul(inv_tau, dsub(fp, f[i])));
+    f[i + 1] = dadd(f[i + 1], dmul(inv_tau, dsub(fm, f[i + 1])));
   }
   return finite(rho) && finite(u0) && finite(u1) && finite(u2);
 }
@@ -212,10 +241,10 @@ __device__ __forceinline__ bool collide_mrt(double* f, const double* K) {
     if (!(rho > 0.0) || !finite(rho)) return false;
     divide3(u0, u1, u2, rho);
   }
-  const double uu = sqnorm(u0, u1, u2);
   double delta[Q];
+  equilibrium<D, INC>(rho, u0, u1, u2, delta);
 #pragma unroll
-  for (int i = 0; i < Q; ++i) delta[i] = dsub(feq<D, INC>(i, rho, u0, u1, u2, uu), f[i]);
+  for (int i = 0; i < Q; ++i) delta[i] = dsub(delta[i], f[i]);
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
     double acc = 0.0;
