@@ -177,6 +177,10 @@ def other_configs(P, K, W, peak):
              ("configs[1] channel 128^3, MRT incompressible", chan, 4, K, mrt_inc),
              ("configs[1] channel 128^3, single-copy (AA) propagation, half the HBM", chan, 4, K,
               "single_copy"),
+             ("configs[1] channel 128^3, f32 BGK quasi (TileEngineT2C<float>, paper Table 2 f32)",
+              chan, 4, K, "f32"),
+             ("configs[1] channel 128^3, f32 BGK incompressible (paper Table 2 f32 headline model)",
+              chan, 4, K, ("f32", inc)),
              ("configs[0] D2Q9 cavity 256^2 a=4, 1000 steps",
               lambda: P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(256, 256, 1))), 4, 1000,
               None),
@@ -189,13 +193,16 @@ def other_configs(P, K, W, peak):
     for name, mk, a, steps, model in cases:
         g = mk()
         single = model == "single_copy"
-        eng = P.TileEngineT2C(g, a, P.FluidModel(tau=0.8) if single or model is None else model,
-                              single_copy=single)
+        prec = "f32" if model == "f32" or (isinstance(model, tuple) and model[0] == "f32") else "f64"
+        fm = model[1] if isinstance(model, tuple) else model
+        if not isinstance(fm, P.FluidModel):
+            fm = P.FluidModel(tau=0.8)
+        eng = P.TileEngineT2C(g, a, fm, single_copy=single, precision=prec)
         eng.initialize_uniform()
         ms, _, _ = time_steps(eng, steps, W)
         nf = eng.fluid_nodes()
         mlups = nf * steps / (ms * 1e-3) / 1e6
-        gbs = mlups * 1e6 * B_NODE[g.d] / 1e9
+        gbs = mlups * 1e6 * B_NODE[g.d] * (0.5 if prec == "f32" else 1.0) / 1e9
         rows.append({"config": name, "steps": steps, "fluid_nodes": nf,
                      "phi_t": round(eng.info.phi_t, 4), "us_per_step": round(ms / steps * 1e3, 2),
                      "mlups": round(mlups, 1), "achieved_gbs": round(gbs, 1),

@@ -1,7 +1,8 @@
 // Drop-in device engine for the reference solver's C++ API (proj/include/splbm/engine.hpp).
 //
-// TileEngineT2CDevice derives from the reference's Engine<double> and has the TileEngineT2C
-// constructor signature (engine.hpp:314-315), so everything written against Engine<T> — the
+// TileEngineT2CDeviceT<T> derives from the reference's Engine<T> (T = double, or float for the
+// reference's precision=f32 path) and has the TileEngineT2C constructor signature
+// (engine.hpp:314-315); TileEngineT2CDevice = TileEngineT2CDeviceT<double>, so everything written against Engine<T> — the
 // driver run_simulation's loop body, the CLI's bench_one, the test template run_engine<EngineT>
 // (test_engine.cpp:34-39) — runs unchanged on a B200. The implementation is a thin, header-only
 // shim over the C ABI of include/splbm_b200.h (libsplbm_b200.so); status codes are rethrown as the
@@ -12,6 +13,7 @@
 #include <array>
 #include <cstdint>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "splbm/engine.hpp"
@@ -39,13 +41,16 @@ inline void check(int code) {
 
 }  // namespace device_detail
 
-class TileEngineT2CDevice : public Engine<double> {
+template <class T>
+class TileEngineT2CDeviceT : public Engine<T> {
+  static_assert(std::is_same_v<T, double> || std::is_same_v<T, float>, "T2C engines are f64/f32");
+
  public:
   // TileEngineT2C(g, a, model, periodic, pool) — the pool is accepted for signature parity; the
   // step runs on the GPU (`device` selects it).
   // single_copy selects the in-place AA propagation (half the HBM, same results).
-  TileEngineT2CDevice(const Geometry& g, int a, const FluidModel& model, Periodicity periodic = {},
-                      ThreadPool* /*pool*/ = nullptr, int device = 0, bool single_copy = false)
+  TileEngineT2CDeviceT(const Geometry& g, int a, const FluidModel& model, Periodicity periodic = {},
+                       ThreadPool* /*pool*/ = nullptr, int device = 0, bool single_copy = false)
       : d_(g.d), dims_(g.dims), types_(g.types) {
     splbm_dev_desc desc{};
     desc.d = g.d;
@@ -61,6 +66,7 @@ class TileEngineT2CDevice : public Engine<double> {
     desc.collision = model.collision == CollisionKind::MRT ? 1 : 0;
     desc.mrt_rates = model.mrt_rates.empty() ? nullptr : model.mrt_rates.data();
     desc.single_copy = single_copy ? 1 : 0;
+    desc.single_precision = std::is_same_v<T, float> ? 1 : 0;
     if (desc.mrt_rates && static_cast<int>(model.mrt_rates.size()) != (g.d == 2 ? 9 : 19))
       throw ConfigError("mrt_rates must have one entry per moment");
     device_detail::check(splbm_dev_create(&desc, &e_));
@@ -71,9 +77,9 @@ class TileEngineT2CDevice : public Engine<double> {
     device_detail::check(splbm_dev_get_tile_grid(e_, nullptr, origins_.data(), nullptr, nullptr,
                                                  nullptr));
   }
-  ~TileEngineT2CDevice() override { splbm_dev_destroy(e_); }
-  TileEngineT2CDevice(const TileEngineT2CDevice&) = delete;
-  TileEngineT2CDevice& operator=(const TileEngineT2CDevice&) = delete;
+  ~TileEngineT2CDeviceT() override { splbm_dev_destroy(e_); }
+  TileEngineT2CDeviceT(const TileEngineT2CDeviceT&) = delete;
+  TileEngineT2CDeviceT& operator=(const TileEngineT2CDeviceT&) = delete;
 
   // NodeInit evaluated at node_coords(tile, p) of every tile node, solid and padding included,
   // exactly as TileEngineT2C::initialize (engine.hpp:336-352); equilibrium on the device.
@@ -141,5 +147,7 @@ class TileEngineT2CDevice : public Engine<double> {
   std::vector<uint64_t> tile_;
   std::vector<int32_t> origins_;
 };
+
+using TileEngineT2CDevice = TileEngineT2CDeviceT<double>;
 
 }  // namespace splbm

@@ -134,6 +134,9 @@ typedef struct {
    * step (the reference T2C scheme, engine.hpp:354-369); 1 = one copy updated in place with the
    * AA access pattern (half the HBM, bit-identical results; power-of-two tiles, no slab). */
   int single_copy;
+  /* Real type of the engine: 0 = TileEngineT2C<double>; 1 = TileEngineT2C<float> (PDFs and every
+   * node operation in float, the reference's `precision=f32`, tools/splbm.cpp:278; no slab). */
+  int single_precision;
 } splbm_dev_desc;
 
 typedef struct {
@@ -192,9 +195,10 @@ int splbm_dev_fields(splbm_dev_engine* e, double* rho, double* ux, double* uy, d
  * out[1] max |u|, out[2] number of non-finite nodes. */
 int splbm_dev_reduce(splbm_dev_engine* e, double out[3]);
 
-/* Raw PDF copies for parity dumps: slot (t*q+i)*n_tn+p (engine.hpp:397-399), current copy. */
-int splbm_dev_get_pdf(splbm_dev_engine* e, double* f_out);
-int splbm_dev_set_pdf(splbm_dev_engine* e, const double* f);
+/* Raw PDF copies for parity dumps: slot (t*q+i)*n_tn+p (engine.hpp:397-399), current copy, in the
+ * engine's real type (double, or float for single_precision engines); n_tiles_stored*q*n_tn slots. */
+int splbm_dev_get_pdf(splbm_dev_engine* e, void* f_out);
+int splbm_dev_set_pdf(splbm_dev_engine* e, const void* f);
 
 /* Streams and timing. The engine launches on its own stream (cudaStream_t as void*). */
 void* splbm_dev_stream(splbm_dev_engine* e);

@@ -18,6 +18,7 @@ _L = None
 
 _dp = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
 _u8 = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+_fp = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
 _u32 = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
 _i32 = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
 
@@ -57,6 +58,14 @@ def lib():
     L.oracle_fields_digest.argtypes = [C.c_size_t, _u8, _dp, _dp, _dp, _dp]
     L.oracle_fields_digest.restype = C.c_uint64
     L.oracle_wavy.argtypes = [C.c_size_t, _i32, _i32, _i32, _dp, _dp, _dp, _dp]
+    # TileEngineT2C<float> instance of the same restatement (oracle/t2c_real.inc)
+    L.oracle_t2c_initialize_f32.argtypes = [C.c_int, C.c_int64, C.c_int, C.c_int, _dp, _dp, _dp,
+                                            _dp, _fp, _fp]
+    L.oracle_t2c_step_f32.argtypes = [C.c_int, C.c_int, C.c_int64, _u8, _u32, _u8, _fp, _fp,
+                                      C.c_float, C.c_int, _fp, C.c_float, C.c_int, C.c_void_p]
+    L.oracle_t2c_step_f32.restype = C.c_int
+    L.oracle_fields_f32.argtypes = [C.c_int, C.c_int, C.c_int64, _i32, _u8, _i32, _fp, C.c_int,
+                                    _dp, _dp, _dp, _dp, _u8]
     _L = L
     return L
 
@@ -149,11 +158,13 @@ def tile_node_coords(origins, a, d):
 
 
 class OracleT2C:
-    """TileEngineT2C<double> restated in C (engine.hpp:311-551), BGK or MRT."""
+    """TileEngineT2C<T> restated in C (engine.hpp:311-551), BGK or MRT; T = double, or float
+    with precision="f32" (constants, BC values, 1/tau and the MRT operator rounded to float as
+    the reference's T(...) casts do, collision.cpp:93, 108-111; engine.hpp:54-63)."""
 
     def __init__(self, types, d, dims, a=4, tau=0.8, incompressible=False, periodic=0,
                  bc_velocity=(0.0, 0.0, 0.0), bc_density=1.0, threads=1, mrt=False,
-                 mrt_rates=None):
+                 mrt_rates=None, precision="f64"):
         if not tau > 0.5:
             raise ValueError("relaxation time tau must be > 0.5")
         self.d, self.a = d, a
@@ -161,11 +172,14 @@ class OracleT2C:
         self.q = 9 if d == 2 else 19
         self.periodic = _pmask(periodic)
         self.incompressible = int(bool(incompressible))
+        self.f32 = precision == "f32"
+        self.dtype = np.float32 if self.f32 else np.float64
         self.inv_tau = 1.0 / tau
-        self.bc_u = np.asarray(bc_velocity, np.float64)
+        self.bc_u = np.asarray(bc_velocity, self.dtype)
         self.bc_rho = float(bc_density)
         self.threads = threads
-        self.K = np.ascontiguousarray(mrt_kernel(d, tau, mrt_rates)).ravel() if mrt else None
+        self.K = (np.ascontiguousarray(mrt_kernel(d, tau, mrt_rates)).ravel().astype(self.dtype)
+                  if mrt else None)
         self.tiles = build_tiles(types, d, self.dims, a, self.periodic)
         self.T = self.tiles["origins"].shape[0]
         self.n_tn = self.tiles["n_tn"]
@@ -178,7 +192,7 @@ class OracleT2C:
         self.bcdeg = np.where(inside, deg[idx], 0).astype(np.uint8)
         self.ttypes = np.ascontiguousarray(self.tiles["types"]).ravel()
         n = self.T * self.q * self.n_tn
-        self.pdf = [np.zeros(max(n, 1)), np.zeros(max(n, 1))]
+        self.pdf = [np.zeros(max(n, 1), self.dtype), np.zeros(max(n, 1), self.dtype)]
         self.read = 0
         self.step_count = 0
 
@@ -187,8 +201,9 @@ class OracleT2C:
 
     def initialize_arrays(self, rho, ux, uy, uz):
         c = lambda v: np.ascontiguousarray(v, np.float64).ravel()
-        lib().oracle_t2c_initialize(self.d, self.T, self.n_tn, self.incompressible, c(rho), c(ux),
-                                    c(uy), c(uz), self.pdf[0], self.pdf[1])
+        fn = lib().oracle_t2c_initialize_f32 if self.f32 else lib().oracle_t2c_initialize
+        fn(self.d, self.T, self.n_tn, self.incompressible, c(rho), c(ux), c(uy), c(uz),
+           self.pdf[0], self.pdf[1])
         self.read = 0
         self.step_count = 0
 
@@ -203,11 +218,11 @@ class OracleT2C:
     def step(self, n=1):
         """Returns (ok, failed_step) like the C-ABI."""
         for _ in range(n):
-            ok = lib().oracle_t2c_step(self.d, self.a, self.T, self.ttypes, self.nb, self.bcdeg,
-                                       self.pdf[self.read], self.pdf[1 - self.read],
-                                       self.inv_tau, self.incompressible, self.bc_u,
-                                       self.bc_rho, self.threads,
-                                       None if self.K is None else self.K.ctypes.data)
+            fn = lib().oracle_t2c_step_f32 if self.f32 else lib().oracle_t2c_step
+            # the f32 arguments are rounded by ctypes' c_float: T(1.0 / tau), T(bc.density)
+            ok = fn(self.d, self.a, self.T, self.ttypes, self.nb, self.bcdeg, self.pdf[self.read],
+                    self.pdf[1 - self.read], self.inv_tau, self.incompressible, self.bc_u,
+                    self.bc_rho, self.threads, None if self.K is None else self.K.ctypes.data)
             self.read = 1 - self.read
             self.step_count += 1
             if not ok:
@@ -221,7 +236,8 @@ class OracleT2C:
         n = self.dims[0] * self.dims[1] * self.dims[2]
         rho, ux, uy, uz = (np.empty(n) for _ in range(4))
         mask = np.empty(n, np.uint8)
-        rc = lib().oracle_fields(self.d, self.a, self.T,
+        fn = lib().oracle_fields_f32 if self.f32 else lib().oracle_fields
+        rc = fn(self.d, self.a, self.T,
                                  np.ascontiguousarray(self.tiles["origins"]).ravel(), self.ttypes,
                                  np.asarray(self.dims, np.int32), self.pdf[self.read],
                                  self.incompressible, rho, ux, uy, uz, mask)

@@ -64,6 +64,8 @@ def lib(fast: bool = False) -> C.CDLL:
     L.ref_degenerate_mask.argtypes = [vp, C.c_int, _u8]
     L.ref_engine_create.argtypes = [vp, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
                                     C.c_int, C.POINTER(vp)]
+    L.ref_engine_create_p.argtypes = [vp, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
+                                      C.c_int, C.c_int, C.POINTER(vp)]
     L.ref_engine_initialize.argtypes = [vp, C.c_int, C.c_double, _dp]
     L.ref_engine_initialize_fields.argtypes = [vp, _i32, _dp, _dp, _dp, _dp]
     L.ref_engine_step.argtypes = [vp, C.c_long, C.POINTER(C.c_int), C.POINTER(C.c_long),
@@ -207,16 +209,19 @@ def degenerate_mask(geom: RefGeometry, periodic=0) -> np.ndarray:
 
 
 class RefEngine:
-    """The reference Engine<double> (Dense/T2C/TGB) with its own ThreadPool."""
+    """The reference Engine<T> (Dense/T2C/TGB) with its own ThreadPool; T = double, or float with
+    precision="f32" (the reference CLI's precision=f32, tools/splbm.cpp:278)."""
 
     def __init__(self, geom: RefGeometry, method="t2c", a=4, tau=0.8, incompressible=False,
-                 mrt=False, periodic=0, threads=1):
+                 mrt=False, periodic=0, threads=1, precision="f64"):
         self._L = geom._L
         self._geom = geom
         h = C.c_void_p()
-        _check(self._L, self._L.ref_engine_create(geom._h, METHOD[method], a, tau,
-                                                  int(incompressible), int(mrt),
-                                                  per_mask(periodic), threads, C.byref(h)))
+        self.dtype = np.float32 if precision == "f32" else np.float64
+        _check(self._L, self._L.ref_engine_create_p(geom._h, METHOD[method], a, tau,
+                                                    int(incompressible), int(mrt),
+                                                    per_mask(periodic), threads,
+                                                    int(precision == "f32"), C.byref(h)))
         self._h = h
         self.dims = geom.info()[1]
 
@@ -268,7 +273,7 @@ class RefEngine:
 
     def pdf(self):
         n = self._L.ref_engine_pdf(self._h, None)
-        out = np.empty(n)
+        out = np.empty(n, self.dtype)
         self._L.ref_engine_pdf(self._h, out.ctypes.data)
         return out
 

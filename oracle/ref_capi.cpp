@@ -43,6 +43,16 @@ struct MrtKernel {
 template struct Rob<MrtKernel, &CollisionOperator<double>::kernel_>;
 template struct Rob<T2CPdf, &TileEngineT2C<double>::pdf_>;
 template struct Rob<T2CRead, &TileEngineT2C<double>::read_>;
+struct T2CPdfF {
+  using type = std::vector<float> (TileEngineT2C<float>::*)[2];
+  friend type get(T2CPdfF);
+};
+struct T2CReadF {
+  using type = int TileEngineT2C<float>::*;
+  friend type get(T2CReadF);
+};
+template struct Rob<T2CPdfF, &TileEngineT2C<float>::pdf_>;
+template struct Rob<T2CReadF, &TileEngineT2C<float>::read_>;
 
 int code_of(const std::exception& e) {
   if (dynamic_cast<const ConfigError*>(&e)) return 1;
@@ -82,7 +92,12 @@ FluidModel model_of(double tau, int incompressible, int mrt) {
 struct RefEngine {
   int method = 1;  // 0 dense, 1 t2c, 2 tgb
   std::unique_ptr<ThreadPool> pool;
-  std::unique_ptr<Engine<double>> eng;
+  std::unique_ptr<Engine<double>> eng;   // T = double
+  std::unique_ptr<Engine<float>> engf;   // T = float (the CLI's precision=f32)
+  template <class F>
+  auto with(F&& f) {  // the engine, whichever T it was built with
+    return eng ? f(*eng) : f(*engf);
+  }
 };
 
 }  // namespace
@@ -207,8 +222,8 @@ void ref_degenerate_mask(const Geometry* g, int periodic, std::uint8_t* out) {
 }
 
 // ---- engines -----------------------------------------------------------------------
-int ref_engine_create(const Geometry* g, int method, int a, double tau, int incompressible,
-                      int mrt, int periodic, int threads, RefEngine** out) {
+int ref_engine_create_p(const Geometry* g, int method, int a, double tau, int incompressible,
+                        int mrt, int periodic, int threads, int f32, RefEngine** out) {
   GUARD({
     auto* e = new RefEngine;
     e->method = method;
@@ -219,7 +234,10 @@ int ref_engine_create(const Geometry* g, int method, int a, double tau, int inco
     cfg.periodic = per_of(periodic);
     cfg.model = model_of(tau, incompressible, mrt);
     try {
-      e->eng = make_engine<double>(*g, cfg, e->pool.get());
+      if (f32)
+        e->engf = make_engine<float>(*g, cfg, e->pool.get());
+      else
+        e->eng = make_engine<double>(*g, cfg, e->pool.get());
     } catch (...) {
       delete e;
       throw;
@@ -228,14 +246,21 @@ int ref_engine_create(const Geometry* g, int method, int a, double tau, int inco
   })
 }
 
+int ref_engine_create(const Geometry* g, int method, int a, double tau, int incompressible,
+                      int mrt, int periodic, int threads, RefEngine** out) {
+  return ref_engine_create_p(g, method, a, tau, incompressible, mrt, periodic, threads, 0, out);
+}
+
 // init_kind: 0 uniform (rho, u), 1 wavy_init (tests/test_util.hpp:39-46)
 int ref_engine_initialize(RefEngine* e, int init_kind, double rho, const double* u) {
   GUARD({
-    if (init_kind == 1) {
-      e->eng->initialize(splbm::testing::wavy_init);
-    } else {
-      e->eng->initialize_uniform(rho, Eigen::Vector3d(u[0], u[1], u[2]));
-    }
+    e->with([&](auto& eng) {
+      if (init_kind == 1)
+        eng.initialize(splbm::testing::wavy_init);
+      else
+        eng.initialize_uniform(rho, Eigen::Vector3d(u[0], u[1], u[2]));
+      return 0;
+    });
   })
 }
 
@@ -245,11 +270,15 @@ int ref_engine_initialize_fields(RefEngine* e, const int* pdims, const double* r
                                  const double* ux, const double* uy, const double* uz) {
   GUARD({
     const int px = pdims[0], py = pdims[1];
-    e->eng->initialize([=](int x, int y, int z) {
+    const NodeInit init = [=](int x, int y, int z) {
       const std::size_t i = static_cast<std::size_t>(x) +
                             static_cast<std::size_t>(px) *
                                 (static_cast<std::size_t>(y) + static_cast<std::size_t>(py) * z);
       return std::make_pair(rho[i], Eigen::Vector3d(ux[i], uy[i], uz[i]));
+    };
+    e->with([&](auto& eng) {
+      eng.initialize(init);
+      return 0;
     });
   })
 }
@@ -262,11 +291,11 @@ int ref_engine_step(RefEngine* e, long n, int* ok_out, long* failed_step, double
     double wall = 0.0;
     for (long s = 0; s < n; ++s) {
       const auto t0 = std::chrono::steady_clock::now();
-      const bool ok = e->eng->step();
+      const bool ok = e->with([](auto& eng) { return eng.step(); });
       wall += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       if (!ok) {
         *ok_out = 0;
-        *failed_step = e->eng->current_step();
+        *failed_step = e->with([](auto& eng) { return eng.current_step(); });
         break;
       }
     }
@@ -274,17 +303,21 @@ int ref_engine_step(RefEngine* e, long n, int* ok_out, long* failed_step, double
   })
 }
 
-long ref_engine_current_step(const RefEngine* e) { return e->eng->current_step(); }
-std::uint64_t ref_engine_tile_visits(const RefEngine* e) { return e->eng->tile_visits(); }
-void ref_engine_padded_dims(const RefEngine* e, int* out) {
-  const auto p = e->eng->padded_dims();
+long ref_engine_current_step(RefEngine* e) {
+  return e->with([](auto& eng) { return eng.current_step(); });
+}
+std::uint64_t ref_engine_tile_visits(RefEngine* e) {
+  return e->with([](auto& eng) { return eng.tile_visits(); });
+}
+void ref_engine_padded_dims(RefEngine* e, int* out) {
+  const auto p = e->with([](auto& eng) { return eng.padded_dims(); });
   for (int k = 0; k < 3; ++k) out[k] = p[k];
 }
 
-int ref_engine_fields(const RefEngine* e, double* rho, double* ux, double* uy, double* uz,
+int ref_engine_fields(RefEngine* e, double* rho, double* ux, double* uy, double* uz,
                       std::uint8_t* mask, double* mass) {
   GUARD({
-    const FieldData f = e->eng->fields();
+    const FieldData f = e->with([](auto& eng) { return eng.fields(); });
     const std::size_t n = f.size();
     std::memcpy(rho, f.rho.data(), n * 8);
     std::memcpy(ux, f.ux.data(), n * 8);
@@ -296,7 +329,15 @@ int ref_engine_fields(const RefEngine* e, double* rho, double* ux, double* uy, d
 }
 
 // Current (read) PDF copy of a T2C engine, slot (t*q+i)*n_tn+p (engine.hpp:397-399).
-std::uint64_t ref_engine_pdf(RefEngine* e, double* out) {
+std::uint64_t ref_engine_pdf(RefEngine* e, void* out) {
+  if (e->engf) {  // TileEngineT2C<float>: float slots
+    auto* t2c = dynamic_cast<TileEngineT2C<float>*>(e->engf.get());
+    if (!t2c) return 0;
+    const auto& pdf = t2c->*get(T2CPdfF());
+    const int rd = t2c->*get(T2CReadF());
+    if (out) std::memcpy(out, pdf[rd].data(), pdf[rd].size() * sizeof(float));
+    return pdf[rd].size();
+  }
   auto* t2c = dynamic_cast<TileEngineT2C<double>*>(e->eng.get());
   if (!t2c) return 0;
   const auto& pdf = t2c->*get(T2CPdf());

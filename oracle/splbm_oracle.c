@@ -181,297 +181,17 @@ void oracle_degenerate_mask(const uint8_t* types, int d, const int* dims, int pe
       }
 }
 
-/* ---- node physics ------------------------------------------------------------------------ */
-/* equilibrium<T>: lattice.hpp:72-91 (squaredNorm in the shim's left-to-right order) */
-static void equilibrium(const lattice_t* L, int incompressible, double rho, const double* u,
-                        double* out) {
-  const double inv_cs2 = 3.0, inv_2cs4 = 4.5, half_inv_cs2 = 1.5;
-  const double uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
-  for (int i = 0; i < L->q; ++i) {
-    const double cu = (double)L->e[i][0] * u[0] + (double)L->e[i][1] * u[1] + (double)L->e[i][2] * u[2];
-    const double shape = cu * inv_cs2 + cu * cu * inv_2cs4 - uu * half_inv_cs2;
-    if (!incompressible)
-      out[i] = L->w[i] * rho * (1.0 + shape);
-    else
-      out[i] = L->w[i] * (rho + shape);
-  }
-}
-
-/* BGK CollisionOperator::operator(): collision.hpp:35-65. Returns finite_moments
- * (engine.hpp:96-102) of the returned moments. */
-static int collide_bgk(const lattice_t* L, int incompressible, double inv_tau, double* f) {
-  double rho = 0.0, m[3] = {0.0, 0.0, 0.0};
-  for (int i = 0; i < L->q; ++i) {
-    rho += f[i];
-    m[0] += (double)L->e[i][0] * f[i];
-    m[1] += (double)L->e[i][1] * f[i];
-    m[2] += (double)L->e[i][2] * f[i];
-  }
-  if (!incompressible) {
-    if (!(rho > 0.0) || !isfinite(rho)) return 0; /* NaN density, f untouched */
-    m[0] /= rho;
-    m[1] /= rho;
-    m[2] /= rho;
-  }
-  double feq[19];
-  equilibrium(L, incompressible, rho, m, feq);
-  for (int i = 0; i < L->q; ++i) f[i] += inv_tau * (feq[i] - f[i]);
-  return isfinite(rho) && isfinite(m[0]) && isfinite(m[1]) && isfinite(m[2]);
-}
-
-/* CollisionOperator::operator() MRT branch: collision.hpp:54-63 */
-static int collide_mrt(const lattice_t* L, int incompressible, const double* K, double* f) {
-  double rho = 0.0, m[3] = {0.0, 0.0, 0.0};
-  for (int i = 0; i < L->q; ++i) {
-    rho += f[i];
-    m[0] += (double)L->e[i][0] * f[i];
-    m[1] += (double)L->e[i][1] * f[i];
-    m[2] += (double)L->e[i][2] * f[i];
-  }
-  if (!incompressible) {
-    if (!(rho > 0.0) || !isfinite(rho)) return 0;
-    m[0] /= rho;
-    m[1] /= rho;
-    m[2] /= rho;
-  }
-  double feq[19], delta[19];
-  equilibrium(L, incompressible, rho, m, feq);
-  for (int i = 0; i < L->q; ++i) delta[i] = feq[i] - f[i];
-  const double* row = K;
-  for (int i = 0; i < L->q; ++i, row += L->q) {
-    double acc = 0.0;
-    for (int j = 0; j < L->q; ++j) acc += row[j] * delta[j];
-    f[i] += acc;
-  }
-  return isfinite(rho) && isfinite(m[0]) && isfinite(m[1]) && isfinite(m[2]);
-}
-
-/* apply_boundary<T>: engine.hpp:32-65 */
-static int apply_boundary(const lattice_t* L, int incompressible, const double* bc_u,
-                          double bc_rho, int type, double* f, int rho_underdetermined) {
-  if (type == 2) { /* VelocityBC */
-    double rho = 1.0;
-    if (!rho_underdetermined) {
-      rho = 0.0;
-      for (int i = 0; i < L->q; ++i) rho += f[i];
-      if (!(rho > 0.0) || !isfinite(rho)) rho = 1.0;
-    }
-    equilibrium(L, incompressible, rho, bc_u, f);
-    return isfinite(rho) && isfinite(bc_u[0]) && isfinite(bc_u[1]) && isfinite(bc_u[2]);
-  }
-  double rho = 0.0, m[3] = {0.0, 0.0, 0.0};
-  for (int i = 0; i < L->q; ++i) {
-    rho += f[i];
-    m[0] += (double)L->e[i][0] * f[i];
-    m[1] += (double)L->e[i][1] * f[i];
-    m[2] += (double)L->e[i][2] * f[i];
-  }
-  double u[3] = {0.0, 0.0, 0.0};
-  if (!incompressible) {
-    if (rho > 0.0) {
-      u[0] = m[0] / rho;
-      u[1] = m[1] / rho;
-      u[2] = m[2] / rho;
-    }
-  } else {
-    u[0] = m[0];
-    u[1] = m[1];
-    u[2] = m[2];
-  }
-  equilibrium(L, incompressible, bc_rho, u, f);
-  return isfinite(bc_rho) && isfinite(u[0]) && isfinite(u[1]) && isfinite(u[2]);
-}
-
-/* ---- engine ------------------------------------------------------------------------------- */
-/* TileEngineT2C::initialize: engine.hpp:336-352; rho/u given per tile node (T*n_tn), i.e. the
- * NodeInit already evaluated at node_coords(tile, p). Writes both copies. */
-void oracle_t2c_initialize(int d, int64_t T, int n_tn, int incompressible, const double* rho,
-                           const double* ux, const double* uy, const double* uz, double* pdf0,
-                           double* pdf1) {
-  lattice_t L;
-  lattice_init(&L, d);
-  double feq[19];
-  for (int64_t t = 0; t < T; ++t)
-    for (int p = 0; p < n_tn; ++p) {
-      const int64_t k = t * n_tn + p;
-      const double u[3] = {ux[k], uy[k], uz[k]};
-      equilibrium(&L, incompressible, rho[k], u, feq);
-      for (int i = 0; i < L.q; ++i) {
-        const size_t s = ((size_t)t * L.q + i) * n_tn + p;
-        pdf0[s] = feq[i];
-        pdf1[s] = feq[i];
-      }
-    }
-}
-
-/* Tile-range worker of the sweep (engine.hpp:466-508); the CPU-baseline threading splits
- * [0,T) into equal contiguous chunks like ThreadPool::parallel_for (thread_pool.hpp:79-82). */
-typedef struct {
-  const lattice_t* L;
-  int a, n_tn;
-  int64_t T;
-  const uint8_t* ttypes;
-  const uint32_t* nb;
-  const uint8_t* bcdeg;
-  const double* read;
-  double* write;
-  double inv_tau;
-  int incompressible;
-  const double* bc_u;
-  double bc_rho;
-  const uint8_t* delta;
-  const uint32_t* src;
-  const double* K; /* MRT operator or NULL (BGK) */
-  int64_t t_begin, t_end;
-  int ok;
-} step_ctx_t;
-
-static void* sweep_range(void* arg) {
-  step_ctx_t* c = (step_ctx_t*)arg;
-  const lattice_t* L = c->L;
-  const int q = L->q, n_tn = c->n_tn;
-  int ok = 1;
-  double fin[19];
-  for (int64_t t = c->t_begin; t < c->t_end; ++t) {
-    const uint8_t* own = c->ttypes + (size_t)t * n_tn;
-    const double* own_pdf = c->read + (size_t)t * q * n_tn;
-    for (int p = 0; p < n_tn; ++p) {
-      const uint8_t type = own[p];
-      if (type == 0) continue;
-      for (int i = 0; i < q; ++i) {
-        const int entry = i * n_tn + p;
-        const int dl = c->delta[entry];
-        const size_t sp = c->src[entry];
-        const double* src_pdf;
-        int blocked;
-        if (dl == 13) {
-          src_pdf = own_pdf;
-          blocked = own[sp] == 0;
-        } else {
-          const uint32_t s = c->nb[(size_t)t * 27 + dl];
-          src_pdf = s == EMPTY_TILE ? NULL : c->read + (size_t)s * q * n_tn;
-          blocked = s == EMPTY_TILE || c->ttypes[(size_t)s * n_tn + sp] == 0;
-        }
-        fin[i] = blocked ? own_pdf[(size_t)L->opp[i] * n_tn + p] : src_pdf[(size_t)i * n_tn + sp];
-      }
-      const int good = type == 1 ? (c->K ? collide_mrt(L, c->incompressible, c->K, fin)
-                                         : collide_bgk(L, c->incompressible, c->inv_tau, fin))
-                                 : apply_boundary(L, c->incompressible, c->bc_u, c->bc_rho, type,
-                                                  fin, c->bcdeg[(size_t)t * n_tn + p] != 0);
-      ok &= good;
-      double* wt = c->write + (size_t)t * q * n_tn;
-      for (int i = 0; i < q; ++i) wt[(size_t)i * n_tn + p] = fin[i];
-    }
-  }
-  c->ok = ok;
-  return NULL;
-}
-
-static void run_chunks(step_ctx_t* ctx, int nthreads) {
-  if (nthreads < 1) nthreads = 1;
-  if (nthreads > 256) nthreads = 256;
-  const int64_t T = ctx->T;
-  const int64_t chunk = (T + nthreads - 1) / nthreads;
-  step_ctx_t sub[256];
-  pthread_t th[256];
-  for (int w = 0; w < nthreads; ++w) {
-    sub[w] = *ctx;
-    sub[w].t_begin = chunk * w < T ? chunk * w : T;
-    sub[w].t_end = sub[w].t_begin + chunk < T ? sub[w].t_begin + chunk : T;
-    if (w > 0) pthread_create(&th[w], NULL, sweep_range, &sub[w]);
-  }
-  sweep_range(&sub[0]);
-  int ok = sub[0].ok;
-  for (int w = 1; w < nthreads; ++w) {
-    pthread_join(th[w], NULL);
-    ok &= sub[w].ok;
-  }
-  ctx->ok = ok;
-}
-
-/* One T2C step: TileEngineT2C::step + sweep, engine.hpp:354-369, 466-514; direction tables
- * delta_/src_ derived as build_neighbor_tables, engine.hpp:419-445. bcdeg is the degenerate
- * flag per tile node (bc_degenerate(t,p), engine.hpp:409-417). Returns the step's ok flag. */
-int oracle_t2c_step(int d, int a, int64_t T, const uint8_t* ttypes, const uint32_t* nb,
-                    const uint8_t* bcdeg, const double* read, double* write, double inv_tau,
-                    int incompressible, const double* bc_u, double bc_rho, int nthreads,
-                    const double* K) {
-  lattice_t L;
-  lattice_init(&L, d);
-  const int q = L.q;
-  const int n_tn = a * a * (d == 3 ? a : 1);
-  uint8_t* delta = (uint8_t*)malloc((size_t)q * n_tn);
-  uint32_t* src = (uint32_t*)malloc((size_t)q * n_tn * 4);
-  for (int i = 0; i < q; ++i)
-    for (int p = 0; p < n_tn; ++p) {
-      int l[3] = {p % a, (p / a) % a, p / (a * a)};
-      int dc[3] = {0, 0, 0};
-      for (int k = 0; k < 3; ++k) {
-        l[k] -= L.e[i][k];
-        const int extent = (k == 2 && d == 2) ? 1 : a;
-        if (l[k] < 0) {
-          dc[k] = -1;
-          l[k] += extent;
-        } else if (l[k] >= extent) {
-          dc[k] = 1;
-          l[k] -= extent;
-        }
-      }
-      delta[i * n_tn + p] = (uint8_t)((dc[0] + 1) + 3 * ((dc[1] + 1) + 3 * (dc[2] + 1)));
-      src[i * n_tn + p] = (uint32_t)(l[0] + a * (l[1] + a * l[2]));
-    }
-  step_ctx_t ctx = {&L, a, n_tn, T, ttypes, nb, bcdeg, read, write, inv_tau, incompressible,
-                    bc_u, bc_rho, delta, src, K, 0, 0, 1};
-  run_chunks(&ctx, nthreads);
-  const int ok = ctx.ok;
-  free(delta);
-  free(src);
-  return ok;
-}
-
-/* TileEngineT2C::fields: engine.hpp:371-390 with moments<T> (lattice.hpp:94-112), scattered
- * to the unpadded raster (fields.hpp:12-23). Returns -2 on the quasi rho==0 DomainError. */
-int oracle_fields(int d, int a, int64_t T, const int32_t* origins, const uint8_t* ttypes,
-                  const int* geo_dims, const double* pdf, int incompressible, double* rho,
-                  double* ux, double* uy, double* uz, uint8_t* mask) {
-  lattice_t L;
-  lattice_init(&L, d);
-  const int q = L.q;
-  const int n_tn = a * a * (d == 3 ? a : 1);
-  const size_t n = (size_t)geo_dims[0] * geo_dims[1] * geo_dims[2];
-  memset(mask, 0, n);
-  memset(rho, 0, n * 8);
-  memset(ux, 0, n * 8);
-  memset(uy, 0, n * 8);
-  memset(uz, 0, n * 8);
-  for (int64_t t = 0; t < T; ++t)
-    for (int p = 0; p < n_tn; ++p) {
-      if (ttypes[(size_t)t * n_tn + p] == 0) continue;
-      double r = 0.0, m[3] = {0.0, 0.0, 0.0};
-      for (int i = 0; i < q; ++i) {
-        const double f = pdf[((size_t)t * q + i) * n_tn + p];
-        r += f;
-        m[0] += (double)L.e[i][0] * f;
-        m[1] += (double)L.e[i][1] * f;
-        m[2] += (double)L.e[i][2] * f;
-      }
-      if (!incompressible) {
-        if (r == 0.0) return -2;
-        m[0] /= r;
-        m[1] /= r;
-        m[2] /= r;
-      }
-      const int x = origins[3 * t] + p % a, y = origins[3 * t + 1] + (p / a) % a,
-                z = origins[3 * t + 2] + p / (a * a);
-      const size_t node = (size_t)x + (size_t)geo_dims[0] * ((size_t)y + (size_t)geo_dims[1] * z);
-      mask[node] = 1;
-      rho[node] = r;
-      ux[node] = m[0];
-      uy[node] = m[1];
-      uz[node] = m[2];
-    }
-  return 0;
-}
+/* ---- node physics and the T2C sweep, for T = double and T = float (oracle/t2c_real.inc) ---- */
+#define REAL double
+#define SFX(name) name
+#include "t2c_real.inc"
+#undef REAL
+#undef SFX
+#define REAL float
+#define SFX(name) name##_f32
+#include "t2c_real.inc"
+#undef REAL
+#undef SFX
 
 /* FieldData::total_mass: fields.hpp:25-31 (sequential, raster order) */
 double oracle_total_mass(size_t n, const double* rho, const uint8_t* mask) {

@@ -34,7 +34,8 @@ class DevDesc(C.Structure):
                 ("bc_velocity", C.c_double * 3), ("bc_density", C.c_double), ("tile", C.c_int),
                 ("tau", C.c_double), ("incompressible", C.c_int), ("periodic", C.c_int),
                 ("device", C.c_int), ("slab_z0", C.c_int), ("slab_z1", C.c_int),
-                ("collision", C.c_int), ("mrt_rates", C.c_void_p), ("single_copy", C.c_int)]
+                ("collision", C.c_int), ("mrt_rates", C.c_void_p), ("single_copy", C.c_int),
+                ("single_precision", C.c_int)]
 
 
 class DevInfo(C.Structure):

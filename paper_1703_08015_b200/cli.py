@@ -118,13 +118,23 @@ def build_model(cfg: Config) -> FluidModel:  # splbm.cpp:118-134
                       tau=cfg.get_float("sim.tau", 0.8))
 
 
+def parse_precision(cfg: Config) -> str:  # splbm.cpp:36-40
+    name = cfg.get("sim.precision", "f64")
+    if name not in ("f32", "f64"):
+        raise ConfigError("precision must be f32 or f64")
+    return name
+
+
 def build_sim(cfg: Config) -> E.SimConfig:  # splbm.cpp:136-150
     method = cfg.get("sim.method", "t2c-b200")
     if method not in ("t2c-b200", "t2c"):
         raise ConfigError(f"unknown method: {method} (the B200 engine is t2c-b200)")
     sim = E.SimConfig(tile=cfg.get_int("sim.tile", 0), steps=cfg.get_int("sim.steps", 0),
                       periodic=parse_periodic(cfg.get("sim.periodic", "")),
-                      model=build_model(cfg), device=cfg.get_int("sim.device", 0))
+                      model=build_model(cfg), device=cfg.get_int("sim.device", 0),
+                      single_copy=cfg.get("sim.storage", "two-copy") == "single-copy")
+    if cfg.get("sim.storage", "two-copy") not in ("two-copy", "single-copy"):
+        raise ConfigError("sim.storage must be two-copy or single-copy")
     sim.initial_density = cfg.get_float("sim.initial_density", 1.0)
     if "sim.initial_velocity" in cfg:
         v = [float(x) for x in cfg["sim.initial_velocity"].replace(",", " ").split()]
@@ -155,8 +165,8 @@ def cmd_stats(cfg, out):  # splbm.cpp:172-225, T2C subset of the overhead report
     tg = build_tile_grid(g, a, parse_periodic(cfg.get("sim.periodic", "")), with_neighbours=False)
     ts = tile_stats(tg)
     p = G.porosity(g)
-    params = O.CostParams(lat=lat, a=a, s_t=cfg.get_float("cost.s_t", 2.0),
-                          s_ti=cfg.get_float("cost.s_ti", 4.0))
+    params = O.CostParams(lat=lat, a=a, s_d=4.0 if parse_precision(cfg) == "f32" else 8.0,
+                          s_t=cfg.get_float("cost.s_t", 2.0), s_ti=cfg.get_float("cost.s_ti", 4.0))
     gs = O.GeometryStats(phi=p.phi, phi_t=ts.phi_t, ratio_tiles=ts.ratio_tiles)
     kv("n_nodes", g.node_count(), out)
     for k, v in (("phi", p.phi), ("eta", p.eta), ("phi_t", ts.phi_t), ("eta_t", ts.eta_t),
@@ -176,7 +186,7 @@ def cmd_stats(cfg, out):  # splbm.cpp:172-225, T2C subset of the overhead report
 
 def cmd_run(cfg, out):  # splbm.cpp:265-293 (VTK/CSV output stays on the reference)
     g = build_geometry(cfg)
-    res = E.run_simulation(g, build_sim(cfg))
+    res = E.run_simulation(g, build_sim(cfg), parse_precision(cfg))
     kv("steps", res.steps, out)
     for k in ("wall_seconds", "mlups", "mass_initial", "mass_final", "mass_drift_rel"):
         kv(k, float(getattr(res, k)), out)
@@ -192,6 +202,7 @@ def cmd_bench(cfg, out):  # splbm.cpp:295-366 for method t2c-b200
     steps = cfg.get_int("bench.steps", max(sim.steps, 50))
     bandwidth = cfg.get_float("bench.mem_bandwidth", 0.0)
     models = cfg.get_list("bench.models") or ["current"]
+    precision = parse_precision(cfg)
     rows = []
     for model in models:
         c = Config(cfg)
@@ -201,7 +212,7 @@ def cmd_bench(cfg, out):  # splbm.cpp:295-366 for method t2c-b200
             coll, comp = model.split("-", 1)
             c["sim.collision"], c["sim.compressibility"] = coll, comp
         s = build_sim(c)
-        eng = E.make_engine(g, s)
+        eng = E.make_engine(g, s, precision)
         eng.initialize_uniform(s.initial_density, s.initial_velocity)
         ok, failed = eng.step_n(warmup)
         if not ok:
@@ -212,8 +223,8 @@ def cmd_bench(cfg, out):  # splbm.cpp:295-366 for method t2c-b200
             raise NumericalError("non-finite state", warmup + failed)
         wall = eng.last_batch_ms() * 1e-3
         mlups = g.fluid_count() * steps / (wall * 1e6) if wall > 0 else 0.0
-        bu = (O.bandwidth_utilization(mlups, O.CostParams(lat=solver_lattice(g.d)), bandwidth)
-              if bandwidth > 0 else None)
+        cost = O.CostParams(lat=solver_lattice(g.d), s_d=4.0 if precision == "f32" else 8.0)
+        bu = O.bandwidth_utilization(mlups, cost, bandwidth) if bandwidth > 0 else None
         rows.append((model, mlups, bu))
     kv("warmup", warmup, out)
     kv("steps", steps, out)

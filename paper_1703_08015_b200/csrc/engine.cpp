@@ -92,7 +92,7 @@ struct splbm_dev_engine {
   uint64_t fluid_nodes = 0;
   // device state
   cudaStream_t stream = nullptr;
-  double* pdf[2] = {nullptr, nullptr};
+  void* pdf[2] = {nullptr, nullptr};  // PDF copies in the engine's real type (double / float)
   uint32_t* info = nullptr;
   uint32_t* nb = nullptr;
   unsigned long long* failed = nullptr;
@@ -107,6 +107,9 @@ struct splbm_dev_engine {
   // single-copy (AA) propagation: one PDF array (pdf[0]); `read` is then the state parity
   // (0 natural layout, 1 swapped, see t2c_aa_kernel)
   bool aa = false;
+  // TileEngineT2C<float> (paper Table 2 f32 rows): PDFs and node arithmetic in float
+  bool f32 = false;
+  int es = 8;  // bytes per PDF slot
   int read = 0;
   long step_count = 0;
   uint64_t visits = 0;
@@ -182,7 +185,7 @@ struct splbm_dev_engine {
   }
 
   uint64_t tile_stride() const { return static_cast<uint64_t>(q) * n_tn; }
-  double* cur_pdf() const { return aa ? pdf[0] : pdf[read]; }
+  void* cur_pdf() const { return aa ? pdf[0] : pdf[read]; }
   splbm_dev::StateView view() const { return {nb, a, aa && read == 1 ? 1 : 0}; }
 
   splbm_dev::StepArgs step_args(int rd, int rel) const {
@@ -220,7 +223,7 @@ struct splbm_dev_engine {
     splbm_dev::StepArgs s = step_args(rd, 0);
     s.t0 = t_begin;
     s.n_nodes = (t_end - t_begin) * n_tn;
-    CK(splbm_dev::launch_step(d, incompressible != 0, s, stream));
+    CK(splbm_dev::launch_step(d, incompressible != 0, f32, s, stream));
     ++launches;
   }
 
@@ -240,7 +243,7 @@ struct splbm_dev_engine {
         s.n_nodes = (send_low_tiles + send_high_tiles) * n_tn;
         s.skip_at = send_low_tiles;
         s.skip_by = t0 - b1;
-        CK(splbm_dev::launch_step(d, incompressible != 0, s, stream));
+        CK(splbm_dev::launch_step(d, incompressible != 0, f32, s, stream));
         ++launches;
       } else {
         launch_range(read, b0, b1);
@@ -260,8 +263,9 @@ struct splbm_dev_engine {
   void halo_copy(int copy, uint64_t tile0, uint64_t ntiles, int layer, const int* dirs, double* buf,
                  bool pack) {
     if (aa) throw config_error("slab halo exchange needs the two-copy scheme");
+    if (f32) throw config_error("slab halo exchange is built for the f64 engine");
     if (!ntiles || !buf) return;
-    splbm_dev::HaloArgs h{pdf[copy], buf, tile0, ntiles, a, layer, n_halo_dirs, dirs, pack ? 1 : 0};
+    splbm_dev::HaloArgs h{static_cast<double*>(pdf[copy]), buf, tile0, ntiles, a, layer, n_halo_dirs, dirs, pack ? 1 : 0};
     CK(splbm_dev::launch_halo(d, h, stream));
     ++launches;
   }
@@ -325,7 +329,7 @@ struct splbm_dev_engine {
   // Enqueue k steps starting from parity rd (direct launches) + the counter bump.
   void enqueue_direct(int rd, int k) {
     for (int r = 0; r < k; ++r) {
-      CK(splbm_dev::launch_step(d, incompressible != 0, step_args(rd, r), stream));
+      CK(splbm_dev::launch_step(d, incompressible != 0, f32, step_args(rd, r), stream));
       rd = 1 - rd;
       ++launches;
     }
@@ -400,7 +404,12 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
   e->periodic = desc->periodic;
   e->incompressible = desc->incompressible ? 1 : 0;
   e->tau = desc->tau;
-  e->inv_tau = 1.0 / desc->tau;  // collision.cpp:93
+  e->f32 = desc->single_precision != 0;
+  e->es = e->f32 ? 4 : 8;
+  // inv_tau_ = T(1.0 / tau) (collision.cpp:93); a float value is exact in the double argument
+  e->inv_tau = e->f32 ? static_cast<double>(static_cast<float>(1.0 / desc->tau)) : 1.0 / desc->tau;
+  if (e->f32 && (desc->slab_z0 != 0 || desc->slab_z1 != 0))
+    throw config_error("the f32 engine is a single-GPU engine (no slab)");
   e->bc = {desc->bc_velocity[0], desc->bc_velocity[1], desc->bc_velocity[2], desc->bc_density};
   e->device = desc->device;
   int dims[3] = {desc->dims[0], desc->dims[1], d == 2 ? 1 : desc->dims[2]};
@@ -470,8 +479,8 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
   CK(cudaEventCreate(&e->ev0));
   CK(cudaEventCreate(&e->ev1));
   const uint64_t nslots = S * e->tile_stride();
-  e->pdf[0] = e->alloc<double>(nslots);
-  if (!e->aa) e->pdf[1] = e->alloc<double>(nslots);
+  e->pdf[0] = e->alloc<char>(nslots * e->es);
+  if (!e->aa) e->pdf[1] = e->alloc<char>(nslots * e->es);
   e->info = e->alloc<uint32_t>(S * n_tn);
   const int nbs = d == 3 ? 27 : 9;  // 2D keeps only the dz = 0 slice (cells 9..17)
   e->nb = e->alloc<uint32_t>(S * nbs);
@@ -497,8 +506,8 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
     CK(cudaMemcpy(e->halo_dirs, dirs.data(), dirs.size() * sizeof(int), cudaMemcpyHostToDevice));
   }
   CK(cudaMemsetAsync(e->step_base, 0, sizeof(long long), e->stream));
-  CK(cudaMemsetAsync(e->pdf[0], 0, nslots * 8, e->stream));
-  if (e->pdf[1]) CK(cudaMemsetAsync(e->pdf[1], 0, nslots * 8, e->stream));
+  CK(cudaMemsetAsync(e->pdf[0], 0, nslots * e->es, e->stream));
+  if (e->pdf[1]) CK(cudaMemsetAsync(e->pdf[1], 0, nslots * e->es, e->stream));
   if (d == 2) {
     std::vector<uint32_t> nb2(S * 9);
     for (uint64_t t = 0; t < S; ++t)
@@ -510,7 +519,7 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
     uint8_t* types_d = nullptr;
     CK(cudaMalloc(&types_d, std::max<std::size_t>(types_local.size(), 1)));
     CK(cudaMemcpyAsync(types_d, types_local.data(), types_local.size(), cudaMemcpyHostToDevice, e->stream));
-    splbm_dev::NodeInfoArgs ni{types_d, e->nb, e->info, S, e->a};
+    splbm_dev::NodeInfoArgs ni{types_d, e->nb, e->info, S, e->a, 32 / e->es};
     CK(splbm_dev::launch_node_info(d, ni, e->stream));
     ++e->launches;
     CK(cudaStreamSynchronize(e->stream));
@@ -633,7 +642,7 @@ static int initialize_impl(splbm_dev_engine* e, const double* rho, const double*
         ia.u0[1] = u0[1];
         ia.u0[2] = u0[2];
       }
-      CK(splbm_dev::launch_init(e->d, e->incompressible != 0, ia, e->stream));
+      CK(splbm_dev::launch_init(e->d, e->incompressible != 0, e->f32, ia, e->stream));
       ++e->launches;
     }
     check_domain_flag(e, "equilibrium requires rho > 0 for the quasi-compressible model");
@@ -752,7 +761,7 @@ int splbm_dev_fields(splbm_dev_engine* e, double* rho, double* ux, double* uy, d
       ma.count = cnt;
       ma.n_tn = n_tn;
       ma.domain_error = e->domain_err;
-      CK(splbm_dev::launch_moments(e->d, e->incompressible != 0, ma, e->stream));
+      CK(splbm_dev::launch_moments(e->d, e->incompressible != 0, e->f32, ma, e->stream));
       ++e->launches;
       CK(cudaMemcpyAsync(stage, e->scratch, 4 * cnt * 8, cudaMemcpyDeviceToHost, e->stream));
       CK(cudaStreamSynchronize(e->stream));
@@ -793,7 +802,7 @@ int splbm_dev_reduce(splbm_dev_engine* e, double out[3]) {
     double* dev = e->alloc<double>(3 * blocks + 3);
     splbm_dev::ReduceArgs ra{e->cur_pdf(), e->info, e->view(), e->n_low * e->n_tn,
                              e->n_own * e->n_tn, e->n_tn, dev};
-    cudaError_t err = splbm_dev::launch_reduce(e->d, e->incompressible != 0, ra, blocks,
+    cudaError_t err = splbm_dev::launch_reduce(e->d, e->incompressible != 0, e->f32, ra, blocks,
                                                dev + 3 * blocks, e->stream);
     e->launches += 2;
     if (err == cudaSuccess)
@@ -805,33 +814,35 @@ int splbm_dev_reduce(splbm_dev_engine* e, double out[3]) {
   });
 }
 
-int splbm_dev_get_pdf(splbm_dev_engine* e, double* f_out) {
+int splbm_dev_get_pdf(splbm_dev_engine* e, void* f_out) {
   return guarded([&] {
     checked(e);
-    const uint64_t stride = e->tile_stride();
+    const uint64_t tile_bytes = e->tile_stride() * e->es;
+    char* out = static_cast<char*>(f_out);
     if (!e->view().swapped) {
-      CK(cudaMemcpyAsync(f_out, e->cur_pdf(), e->n_stored * stride * 8, cudaMemcpyDeviceToHost,
+      CK(cudaMemcpyAsync(out, e->cur_pdf(), e->n_stored * tile_bytes, cudaMemcpyDeviceToHost,
                          e->stream));
     } else {  // swapped single-copy state: natural layout through the staging buffer, by tiles
-      const uint64_t per = std::max<uint64_t>(1, 4 * std::min<uint64_t>(kChunkNodes, std::max<uint64_t>(e->n_stored * e->n_tn, 1)) / stride);
+      const uint64_t scratch_bytes = 8 * std::max<uint64_t>(4 * std::min<uint64_t>(kChunkNodes, std::max<uint64_t>(e->n_stored * e->n_tn, 1)), e->tile_stride());
+      const uint64_t per = std::max<uint64_t>(1, scratch_bytes / tile_bytes);
       for (uint64_t t0 = 0; t0 < e->n_stored; t0 += per) {
         const uint64_t nt = std::min(per, e->n_stored - t0);
-        CK(splbm_dev::launch_unswap(e->d, e->cur_pdf(), e->info, e->view(), e->n_tn, t0, nt,
-                                    e->scratch, e->stream));
+        CK(splbm_dev::launch_unswap(e->d, e->f32, e->cur_pdf(), e->info, e->view(), e->n_tn, t0,
+                                    nt, e->scratch, e->stream));
         ++e->launches;
-        CK(cudaMemcpyAsync(f_out + t0 * stride, e->scratch, nt * stride * 8, cudaMemcpyDeviceToHost,
-                           e->stream));
+        CK(cudaMemcpyAsync(out + t0 * tile_bytes, e->scratch, nt * tile_bytes,
+                           cudaMemcpyDeviceToHost, e->stream));
       }
     }
     CK(cudaStreamSynchronize(e->stream));
   });
 }
 
-int splbm_dev_set_pdf(splbm_dev_engine* e, const double* f) {
+int splbm_dev_set_pdf(splbm_dev_engine* e, const void* f) {
   return guarded([&] {
     checked(e);
     if (e->aa) e->read = 0;  // a natural-layout state
-    CK(cudaMemcpyAsync(e->cur_pdf(), f, e->n_stored * e->tile_stride() * 8,
+    CK(cudaMemcpyAsync(e->cur_pdf(), f, e->n_stored * e->tile_stride() * e->es,
                        cudaMemcpyHostToDevice, e->stream));
     CK(cudaStreamSynchronize(e->stream));
   });
@@ -936,6 +947,7 @@ int splbm_dev_p2p_attach(splbm_dev_engine* e, const uint8_t* lower_blob, const u
     checked(e);
     if (e->p2p || e->comm) throw config_error("engine already has a halo transport");
     if (e->aa) throw config_error("slab halo exchange needs the two-copy scheme");
+    if (e->f32) throw config_error("slab halo exchange is built for the f64 engine");
     if (!e->mrt_K.empty()) throw config_error("peer-store halos are built for the BGK kernels");
     if (!e->flags) throw config_error("call splbm_dev_ipc_blob before attaching");
     if (e->a != 4 && e->a != 2 && !(e->d == 2 && (e->a == 8 || e->a == 16)))
@@ -993,6 +1005,7 @@ int splbm_dev_comm_attach(splbm_dev_engine* e, const uint8_t* id, int world, int
     checked(e);
     if (e->comm) throw config_error("engine already has a communicator");
     if (e->aa) throw config_error("slab halo exchange needs the two-copy scheme");
+    if (e->f32) throw config_error("slab halo exchange is built for the f64 engine");
     if (!id || world < 1 || rank < 0 || rank >= world || lower_rank >= world || upper_rank >= world)
       throw config_error("invalid communicator arguments");
     ncclUniqueId uid;

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "lattice.cuh"
 #include "kernels.h"
@@ -51,16 +52,23 @@ __device__ __forceinline__ void st_stream(double* p, double v) {
   *p = v;
 #endif
 }
+__device__ __forceinline__ void st_stream(float* p, float v) {
+#if SPLBM_STORE_CS
+  asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+#else
+  *p = v;
+#endif
+}
 
 // L2 prefetch of a future CTA's read blocks (the CTA StepArgs::l2pf CTAs ahead, about half a
 // wave): one bulk request per tile block (Q*NTN doubles, contiguous) holds no registers, so more
 // DRAM reads are in flight than the gather alone keeps. Whole blocks measured faster than
 // per-direction or non-solid-row requests even on sparse media.
-template <int Q, int NTN, int TILES>
-__device__ __forceinline__ void l2_prefetch_blocks(const double* pdf, uint64_t tile, bool valid) {
+template <int Q, int NTN, int TILES, class R>
+__device__ __forceinline__ void l2_prefetch_blocks(const R* pdf, uint64_t tile, bool valid) {
   if (threadIdx.x < TILES && valid)
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pdf + tile * Q * NTN),
-                 "r"(static_cast<uint32_t>(Q * NTN * sizeof(double))) : "memory");
+                 "r"(static_cast<uint32_t>(Q * NTN * sizeof(R))) : "memory");
 }
 
 // Slot the natural-state gather of direction i reads for node (t, p) (engine.hpp:485-501): the
@@ -84,9 +92,9 @@ __device__ __forceinline__ uint64_t gather_slot(const uint32_t* nb, uint32_t inf
 }
 
 // The post-collision PDFs S[x][.] of node (t, p) in the current state (StateView).
-template <int D>
-__device__ __forceinline__ void load_state(const double* pdf, uint32_t info, const StateView& v,
-                                           int n_tn, uint64_t t, int p, double* f) {
+template <int D, class R>
+__device__ __forceinline__ void load_state(const R* pdf, uint32_t info, const StateView& v,
+                                           int n_tn, uint64_t t, int p, R* f) {
   constexpr int Q = Lat<D>::Q;
 #pragma unroll
   for (int i = 0; i < Q; ++i)
@@ -97,10 +105,11 @@ __device__ __forceinline__ void load_state(const double* pdf, uint32_t info, con
 // ---------------------------------------------------------------------------------------------
 // The fused gather-propagation + BGK/boundary + store step (engine.hpp:466-514, collision.hpp:35-65,
 // engine.hpp:32-65). A > 0 is a compile-time tile edge; A == 0 reads a_rt.
-template <int D, int A, bool INC, bool MRT>
+template <int D, int A, bool INC, bool MRT, class R>
 __global__ void __launch_bounds__(kThreads)
-    t2c_step_kernel(StepArgs args, const __grid_constant__ MrtMatrix<MRT ? Lat<D>::Q : 1> mrt) {
+    t2c_step_kernel(StepArgs args, const __grid_constant__ MrtMatrix<R, MRT ? Lat<D>::Q : 1> mrt) {
   constexpr int Q = Lat<D>::Q;
+  const R* const rd = static_cast<const R*>(args.read);
   const int a = A > 0 ? A : args.a;
   const int az = D == 3 ? a : 1;
   const int n_tn = a * a * az;
@@ -114,21 +123,21 @@ __global__ void __launch_bounds__(kThreads)
   const uint32_t info = __ldg(args.info + node);
   const int type = (info >> 24) & 3;
   const uint64_t tile_stride = static_cast<uint64_t>(Q) * n_tn;
-  double* wr = args.write + t * tile_stride + p;
+  R* wr = static_cast<R*>(args.write) + t * tile_stride + p;
   if (type == 0) {
     if (info & (1u << 27)) {
 #pragma unroll
-      for (int i = 0; i < Q; ++i) st_stream(wr + i * n_tn, 0.0);
+      for (int i = 0; i < Q; ++i) st_stream(wr + i * n_tn, R(0));
     }
     return;
   }
   const int lx = p % a;
   const int ly = (p / a) % a;
   const int lz = D == 3 ? p / (a * a) : 0;
-  const double* own = args.read + t * tile_stride;
+  const R* own = rd + t * tile_stride;
   const uint32_t* nbt = args.nb + t * nb_stride<D>() - nb_offset<D>();
 
-  double f[Q];
+  R f[Q];
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
     // source node x - e_i (engine.hpp:421-445): local coordinates and neighbour cell offset
@@ -146,14 +155,14 @@ __global__ void __launch_bounds__(kThreads)
     const int delta = (dx + 1) + 3 * ((dy + 1) + 3 * (dz + 1));
     const int sp = sx + a * (sy + a * sz);
     const bool blocked = (info >> i) & 1u;
-    const double* src;
+    const R* src;
     if (blocked) {
       src = own + opp(i) * n_tn + p;  // half-way bounce-back (engine.hpp:498-500)
     } else if (delta == 13) {
       src = own + i * n_tn + sp;
     } else {
       const uint64_t s = __ldg(nbt + delta);
-      src = args.read + s * tile_stride + i * n_tn + sp;
+      src = rd + s * tile_stride + i * n_tn + sp;
     }
     f[i] = __ldg(src);
   }
@@ -163,7 +172,7 @@ __global__ void __launch_bounds__(kThreads)
     if constexpr (MRT)
       good = collide_mrt<D, INC>(f, mrt.K);
     else
-      good = collide_bgk<D, INC>(f, args.inv_tau);
+      good = collide_bgk<D, INC>(f, static_cast<R>(args.inv_tau));
   } else {
     good = apply_boundary<D, INC>(f, type, (info >> 26) & 1u, args.bc);
   }
@@ -178,26 +187,27 @@ __global__ void __launch_bounds__(kThreads)
 // the per-direction source address is pure integer arithmetic on compile-time lattice constants
 // plus one shared-memory lookup and two selects — no divergent branches, no dependent global load
 // before the PDF gather.
-template <int D, int LOGA, bool INC, bool PEER, bool MRT>
+template <int D, int LOGA, bool INC, bool PEER, bool MRT, class R>
 __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2))
-    t2c_step_pow2_kernel(StepArgs args, const __grid_constant__ MrtMatrix<MRT ? Lat<D>::Q : 1> mrt) {
+    t2c_step_pow2_kernel(StepArgs args, const __grid_constant__ MrtMatrix<R, MRT ? Lat<D>::Q : 1> mrt) {
   constexpr int Q = Lat<D>::Q;
+  const R* const rd = static_cast<const R*>(args.read);
   constexpr int A = 1 << LOGA;
   constexpr int NTN = D == 3 ? A * A * A : A * A;
   constexpr int TILES = kThreads / NTN;
   constexpr uint64_t STRIDE = static_cast<uint64_t>(Q) * NTN;
   constexpr int NBS = nb_stride<D>();
-  __shared__ const double* s_base[TILES][NBS];
+  __shared__ const R* s_base[TILES][NBS];
 
   const uint64_t n_tiles = args.n_nodes / NTN;
   const uint64_t tile_blk = static_cast<uint64_t>(blockIdx.x) * TILES;
   for (int k = threadIdx.x; k < TILES * NBS; k += kThreads) {
     const int tl = k / NBS, dd = k % NBS;
     const uint64_t tt = tile_blk + tl;
-    const double* b = nullptr;
+    const R* b = nullptr;
     if (tt < n_tiles) {
       const uint32_t s = __ldg(args.nb + (args.t0 + tt + (tt >= args.skip_at ? args.skip_by : 0)) * NBS + dd);
-      b = s == kEmpty ? nullptr : args.read + static_cast<uint64_t>(s) * STRIDE;
+      b = s == kEmpty ? nullptr : rd + static_cast<uint64_t>(s) * STRIDE;
     }
     s_base[tl][dd] = b;
   }
@@ -215,24 +225,24 @@ __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SP
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
-  l2_prefetch_blocks<Q, NTN, TILES>(args.read, args.t0 + pf + (pf >= args.skip_at ? args.skip_by : 0),
+  l2_prefetch_blocks<Q, NTN, TILES>(rd, args.t0 + pf + (pf >= args.skip_at ? args.skip_by : 0),
                                     args.l2pf && pf < n_tiles);
   const int type = (info >> 24) & 3;
-  double* wr = args.write + t * STRIDE + p;
+  R* wr = static_cast<R*>(args.write) + t * STRIDE + p;
   if (type == 0) {
     if (info & (1u << 27)) {
 #pragma unroll
-      for (int i = 0; i < Q; ++i) st_stream(wr + i * NTN, 0.0);
+      for (int i = 0; i < Q; ++i) st_stream(wr + i * NTN, R(0));
     }
     return;
   }
   const int lx = p & (A - 1);
   const int ly = (p >> LOGA) & (A - 1);
   const int lz = D == 3 ? (p >> (2 * LOGA)) : 0;
-  const double* own = args.read + t * STRIDE;
-  const double* const* nbp = s_base[tl];
+  const R* own = rd + t * STRIDE;
+  const R* const* nbp = s_base[tl];
 
-  double f[Q];
+  R f[Q];
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
     const int vx = lx - ex<D>(i), vy = ly - ey<D>(i), vz = lz - ez<D>(i);
@@ -241,8 +251,8 @@ __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SP
     const int dz = (D == 3 && ez<D>(i)) ? (vz >> LOGA) : 0;
     const int sp = (vx & (A - 1)) | ((vy & (A - 1)) << LOGA) | (D == 3 ? ((vz & (A - 1)) << (2 * LOGA)) : 0);
     const int delta = 13 + dx + 3 * dy + 9 * dz;
-    const double* src = (delta == 13 ? own : nbp[delta - nb_offset<D>()]) + (i * NTN + sp);
-    const double* bb = own + (opp(i) * NTN + p);  // half-way bounce-back (engine.hpp:498-500)
+    const R* src = (delta == 13 ? own : nbp[delta - nb_offset<D>()]) + (i * NTN + sp);
+    const R* bb = own + (opp(i) * NTN + p);  // half-way bounce-back (engine.hpp:498-500)
     f[i] = __ldg(((info >> i) & 1u) ? bb : src);
   }
 
@@ -251,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SP
     if constexpr (MRT)
       good = collide_mrt<D, INC>(f, mrt.K);
     else
-      good = collide_bgk<D, INC>(f, args.inv_tau);
+      good = collide_bgk<D, INC>(f, static_cast<R>(args.inv_tau));
   } else {
     good = apply_boundary<D, INC>(f, type, (info >> 26) & 1u, args.bc);
   }
@@ -261,7 +271,8 @@ __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SP
 
   // Slab faces straight into the neighbours' halo tiles over NVLink (fused with the step): the
   // neighbour gathers exactly these slots (layer a-1 / 0, directions crossing the face).
-  if constexpr (!PEER) return;
+  if constexpr (!PEER || !std::is_same<R, double>::value) return;
+  else {
   const int lslab = D == 3 ? lz : ly;
   if (args.peer_up && t >= args.top_begin && lslab == A - 1) {
     double* dst = args.peer_up + (t - args.top_begin) * STRIDE + p;
@@ -275,6 +286,7 @@ __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SP
     for (int i = 0; i < Q; ++i)
       if ((D == 3 ? ez<D>(i) : ey<D>(i)) < 0) dst[i * NTN] = f[i];
   }
+  }
 }
 
 // Single-copy propagation (the AA access pattern on the reference's tile layout). One
@@ -285,25 +297,25 @@ __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SP
 //   PHASE 2 (swapped state):  f_i = own[opp(i)];  collide; own[i] = f*_i       -> natural state
 // Each node reads and writes exactly the slots of its own set, so the in-place update is race
 // free; phase 2 touches only the node's own slots (no neighbour tables, no cross-tile reads).
-template <int D, int LOGA, bool INC, bool MRT, int PHASE>
+template <int D, int LOGA, bool INC, bool MRT, int PHASE, class R>
 __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2))
-    t2c_aa_kernel(StepArgs args, const __grid_constant__ MrtMatrix<MRT ? Lat<D>::Q : 1> mrt) {
+    t2c_aa_kernel(StepArgs args, const __grid_constant__ MrtMatrix<R, MRT ? Lat<D>::Q : 1> mrt) {
   constexpr int Q = Lat<D>::Q;
   constexpr int A = 1 << LOGA;
   constexpr int NTN = D == 3 ? A * A * A : A * A;
   constexpr int TILES = kThreads / NTN;
   constexpr uint64_t STRIDE = static_cast<uint64_t>(Q) * NTN;
   constexpr int NBS = nb_stride<D>();
-  __shared__ double* s_base[PHASE == 1 ? TILES : 1][NBS];
+  __shared__ R* s_base[PHASE == 1 ? TILES : 1][NBS];
 
-  double* const pdf = args.write;
+  R* const pdf = static_cast<R*>(args.write);
   const uint64_t n_tiles = args.n_nodes / NTN;
   const uint64_t tile_blk = static_cast<uint64_t>(blockIdx.x) * TILES;
   if constexpr (PHASE == 1) {
     for (int k = threadIdx.x; k < TILES * NBS; k += kThreads) {
       const int tl = k / NBS, dd = k % NBS;
       const uint64_t tt = tile_blk + tl;
-      double* b = nullptr;
+      R* b = nullptr;
       if (tt < n_tiles) {
         const uint32_t s = __ldg(args.nb + (args.t0 + tt) * NBS + dd);
         b = s == kEmpty ? nullptr : pdf + static_cast<uint64_t>(s) * STRIDE;
@@ -326,31 +338,31 @@ __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SP
     l2_prefetch_blocks<Q, NTN, TILES>(pdf, args.t0 + pf, args.l2pf && pf < n_tiles);
   }
   const int type = (info >> 24) & 3;
-  double* own = pdf + t * STRIDE;
+  R* own = pdf + t * STRIDE;
   if (type == 0) {  // solid slots are never read: whole store sectors (see file header)
     if (info & (1u << 27)) {
 #pragma unroll
-      for (int i = 0; i < Q; ++i) st_stream(own + i * NTN + p, 0.0);
+      for (int i = 0; i < Q; ++i) st_stream(own + i * NTN + p, R(0));
     }
     return;
   }
   const int lx = p & (A - 1);
   const int ly = (p >> LOGA) & (A - 1);
   const int lz = D == 3 ? (p >> (2 * LOGA)) : 0;
-  double* const* nbp = s_base[PHASE == 1 ? tl : 0];
-  auto addr = [&](int i) -> double* {  // PHASE 1 only
+  R* const* nbp = s_base[PHASE == 1 ? tl : 0];
+  auto addr = [&](int i) -> R* {  // PHASE 1 only
     const int vx = lx - ex<D>(i), vy = ly - ey<D>(i), vz = lz - ez<D>(i);
     const int dx = ex<D>(i) ? (vx >> LOGA) : 0;
     const int dy = ey<D>(i) ? (vy >> LOGA) : 0;
     const int dz = (D == 3 && ez<D>(i)) ? (vz >> LOGA) : 0;
     const int sp = (vx & (A - 1)) | ((vy & (A - 1)) << LOGA) | (D == 3 ? ((vz & (A - 1)) << (2 * LOGA)) : 0);
     const int delta = 13 + dx + 3 * dy + 9 * dz;
-    double* src = (delta == 13 ? own : nbp[delta - nb_offset<D>()]) + (i * NTN + sp);
-    double* bb = own + (opp(i) * NTN + p);
+    R* src = (delta == 13 ? own : nbp[delta - nb_offset<D>()]) + (i * NTN + sp);
+    R* bb = own + (opp(i) * NTN + p);
     return ((info >> i) & 1u) ? bb : src;
   };
 
-  double f[Q];
+  R f[Q];
 #pragma unroll
   for (int i = 0; i < Q; ++i) f[i] = __ldg(PHASE == 1 ? addr(i) : own + (opp(i) * NTN + p));
 
@@ -359,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SP
     if constexpr (MRT)
       good = collide_mrt<D, INC>(f, mrt.K);
     else
-      good = collide_bgk<D, INC>(f, args.inv_tau);
+      good = collide_bgk<D, INC>(f, static_cast<R>(args.inv_tau));
   } else {
     good = apply_boundary<D, INC>(f, type, (info >> 26) & 1u, args.bc);
   }
@@ -388,9 +400,13 @@ __global__ void node_info_kernel(NodeInfoArgs args) {
   uint32_t info = static_cast<uint32_t>(type) << 24;
   if (own_byte & 4) info |= 1u << 26;
   if (type == 0) {
-    if (SPLBM_ZERO_FILL && (n_tn & 3) == 0) {
-      const uint8_t* grp = args.types + (node & ~static_cast<uint64_t>(3));
-      if ((grp[0] | grp[1] | grp[2] | grp[3]) & 3) info |= 1u << 27;
+    // the 32-B store sector holds `sector` consecutive slots (4 doubles / 8 floats)
+    const int g = args.sector;
+    if (SPLBM_ZERO_FILL && n_tn % g == 0) {
+      const uint8_t* grp = args.types + (node - node % g);
+      uint8_t any = 0;
+      for (int k = 0; k < g; ++k) any |= grp[k];
+      if (any & 3) info |= 1u << 27;
     }
     args.info[node] = info;
     return;
@@ -420,8 +436,9 @@ __global__ void node_info_kernel(NodeInfoArgs args) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// TileEngineT2C::initialize (engine.hpp:336-352): equilibrium of per-node (rho, u) into both copies.
-template <int D, bool INC>
+// TileEngineT2C::initialize (engine.hpp:336-352): equilibrium<T>(T(rho), u.cast<T>()) of per-node
+// (rho, u) into both copies (one in single-copy mode).
+template <int D, bool INC, class R>
 __global__ void init_kernel(InitArgs args) {
   constexpr int Q = Lat<D>::Q;
   const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -441,20 +458,24 @@ __global__ void init_kernel(InitArgs args) {
     u1 = args.u0[1];
     u2 = args.u0[2];
   }
-  if (!INC && !(rho > 0.0)) atomicOr(args.domain_error, 1);  // lattice.hpp:76-78
-  double f[Q];
-  equilibrium<D, INC>(rho, u0, u1, u2, f);
+  const R r = static_cast<R>(rho);
+  if (!INC && !(r > R(0))) atomicOr(args.domain_error, 1);  // lattice.hpp:76-78
+  R f[Q];
+  equilibrium<D, INC>(r, static_cast<R>(u0), static_cast<R>(u1), static_cast<R>(u2), f);
   const uint64_t base = t * static_cast<uint64_t>(Q) * args.n_tn + p;
+  R* p0 = static_cast<R*>(args.pdf0);
+  R* p1 = static_cast<R*>(args.pdf1);
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
-    args.pdf0[base + static_cast<uint64_t>(i) * args.n_tn] = f[i];
-    if (args.pdf1) args.pdf1[base + static_cast<uint64_t>(i) * args.n_tn] = f[i];
+    p0[base + static_cast<uint64_t>(i) * args.n_tn] = f[i];
+    if (p1) p1[base + static_cast<uint64_t>(i) * args.n_tn] = f[i];
   }
 }
 
 // ---------------------------------------------------------------------------------------------
-// moments<T> per stored tile node (lattice.hpp:94-112), tile-node order; solid nodes -> 0.
-template <int D, bool INC>
+// moments<T> per stored tile node (lattice.hpp:94-112), tile-node order; solid nodes -> 0; the
+// FieldData doubles are static_cast<double>(m) (engine.hpp:383-386).
+template <int D, bool INC, class R>
 __global__ void moments_kernel(MomentsArgs args) {
   constexpr int Q = Lat<D>::Q;
   const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -463,31 +484,32 @@ __global__ void moments_kernel(MomentsArgs args) {
   const uint64_t t = node / args.n_tn;
   const int p = static_cast<int>(node % args.n_tn);
   const int type = (args.info[node] >> 24) & 3;
-  double r = 0.0, m0 = 0.0, m1 = 0.0, m2 = 0.0;
+  R r = R(0), m0 = R(0), m1 = R(0), m2 = R(0);
   if (type != 0) {
-    double f[Q];
-    load_state<D>(args.pdf, args.info[node], args.view, args.n_tn, t, p, f);
+    R f[Q];
+    load_state<D>(static_cast<const R*>(args.pdf), args.info[node], args.view, args.n_tn, t, p, f);
     r = density<D>(f);
     m0 = momentum<D, 0>(f);
     m1 = momentum<D, 1>(f);
     m2 = momentum<D, 2>(f);
     if (!INC) {
-      if (r == 0.0) {
+      if (r == R(0)) {
         atomicOr(args.domain_error, 1);  // lattice.hpp:105-108
       } else {
         divide3(m0, m1, m2, r);
       }
     }
   }
-  args.rho[k] = r;
-  args.ux[k] = m0;
-  args.uy[k] = m1;
-  args.uz[k] = m2;
+  args.rho[k] = static_cast<double>(r);
+  args.ux[k] = static_cast<double>(m0);
+  args.uy[k] = static_cast<double>(m1);
+  args.uz[k] = static_cast<double>(m2);
 }
 
 // ---------------------------------------------------------------------------------------------
 // Deterministic reduction over owned non-solid nodes: fixed per-block tree, then one block.
-template <int D, bool INC>
+// Moments in the engine's type, accumulated in double.
+template <int D, bool INC, class R>
 __global__ void __launch_bounds__(kThreads) reduce_partial_kernel(ReduceArgs args) {
   constexpr int Q = Lat<D>::Q;
   __shared__ double s_mass[kThreads];
@@ -502,16 +524,18 @@ __global__ void __launch_bounds__(kThreads) reduce_partial_kernel(ReduceArgs arg
     if (type == 0) continue;
     const uint64_t t = node / args.n_tn;
     const int p = static_cast<int>(node % args.n_tn);
-    double f[Q];
-    load_state<D>(args.pdf, args.info[node], args.view, args.n_tn, t, p, f);
-    const double r = density<D>(f);
-    double u0 = momentum<D, 0>(f), u1 = momentum<D, 1>(f), u2 = momentum<D, 2>(f);
-    if (!INC && r != 0.0) {
-      u0 = ddiv(u0, r);
-      u1 = ddiv(u1, r);
-      u2 = ddiv(u2, r);
+    R f[Q];
+    load_state<D>(static_cast<const R*>(args.pdf), args.info[node], args.view, args.n_tn, t, p, f);
+    const R rr = density<D>(f);
+    R v0 = momentum<D, 0>(f), v1 = momentum<D, 1>(f), v2 = momentum<D, 2>(f);
+    if (!INC && rr != R(0)) {
+      v0 = ddiv(v0, rr);
+      v1 = ddiv(v1, rr);
+      v2 = ddiv(v2, rr);
     }
-    const double sp = sqrt(sqnorm(u0, u1, u2));
+    const double r = static_cast<double>(rr);
+    const double sp = sqrt(sqnorm(static_cast<double>(v0), static_cast<double>(v1),
+                                  static_cast<double>(v2)));
     if (!(isfinite(r) && isfinite(sp))) {
       bad += 1.0;
     } else {
@@ -578,23 +602,23 @@ __global__ void halo_copy_kernel(HaloArgs args) {
 }
 
 // Natural-layout copy of a tile range of the current state (parity dumps of a swapped AA state).
-template <int D>
-__global__ void unswap_kernel(const double* pdf, const uint32_t* info, StateView v, int n_tn,
-                              uint64_t tile0, uint64_t n_tiles, double* out) {
+template <int D, class R>
+__global__ void unswap_kernel(const R* pdf, const uint32_t* info, StateView v, int n_tn,
+                              uint64_t tile0, uint64_t n_tiles, R* out) {
   constexpr int Q = Lat<D>::Q;
   const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n_tiles * n_tn) return;
   const uint64_t t = tile0 + k / n_tn;
   const int p = static_cast<int>(k % n_tn);
   const uint32_t w = info[t * n_tn + p];
-  double f[Q];
+  R f[Q];
   if (((w >> 24) & 3) == 0) {  // solid slots are not part of the state: copied as stored
 #pragma unroll
     for (int i = 0; i < Q; ++i) f[i] = pdf[(t * Q + i) * static_cast<uint64_t>(n_tn) + p];
   } else {
     load_state<D>(pdf, w, v, n_tn, t, p, f);
   }
-  double* o = out + (k / n_tn) * Q * n_tn + p;
+  R* o = out + (k / n_tn) * Q * n_tn + p;
 #pragma unroll
   for (int i = 0; i < Q; ++i) o[static_cast<uint64_t>(i) * n_tn] = f[i];
 }
@@ -612,10 +636,11 @@ __global__ void divide_selftest_kernel(uint64_t n, const double* m, const double
 
 // ---------------------------------------------------------------------------------------------
 // Launchers (host side of this translation unit)
-template <int Q>
-static MrtMatrix<Q> mrt_param(const double* K) {
-  MrtMatrix<Q> m;
-  for (int i = 0; i < Q * Q; ++i) m.K[i] = K[i];
+// T(kernel(i, j)): the double MRT operator rounded to the engine's type (collision.cpp:108-111)
+template <class R, int Q>
+static MrtMatrix<R, Q> mrt_param(const double* K) {
+  MrtMatrix<R, Q> m;
+  for (int i = 0; i < Q * Q; ++i) m.K[i] = static_cast<R>(K[i]);
   return m;
 }
 
@@ -641,73 +666,127 @@ static void launch_maybe_pdl(Kern kern, unsigned blocks, cudaStream_t st, const 
   kern<<<blocks, kThreads, 0, st>>>(a, m);
 }
 
-template <int D, int LOGA, bool INC, int PHASE>
+template <int D, int LOGA, bool INC, int PHASE, class R>
 static void launch_aa(const StepArgs& a, unsigned blocks, cudaStream_t st) {
   if (a.mrt_K)
-    launch_maybe_pdl(t2c_aa_kernel<D, LOGA, INC, true, PHASE>, blocks, st, a, mrt_param<Lat<D>::Q>(a.mrt_K));
+    launch_maybe_pdl(t2c_aa_kernel<D, LOGA, INC, true, PHASE, R>, blocks, st, a,
+                     mrt_param<R, Lat<D>::Q>(a.mrt_K));
   else
-    launch_maybe_pdl(t2c_aa_kernel<D, LOGA, INC, false, PHASE>, blocks, st, a, MrtMatrix<1>{});
+    launch_maybe_pdl(t2c_aa_kernel<D, LOGA, INC, false, PHASE, R>, blocks, st, a, MrtMatrix<R, 1>{});
 }
 
-template <int D, int LOGA, bool INC>
+template <int D, int LOGA, bool INC, class R>
 static void launch_pow2(const StepArgs& a, cudaStream_t st) {
   constexpr int NTN = D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA));
   constexpr int TILES = kThreads / NTN;
   const uint64_t tiles = a.n_nodes / NTN;
   const unsigned blocks = static_cast<unsigned>((tiles + TILES - 1) / TILES);
-  const MrtMatrix<1> none{};
+  const MrtMatrix<R, 1> none{};
   if (a.aa) {
-    if (a.aa == 1) launch_aa<D, LOGA, INC, 1>(a, blocks, st);
-    else launch_aa<D, LOGA, INC, 2>(a, blocks, st);
+    if (a.aa == 1) launch_aa<D, LOGA, INC, 1, R>(a, blocks, st);
+    else launch_aa<D, LOGA, INC, 2, R>(a, blocks, st);
     return;
   }
   if (a.mrt_K) {
-    t2c_step_pow2_kernel<D, LOGA, INC, false, true>
-        <<<blocks, kThreads, 0, st>>>(a, mrt_param<Lat<D>::Q>(a.mrt_K));
+    t2c_step_pow2_kernel<D, LOGA, INC, false, true, R>
+        <<<blocks, kThreads, 0, st>>>(a, mrt_param<R, Lat<D>::Q>(a.mrt_K));
     return;
   }
-  if (a.peer_up || a.peer_down) {  // slab boundary planes with NVLink peer stores
-    t2c_step_pow2_kernel<D, LOGA, INC, true, false><<<blocks, kThreads, 0, st>>>(a, none);
-    return;
+  if constexpr (std::is_same<R, double>::value) {
+    if (a.peer_up || a.peer_down) {  // slab boundary planes with NVLink peer stores
+      t2c_step_pow2_kernel<D, LOGA, INC, true, false, R><<<blocks, kThreads, 0, st>>>(a, none);
+      return;
+    }
   }
-  launch_maybe_pdl(t2c_step_pow2_kernel<D, LOGA, INC, false, false>, blocks, st, a, none);
+  launch_maybe_pdl(t2c_step_pow2_kernel<D, LOGA, INC, false, false, R>, blocks, st, a, none);
 }
 
-template <int D, int A, bool INC>
+template <int D, int A, bool INC, class R>
 static void launch_generic(const StepArgs& a, unsigned blocks, cudaStream_t st) {
   if (a.aa) return;  // the engine rejects single-copy mode for non-power-of-two tiles
   if (a.mrt_K)
-    t2c_step_kernel<D, A, INC, true><<<blocks, kThreads, 0, st>>>(a, mrt_param<Lat<D>::Q>(a.mrt_K));
+    t2c_step_kernel<D, A, INC, true, R><<<blocks, kThreads, 0, st>>>(a, mrt_param<R, Lat<D>::Q>(a.mrt_K));
   else
-    t2c_step_kernel<D, A, INC, false><<<blocks, kThreads, 0, st>>>(a, MrtMatrix<1>{});
+    t2c_step_kernel<D, A, INC, false, R><<<blocks, kThreads, 0, st>>>(a, MrtMatrix<R, 1>{});
 }
 
-template <int D, bool INC>
+template <int D, bool INC, class R>
 static cudaError_t launch_step_d(const StepArgs& a, cudaStream_t st) {
   const unsigned blocks = static_cast<unsigned>((a.n_nodes + kThreads - 1) / kThreads);
   if (blocks == 0) return cudaSuccess;
   if constexpr (D == 3) {
     switch (a.a) {
-      case 2: launch_pow2<D, 1, INC>(a, st); break;
-      case 4: launch_pow2<D, 2, INC>(a, st); break;
-      case 8: launch_generic<D, 8, INC>(a, blocks, st); break;
-      default: launch_generic<D, 0, INC>(a, blocks, st); break;
+      case 2: launch_pow2<D, 1, INC, R>(a, st); break;
+      case 4: launch_pow2<D, 2, INC, R>(a, st); break;
+      case 8: launch_generic<D, 8, INC, R>(a, blocks, st); break;
+      default: launch_generic<D, 0, INC, R>(a, blocks, st); break;
     }
   } else {
     switch (a.a) {
-      case 2: launch_pow2<D, 1, INC>(a, st); break;
-      case 4: launch_pow2<D, 2, INC>(a, st); break;
-      case 8: launch_pow2<D, 3, INC>(a, st); break;
-      case 16: launch_pow2<D, 4, INC>(a, st); break;
-      default: launch_generic<D, 0, INC>(a, blocks, st); break;
+      case 2: launch_pow2<D, 1, INC, R>(a, st); break;
+      case 4: launch_pow2<D, 2, INC, R>(a, st); break;
+      case 8: launch_pow2<D, 3, INC, R>(a, st); break;
+      case 16: launch_pow2<D, 4, INC, R>(a, st); break;
+      default: launch_generic<D, 0, INC, R>(a, blocks, st); break;
     }
   }
   return cudaGetLastError();
 }
 
-cudaError_t launch_step(int d, bool inc, const StepArgs& a, cudaStream_t st) {
-  if (d == 2) return inc ? launch_step_d<2, true>(a, st) : launch_step_d<2, false>(a, st);
-  return inc ? launch_step_d<3, true>(a, st) : launch_step_d<3, false>(a, st);
+// Dispatch on (dimension, compressibility, real type) for the per-type launchers below.
+template <template <int, bool, class> class F, class... Args>
+static cudaError_t dispatch(int d, bool inc, bool f32, Args&&... args) {
+  if (d == 2) {
+    if (f32) return inc ? F<2, true, float>::run(args...) : F<2, false, float>::run(args...);
+    return inc ? F<2, true, double>::run(args...) : F<2, false, double>::run(args...);
+  }
+  if (f32) return inc ? F<3, true, float>::run(args...) : F<3, false, float>::run(args...);
+  return inc ? F<3, true, double>::run(args...) : F<3, false, double>::run(args...);
+}
+
+template <int D, bool INC, class R>
+struct StepL {
+  static cudaError_t run(const StepArgs& a, cudaStream_t st) { return launch_step_d<D, INC, R>(a, st); }
+};
+template <int D, bool INC, class R>
+struct InitL {
+  static cudaError_t run(const InitArgs& a, cudaStream_t st) {
+    const unsigned blocks = static_cast<unsigned>((a.count + 255) / 256);
+    if (blocks) init_kernel<D, INC, R><<<blocks, 256, 0, st>>>(a);
+    return cudaGetLastError();
+  }
+};
+template <int D, bool INC, class R>
+struct MomentsL {
+  static cudaError_t run(const MomentsArgs& a, cudaStream_t st) {
+    const unsigned blocks = static_cast<unsigned>((a.count + 255) / 256);
+    if (blocks) moments_kernel<D, INC, R><<<blocks, 256, 0, st>>>(a);
+    return cudaGetLastError();
+  }
+};
+template <int D, bool INC, class R>
+struct ReduceL {
+  static cudaError_t run(const ReduceArgs& a, int blocks, double* out, cudaStream_t st) {
+    reduce_partial_kernel<D, INC, R><<<blocks, kThreads, 0, st>>>(a);
+    reduce_final_kernel<<<1, 32, 0, st>>>(a.partial, blocks, out);
+    return cudaGetLastError();
+  }
+};
+template <int D, bool INC, class R>
+struct UnswapL {
+  static cudaError_t run(const void* pdf, const uint32_t* info, StateView v, int n_tn,
+                         uint64_t tile0, uint64_t n_tiles, void* out, cudaStream_t st) {
+    const uint64_t n = n_tiles * n_tn;
+    const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
+    if (blocks)
+      unswap_kernel<D, R><<<blocks, 256, 0, st>>>(static_cast<const R*>(pdf), info, v, n_tn, tile0,
+                                                  n_tiles, static_cast<R*>(out));
+    return cudaGetLastError();
+  }
+};
+
+cudaError_t launch_step(int d, bool inc, bool f32, const StepArgs& a, cudaStream_t st) {
+  return dispatch<StepL>(d, inc, f32, a, st);
 }
 
 cudaError_t launch_bump(long long* step_base, long long by, cudaStream_t st) {
@@ -727,55 +806,22 @@ cudaError_t launch_node_info(int d, const NodeInfoArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_init(int d, bool inc, const InitArgs& a, cudaStream_t st) {
-  const unsigned blocks = static_cast<unsigned>((a.count + 255) / 256);
-  if (blocks == 0) return cudaSuccess;
-  if (d == 2) {
-    if (inc) init_kernel<2, true><<<blocks, 256, 0, st>>>(a);
-    else init_kernel<2, false><<<blocks, 256, 0, st>>>(a);
-  } else {
-    if (inc) init_kernel<3, true><<<blocks, 256, 0, st>>>(a);
-    else init_kernel<3, false><<<blocks, 256, 0, st>>>(a);
-  }
-  return cudaGetLastError();
+cudaError_t launch_init(int d, bool inc, bool f32, const InitArgs& a, cudaStream_t st) {
+  return dispatch<InitL>(d, inc, f32, a, st);
 }
 
-cudaError_t launch_moments(int d, bool inc, const MomentsArgs& a, cudaStream_t st) {
-  const unsigned blocks = static_cast<unsigned>((a.count + 255) / 256);
-  if (blocks == 0) return cudaSuccess;
-  if (d == 2) {
-    if (inc) moments_kernel<2, true><<<blocks, 256, 0, st>>>(a);
-    else moments_kernel<2, false><<<blocks, 256, 0, st>>>(a);
-  } else {
-    if (inc) moments_kernel<3, true><<<blocks, 256, 0, st>>>(a);
-    else moments_kernel<3, false><<<blocks, 256, 0, st>>>(a);
-  }
-  return cudaGetLastError();
+cudaError_t launch_moments(int d, bool inc, bool f32, const MomentsArgs& a, cudaStream_t st) {
+  return dispatch<MomentsL>(d, inc, f32, a, st);
 }
 
-cudaError_t launch_reduce(int d, bool inc, const ReduceArgs& a, int blocks, double* out,
+cudaError_t launch_reduce(int d, bool inc, bool f32, const ReduceArgs& a, int blocks, double* out,
                           cudaStream_t st) {
-  if (d == 2) {
-    if (inc) reduce_partial_kernel<2, true><<<blocks, kThreads, 0, st>>>(a);
-    else reduce_partial_kernel<2, false><<<blocks, kThreads, 0, st>>>(a);
-  } else {
-    if (inc) reduce_partial_kernel<3, true><<<blocks, kThreads, 0, st>>>(a);
-    else reduce_partial_kernel<3, false><<<blocks, kThreads, 0, st>>>(a);
-  }
-  reduce_final_kernel<<<1, 32, 0, st>>>(a.partial, blocks, out);
-  return cudaGetLastError();
+  return dispatch<ReduceL>(d, inc, f32, a, blocks, out, st);
 }
 
-cudaError_t launch_unswap(int d, const double* pdf, const uint32_t* info, StateView v, int n_tn,
-                          uint64_t tile0, uint64_t n_tiles, double* out, cudaStream_t st) {
-  const uint64_t n = n_tiles * n_tn;
-  const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
-  if (blocks == 0) return cudaSuccess;
-  if (d == 2)
-    unswap_kernel<2><<<blocks, 256, 0, st>>>(pdf, info, v, n_tn, tile0, n_tiles, out);
-  else
-    unswap_kernel<3><<<blocks, 256, 0, st>>>(pdf, info, v, n_tn, tile0, n_tiles, out);
-  return cudaGetLastError();
+cudaError_t launch_unswap(int d, bool f32, const void* pdf, const uint32_t* info, StateView v,
+                          int n_tn, uint64_t tile0, uint64_t n_tiles, void* out, cudaStream_t st) {
+  return dispatch<UnswapL>(d, false, f32, pdf, info, v, n_tn, tile0, n_tiles, out, st);
 }
 
 cudaError_t launch_divide_selftest(uint64_t n, const double* m, const double* rho, double* out,

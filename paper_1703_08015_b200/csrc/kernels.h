@@ -8,9 +8,11 @@
 
 namespace splbm_dev {
 
+// PDF arrays are `void*` here: the engine's real type (double for TileEngineT2C<double>, float
+// for TileEngineT2C<float>) selects the kernel instantiation (launch_* `f32`).
 struct StepArgs {
-  const double* read;
-  double* write;
+  const void* read;
+  void* write;
   const uint32_t* info;  // per stored tile node gather word
   const uint32_t* nb;    // stored tiles x 27 (3D) / 9 (2D, dz = 0 slice), local indices
   uint64_t t0;           // first stepped tile (stored index)
@@ -18,8 +20,9 @@ struct StepArgs {
   uint64_t skip_at;      // stepped-tile ordinal from which `skip_by` tiles are jumped (two ranges
   uint64_t skip_by;      // in one launch: a slab's bottom and top planes); skip_by = 0 = one range
   int a;
-  double inv_tau;
-  const double* mrt_K;  // MRT operator (q x q, HOST memory, copied into the launch); nullptr = BGK
+  double inv_tau;  // T(1.0 / tau) (collision.cpp:93), exact in double for either T
+  const double* mrt_K;  // MRT operator (q x q, HOST memory, rounded to T and copied into the
+                        // launch); nullptr = BGK
   BcParams bc;
   unsigned long long* failed;  // min failing step number (ULLONG_MAX = none)
   const long long* step_base;  // steps completed before this batch
@@ -41,9 +44,9 @@ struct StepArgs {
 
 // The MRT operator as a kernel parameter (constant bank): the unrolled K_ij * delta_j products
 // read it as immediate constant operands instead of 361 loads per node.
-template <int Q>
+template <class R, int Q>
 struct MrtMatrix {
-  double K[Q * Q];
+  R K[Q * Q];
 };
 
 struct NodeInfoArgs {
@@ -52,11 +55,12 @@ struct NodeInfoArgs {
   uint32_t* info;
   uint64_t n_stored;
   int a;
+  int sector;  // PDF slots per 32-B sector (4 doubles, 8 floats): the zero-fill group
 };
 
 struct InitArgs {
-  double* pdf0;
-  double* pdf1;
+  void* pdf0;
+  void* pdf1;
   const double* rho;  // nullptr -> uniform (rho0, u0)
   const double* ux;
   const double* uy;
@@ -78,7 +82,7 @@ struct StateView {
 };
 
 struct MomentsArgs {
-  const double* pdf;
+  const void* pdf;
   const uint32_t* info;
   StateView view;
   double* rho;
@@ -91,7 +95,7 @@ struct MomentsArgs {
 };
 
 struct ReduceArgs {
-  const double* pdf;
+  const void* pdf;
   const uint32_t* info;
   StateView view;
   uint64_t node0, n_nodes;
@@ -110,17 +114,17 @@ struct HaloArgs {
   int pack;         // 1: pdf -> buf, 0: buf -> pdf
 };
 
-cudaError_t launch_step(int d, bool inc, const StepArgs& a, cudaStream_t st);
+cudaError_t launch_step(int d, bool inc, bool f32, const StepArgs& a, cudaStream_t st);
 cudaError_t launch_bump(long long* step_base, long long by, cudaStream_t st);
 cudaError_t launch_node_info(int d, const NodeInfoArgs& a, cudaStream_t st);
-cudaError_t launch_init(int d, bool inc, const InitArgs& a, cudaStream_t st);
-cudaError_t launch_moments(int d, bool inc, const MomentsArgs& a, cudaStream_t st);
-cudaError_t launch_reduce(int d, bool inc, const ReduceArgs& a, int blocks, double* out,
+cudaError_t launch_init(int d, bool inc, bool f32, const InitArgs& a, cudaStream_t st);
+cudaError_t launch_moments(int d, bool inc, bool f32, const MomentsArgs& a, cudaStream_t st);
+cudaError_t launch_reduce(int d, bool inc, bool f32, const ReduceArgs& a, int blocks, double* out,
                           cudaStream_t st);
 cudaError_t launch_halo(int d, const HaloArgs& a, cudaStream_t st);
 // Natural-layout copy of tiles [tile0, tile0 + n_tiles) of a (possibly swapped) state into out.
-cudaError_t launch_unswap(int d, const double* pdf, const uint32_t* info, StateView v, int n_tn,
-                          uint64_t tile0, uint64_t n_tiles, double* out, cudaStream_t st);
+cudaError_t launch_unswap(int d, bool f32, const void* pdf, const uint32_t* info, StateView v,
+                          int n_tn, uint64_t tile0, uint64_t n_tiles, void* out, cudaStream_t st);
 cudaError_t launch_divide_selftest(uint64_t n, const double* m, const double* rho, double* out,
                                    cudaStream_t st);
 

@@ -5,9 +5,10 @@
 // per direction so every lookup folds to an immediate in the unrolled loops.
 //
 // Arithmetic contract: every floating-point operation is an explicit
-// round-to-nearest intrinsic (__dadd_rn/__dmul_rn/__ddiv_rn) in the reference's operation order,
-// so nvcc cannot contract to FMA and results are bit-identical to the reference built with its
-// CMake Release flags. Products by a zero direction component are omitted: x + (+-0) == x for
+// round-to-nearest intrinsic (__dadd_rn/__dmul_rn/__ddiv_rn, __fadd_rn/... for the f32 engine) in
+// the reference's operation order, all in the engine's real type R (the reference's T: double or
+// float, lattice.hpp:72-112), so nvcc cannot contract to FMA and results are bit-identical to the
+// reference built with its CMake Release flags. Products by a zero direction component are omitted: x + (+-0) == x for
 // x != 0 and a zero sum starts from +0, so the omitted terms never change a finite result (the
 // only difference is on states that already fail the step's finite check).
 #pragma once
@@ -68,11 +69,18 @@ __host__ __device__ constexpr int ez(int i) {
 // opposite pairs are adjacent (lattice.cpp:65-74 finds exactly this)
 __host__ __device__ constexpr int opp(int i) { return i == 0 ? 0 : ((i & 1) ? i + 1 : i - 1); }
 
+// Round-to-nearest arithmetic in the engine's real type (overloads; never mix with a double
+// literal — every constant below is R(...), as the reference writes T(...)).
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float dadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float dsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float dmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float ddiv(float a, float b) { return __fdiv_rn(a, b); }
 __device__ __forceinline__ bool finite(double v) { return isfinite(v); }
+__device__ __forceinline__ bool finite(float v) { return isfinite(v); }
 
 #ifndef SPLBM_FAST_DIV
 #define SPLBM_FAST_DIV 1
@@ -110,11 +118,17 @@ __device__ __forceinline__ void divide3(double& m0, double& m1, double& m2, doub
   m1 = ddiv(m1, rho);
   m2 = ddiv(m2, rho);
 }
+// f32 engine: IEEE single division per component (__fdiv_rn)
+__device__ __forceinline__ void divide3(float& m0, float& m1, float& m2, float rho) {
+  m0 = ddiv(m0, rho);
+  m1 = ddiv(m1, rho);
+  m2 = ddiv(m2, rho);
+}
 
 // sum_i e_ik * f_i in direction order, zero components omitted (moments<T>, lattice.hpp:97-102)
-template <int D, int K>
-__device__ __forceinline__ double momentum(const double* f) {
-  double m = 0.0;
+template <int D, int K, class R>
+__device__ __forceinline__ R momentum(const R* f) {
+  R m = R(0);
 #pragma unroll
   for (int i = 0; i < Lat<D>::Q; ++i) {
     const int e = K == 0 ? ex<D>(i) : (K == 1 ? ey<D>(i) : ez<D>(i));
@@ -124,78 +138,82 @@ __device__ __forceinline__ double momentum(const double* f) {
   return m;
 }
 
-template <int D>
-__device__ __forceinline__ double density(const double* f) {
-  double r = 0.0;
+template <int D, class R>
+__device__ __forceinline__ R density(const R* f) {
+  R r = R(0);
 #pragma unroll
   for (int i = 0; i < Lat<D>::Q; ++i) r = dadd(r, f[i]);
   return r;
 }
 
 // e_i . u in the order (e0 u0 + e1 u1) + e2 u2 with zero terms omitted (lattice.hpp:82)
-template <int D>
-__device__ __forceinline__ double edotu(int i, double u0, double u1, double u2) {
+template <int D, class R>
+__device__ __forceinline__ R edotu(int i, R u0, R u1, R u2) {
   const int a = ex<D>(i), b = ey<D>(i), c = ez<D>(i);
-  double cu = 0.0;
+  R cu = R(0);
   bool first = true;
   if (a != 0) {
     cu = a > 0 ? u0 : -u0;
     first = false;
   }
   if (b != 0) {
-    const double t = b > 0 ? u1 : -u1;
+    const R t = b > 0 ? u1 : -u1;
     cu = first ? t : dadd(cu, t);
     first = false;
   }
   if (c != 0) {
-    const double t = c > 0 ? u2 : -u2;
+    const R t = c > 0 ? u2 : -u2;
     cu = first ? t : dadd(cu, t);
   }
   return cu;
 }
 
+// T(lat.w[i]): the double weight rounded to the engine's type (lattice.hpp:86-88)
+template <int D, class R>
+__device__ __forceinline__ constexpr R weight(int i) {
+  return static_cast<R>(Lat<D>::w(i));
+}
+
 // equilibrium<T> (lattice.hpp:72-91); uu = (u0^2 + u1^2) + u2^2 (oracle Eigen-shim order).
-template <int D, bool INC>
-__device__ __forceinline__ double feq(int i, double rho, double u0, double u1, double u2,
-                                      double uu) {
-  const double cu = edotu<D>(i, u0, u1, u2);
-  const double shape = dsub(dadd(dmul(cu, 3.0), dmul(dmul(cu, cu), 4.5)), dmul(uu, 1.5));
-  const double w = Lat<D>::w(i);
-  return INC ? dmul(w, dadd(rho, shape)) : dmul(dmul(w, rho), dadd(1.0, shape));
+template <int D, bool INC, class R>
+__device__ __forceinline__ R feq(int i, R rho, R u0, R u1, R u2, R uu) {
+  const R cu = edotu<D>(i, u0, u1, u2);
+  const R shape = dsub(dadd(dmul(cu, R(3)), dmul(dmul(cu, cu), R(4.5))), dmul(uu, R(1.5)));
+  const R w = weight<D, R>(i);
+  return INC ? dmul(w, dadd(rho, shape)) : dmul(dmul(w, rho), dadd(R(1), shape));
 }
 
 // The equilibria of an opposite pair (i, opp(i) = i + 1, i odd) at once. Negation is exact and
 // round-to-nearest is sign-symmetric, so with cu' = -cu: cu'*3 = -(cu*3), cu'*cu' = cu*cu and
 // (-(cu*3)) + q = q - cu*3 — the pair shares e.u, cu*3 and (cu*cu)*4.5 and each value is still
 // bit-identical to feq() (the reference's per-direction formula, lattice.hpp:78-89).
-template <int D, bool INC>
-__device__ __forceinline__ void feq_pair(int i, double rho, double u0, double u1, double u2,
-                                         double uu15, double& fp, double& fm) {
-  const double cu = edotu<D>(i, u0, u1, u2);
-  const double c3 = dmul(cu, 3.0);
-  const double q = dmul(dmul(cu, cu), 4.5);
-  const double sp = dsub(dadd(c3, q), uu15);
-  const double sm = dsub(dsub(q, c3), uu15);
-  const double w = Lat<D>::w(i);
+template <int D, bool INC, class R>
+__device__ __forceinline__ void feq_pair(int i, R rho, R u0, R u1, R u2, R uu15, R& fp, R& fm) {
+  const R cu = edotu<D>(i, u0, u1, u2);
+  const R c3 = dmul(cu, R(3));
+  const R q = dmul(dmul(cu, cu), R(4.5));
+  const R sp = dsub(dadd(c3, q), uu15);
+  const R sm = dsub(dsub(q, c3), uu15);
+  const R w = weight<D, R>(i);
   if (INC) {
     fp = dmul(w, dadd(rho, sp));
     fm = dmul(w, dadd(rho, sm));
   } else {
-    const double wr = dmul(w, rho);
-    fp = dmul(wr, dadd(1.0, sp));
-    fm = dmul(wr, dadd(1.0, sm));
+    const R wr = dmul(w, rho);
+    fp = dmul(wr, dadd(R(1), sp));
+    fm = dmul(wr, dadd(R(1), sm));
   }
 }
 
-__device__ __forceinline__ double sqnorm(double u0, double u1, double u2) {
+template <class R>
+__device__ __forceinline__ R sqnorm(R u0, R u1, R u2) {
   return dadd(dadd(dmul(u0, u0), dmul(u1, u1)), dmul(u2, u2));
 }
 
-template <int D, bool INC>
-__device__ __forceinline__ void equilibrium(double rho, double u0, double u1, double u2,
-                                            double* out) {
-  const double uu = sqnorm(u0, u1, u2);
-  const double uu15 = dmul(uu, 1.5);
+template <int D, bool INC, class R>
+__device__ __forceinline__ void equilibrium(R rho, R u0, R u1, R u2, R* out) {
+  const R uu = sqnorm(u0, u1, u2);
+  const R uu15 = dmul(uu, R(1.5));
   out[0] = feq<D, INC>(0, rho, u0, u1, u2, uu);
 #pragma unroll
   for (int i = 1; i < Lat<D>::Q; i += 2) feq_pair<D, INC>(i, rho, u0, u1, u2, uu15, out[i], out[i + 1]);
@@ -203,23 +221,23 @@ __device__ __forceinline__ void equilibrium(double rho, double u0, double u1, do
 
 // CollisionOperator<T>::operator() BGK branch (collision.hpp:35-65). Returns
 // finite_moments(m) (engine.hpp:96-102); on a broken quasi-compressible density f is left
-// untouched and the step fails (collision.hpp:44-47).
-template <int D, bool INC>
-__device__ __forceinline__ bool collide_bgk(double* f, double inv_tau) {
-  const double rho = density<D>(f);
-  double u0 = momentum<D, 0>(f);
-  double u1 = momentum<D, 1>(f);
-  double u2 = momentum<D, 2>(f);
+// untouched and the step fails (collision.hpp:44-47). inv_tau = T(1.0 / tau) (collision.cpp:93).
+template <int D, bool INC, class R>
+__device__ __forceinline__ bool collide_bgk(R* f, R inv_tau) {
+  const R rho = density<D>(f);
+  R u0 = momentum<D, 0>(f);
+  R u1 = momentum<D, 1>(f);
+  R u2 = momentum<D, 2>(f);
   if (!INC) {
-    if (!(rho > 0.0) || !finite(rho)) return false;
+    if (!(rho > R(0)) || !finite(rho)) return false;
     divide3(u0, u1, u2, rho);
   }
-  const double uu = sqnorm(u0, u1, u2);
-  const double uu15 = dmul(uu, 1.5);
+  const R uu = sqnorm(u0, u1, u2);
+  const R uu15 = dmul(uu, R(1.5));
   f[0] = dadd(f[0], dmul(inv_tau, dsub(feq<D, INC>(0, rho, u0, u1, u2, uu), f[0])));
 #pragma unroll
   for (int i = 1; i < Lat<D>::Q; i += 2) {
-    double fp, fm;
+    R fp, fm;
     feq_pair<D, INC>(i, rho, u0, u1, u2, uu15, fp, fm);
     f[i] = dadd(f[i], dmul(inv_tau, dsub(fp, f[i])));
     f[i + 1] = dadd(f[i + 1], dmul(inv_tau, dsub(fm, f[i + 1])));
@@ -229,25 +247,26 @@ __device__ __forceinline__ bool collide_bgk(double* f, double inv_tau) {
 
 // CollisionOperator<T>::operator() MRT branch (collision.hpp:54-63): the same moments and
 // equilibrium as BGK, then f_i += sum_j K_ij (feq_j - f_j) with the q x q operator K = M^-1 S M
-// (row-major, a __grid_constant__ kernel parameter: the constants feed the DMULs directly).
-template <int D, bool INC>
-__device__ __forceinline__ bool collide_mrt(double* f, const double* K) {
+// (row-major, T(kernel(i, j)), a __grid_constant__ kernel parameter: the constants feed the
+// multiplies directly).
+template <int D, bool INC, class R>
+__device__ __forceinline__ bool collide_mrt(R* f, const R* K) {
   constexpr int Q = Lat<D>::Q;
-  const double rho = density<D>(f);
-  double u0 = momentum<D, 0>(f);
-  double u1 = momentum<D, 1>(f);
-  double u2 = momentum<D, 2>(f);
+  const R rho = density<D>(f);
+  R u0 = momentum<D, 0>(f);
+  R u1 = momentum<D, 1>(f);
+  R u2 = momentum<D, 2>(f);
   if (!INC) {
-    if (!(rho > 0.0) || !finite(rho)) return false;
+    if (!(rho > R(0)) || !finite(rho)) return false;
     divide3(u0, u1, u2, rho);
   }
-  double delta[Q];
+  R delta[Q];
   equilibrium<D, INC>(rho, u0, u1, u2, delta);
 #pragma unroll
   for (int i = 0; i < Q; ++i) delta[i] = dsub(delta[i], f[i]);
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
-    double acc = 0.0;
+    R acc = R(0);
 #pragma unroll
     for (int j = 0; j < Q; ++j) acc = dadd(acc, dmul(K[i * Q + j], delta[j]));
     f[i] = dadd(f[i], acc);
@@ -260,24 +279,26 @@ struct BcParams {
   double rho;
 };
 
-// apply_boundary<T> (engine.hpp:32-65). type 2 = VelocityBC, 3 = PressureBC.
-template <int D, bool INC>
-__device__ __forceinline__ bool apply_boundary(double* f, int type, bool rho_underdetermined,
-                                            const BcParams bc) {
+// apply_boundary<T> (engine.hpp:32-65). type 2 = VelocityBC, 3 = PressureBC. The BC velocity and
+// density are the doubles of BcParams rounded to T (bc.velocity.cast<T>(), T(bc.density)).
+template <int D, bool INC, class R>
+__device__ __forceinline__ bool apply_boundary(R* f, int type, bool rho_underdetermined,
+                                               const BcParams bc) {
   if (type == 2) {
-    double rho = 1.0;
+    R rho = R(1);
     if (!rho_underdetermined) {
       rho = density<D>(f);
-      if (!(rho > 0.0) || !finite(rho)) rho = 1.0;
+      if (!(rho > R(0)) || !finite(rho)) rho = R(1);
     }
-    equilibrium<D, INC>(rho, bc.u0, bc.u1, bc.u2, f);
-    return finite(rho) && finite(bc.u0) && finite(bc.u1) && finite(bc.u2);
+    const R b0 = static_cast<R>(bc.u0), b1 = static_cast<R>(bc.u1), b2 = static_cast<R>(bc.u2);
+    equilibrium<D, INC>(rho, b0, b1, b2, f);
+    return finite(rho) && finite(b0) && finite(b1) && finite(b2);
   }
-  const double rho = density<D>(f);
-  const double m0 = momentum<D, 0>(f), m1 = momentum<D, 1>(f), m2 = momentum<D, 2>(f);
-  double u0 = 0.0, u1 = 0.0, u2 = 0.0;
+  const R rho = density<D>(f);
+  const R m0 = momentum<D, 0>(f), m1 = momentum<D, 1>(f), m2 = momentum<D, 2>(f);
+  R u0 = R(0), u1 = R(0), u2 = R(0);
   if (!INC) {
-    if (rho > 0.0) {
+    if (rho > R(0)) {
       u0 = m0;
       u1 = m1;
       u2 = m2;
@@ -288,8 +309,9 @@ __device__ __forceinline__ bool apply_boundary(double* f, int type, bool rho_und
     u1 = m1;
     u2 = m2;
   }
-  equilibrium<D, INC>(bc.rho, u0, u1, u2, f);
-  return finite(bc.rho) && finite(u0) && finite(u1) && finite(u2);
+  const R rb = static_cast<R>(bc.rho);
+  equilibrium<D, INC>(rb, u0, u1, u2, f);
+  return finite(rb) && finite(u0) && finite(u1) && finite(u2);
 }
 
 }  // namespace splbm_dev

@@ -38,12 +38,15 @@ class TileEngineT2C:
 
     Constructor mirrors `TileEngineT2C(const Geometry&, int a, const FluidModel&, Periodicity)`
     (engine.hpp:314-315); `device` selects the GPU, `slab=(z0, z1)` the owned tile planes of
-    the multi-GPU slab mode and `single_copy=True` the in-place AA propagation
-    (one PDF array instead of two, bit-identical results).
+    the multi-GPU slab mode, `single_copy=True` the in-place AA propagation (one PDF
+    array instead of two, bit-identical results) and `precision="f32"` the
+    TileEngineT2C<float> instantiation (the reference CLI's precision=f32, tools/splbm.cpp:278).
     """
 
     def __init__(self, g: Geometry, a: int, model: FluidModel, periodic=None, device: int = 0,
-                 slab: tuple | None = None, single_copy: bool = False):
+                 slab: tuple | None = None, single_copy: bool = False, precision: str = "f64"):
+        if precision not in ("f64", "f32"):
+            raise ConfigError("precision must be f32 or f64")
         L = _native.lib()
         q = 9 if g.d == 2 else 19
         rates = None
@@ -68,6 +71,7 @@ class TileEngineT2C:
         desc.collision = int(model.collision)
         desc.mrt_rates = rates.ctypes.data_as(C.c_void_p) if rates is not None else None
         desc.single_copy = int(bool(single_copy))
+        desc.single_precision = int(precision == "f32")
         h = C.c_void_p()
         _native.check(L.splbm_dev_create(C.byref(desc), C.byref(h)))
         self._h = h
@@ -77,6 +81,8 @@ class TileEngineT2C:
         self.model = model
         self.periodic = per
         self.single_copy = bool(single_copy)
+        self.precision = precision
+        self.dtype = np.float32 if precision == "f32" else np.float64
         info = _native.DevInfo()
         _native.check(L.splbm_dev_get_info(h, C.byref(info)))
         self.info = info
@@ -220,12 +226,12 @@ class TileEngineT2C:
 
     # ---- parity / plumbing ------------------------------------------------------------------
     def get_pdf(self) -> np.ndarray:
-        out = np.empty(int(self.info.n_tiles_stored) * self.q * self.n_tn)
+        out = np.empty(int(self.info.n_tiles_stored) * self.q * self.n_tn, self.dtype)
         _native.check(self._L.splbm_dev_get_pdf(self._h, _native.ptr(out)))
         return out
 
     def set_pdf(self, f: np.ndarray) -> None:
-        f = np.ascontiguousarray(f, np.float64)
+        f = np.ascontiguousarray(f, self.dtype)
         if f.size != int(self.info.n_tiles_stored) * self.q * self.n_tn:
             raise ConfigError("PDF array has the wrong size")
         _native.check(self._L.splbm_dev_set_pdf(self._h, _native.ptr(f)))
@@ -294,6 +300,7 @@ class SimConfig:  # engine.hpp:562-576
     init: NodeInit | None = None
     snapshot_sink: SnapshotSink | None = None
     device: int = 0
+    single_copy: bool = False  # device extension: in-place AA propagation
 
     def tile_edge(self, d: int) -> int:
         return self.tile if self.tile > 0 else (16 if d == 2 else 4)
@@ -315,14 +322,17 @@ class SimulationResult:  # engine.hpp:578-591
     fields: FieldData | None = None
 
 
-def make_engine(g: Geometry, cfg: SimConfig) -> TileEngineT2C:  # engine.hpp:593-607
+def make_engine(g: Geometry, cfg: SimConfig, precision: str = "f64") -> TileEngineT2C:
+    """make_engine<T> (engine.hpp:593-607); precision "f64"/"f32" selects T = double/float."""
     if cfg.method != Method.T2C:
         raise ConfigError("the B200 path implements Method::T2C; Dense/TGB stay on the reference")
-    return TileEngineT2C(g, cfg.tile_edge(g.d), cfg.model, cfg.periodic, device=cfg.device)
+    return TileEngineT2C(g, cfg.tile_edge(g.d), cfg.model, cfg.periodic, device=cfg.device,
+                         single_copy=cfg.single_copy, precision=precision)
 
 
-def run_simulation(g: Geometry, cfg: SimConfig) -> SimulationResult:
-    """run_simulation<double> (engine.hpp:609-655) on the device engine.
+def run_simulation(g: Geometry, cfg: SimConfig, precision: str = "f64") -> SimulationResult:
+    """run_simulation<T> (engine.hpp:609-655) on the device engine; precision "f64"/"f32" is the
+    template argument T = double/float (the CLI's sim.precision, tools/splbm.cpp:278).
 
     Steps run in device batches (one batch, or one per snapshot interval); wall time is the
     device time of the batches (CUDA events on the engine stream); a failing batch raises
@@ -330,7 +340,7 @@ def run_simulation(g: Geometry, cfg: SimConfig) -> SimulationResult:
     """
     if cfg.steps < 0:
         raise ConfigError("steps must be non-negative")
-    eng = make_engine(g, cfg)
+    eng = make_engine(g, cfg, precision)
     if cfg.init is not None:
         eng.initialize(cfg.init)
     else:

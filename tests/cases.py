@@ -73,9 +73,10 @@ CASES = {
 }
 
 
-def make_oracle(O, g, a, tau, inc, per):
+def make_oracle(O, g, a, tau, inc, per, precision="f64", mrt=False):
     return O.OracleT2C(g.types, g.d, g.dims, a, tau, incompressible=inc, periodic=per,
-                       bc_velocity=g.bc.velocity, bc_density=g.bc.density, threads=4)
+                       bc_velocity=g.bc.velocity, bc_density=g.bc.density, threads=4,
+                       precision=precision, mrt=mrt)
 
 
 def init_both(O, oe, de, init):

@@ -23,6 +23,7 @@ FieldData run_engine(EngineT& e, int steps, const NodeInit& init) {  // test_eng
 }
 
 bool same(const FieldData& a, const FieldData& b) {
+  if (a.rho.size() != b.rho.size()) return false;
   return a.mask == b.mask && std::memcmp(a.rho.data(), b.rho.data(), a.rho.size() * 8) == 0 &&
          std::memcmp(a.ux.data(), b.ux.data(), a.ux.size() * 8) == 0 &&
          std::memcmp(a.uy.data(), b.uy.data(), a.uy.size() * 8) == 0 &&
@@ -31,10 +32,11 @@ bool same(const FieldData& a, const FieldData& b) {
 
 int failures = 0;
 
+template <class T = double>
 void check_case(const char* name, const Geometry& g, int a, const FluidModel& m, Periodicity per,
-                const NodeInit& init, int steps) {
-  TileEngineT2C<double> ref(g, a, m, per);
-  TileEngineT2CDevice dev(g, a, m, per);
+                const NodeInit& init, int steps, bool single_copy = false) {
+  TileEngineT2C<T> ref(g, a, m, per);
+  TileEngineT2CDeviceT<T> dev(g, a, m, per, nullptr, 0, single_copy);
   const FieldData fr = run_engine(ref, steps, init);
   const FieldData fd = run_engine(dev, steps, init);
   const bool ok = same(fr, fd) && linf_rel_diff(fr, fd) == 0.0 &&
@@ -70,6 +72,33 @@ int main() {
                splbm::testing::wavy_init, 50);
     check_case("ras 24^3 periodic wavy incompressible", generate(GeometryKind::Ras3D, p), 4, mi,
                per, splbm::testing::wavy_init, 50);
+    check_case("ras 24^3 periodic wavy, single copy (odd steps)", generate(GeometryKind::Ras3D, p),
+               4, m, per, splbm::testing::wavy_init, 51, true);
+    // TileEngineT2C<float> (the reference's precision=f32): float PDFs and arithmetic
+    check_case<float>("f32 ras 24^3 periodic wavy", generate(GeometryKind::Ras3D, p), 4, m, per,
+                      splbm::testing::wavy_init, 50);
+    check_case<float>("f32 ras 24^3 periodic wavy incompressible, single copy",
+                      generate(GeometryKind::Ras3D, p), 4, mi, per, splbm::testing::wavy_init, 31,
+                      true);
+    FluidModel mm = m;
+    mm.collision = CollisionKind::MRT;
+    check_case<float>("f32 MRT ras 24^3 periodic wavy", generate(GeometryKind::Ras3D, p), 4, mm, per,
+                      splbm::testing::wavy_init, 40);
+    check_case("MRT ras 24^3 periodic wavy", generate(GeometryKind::Ras3D, p), 4, mm, per,
+               splbm::testing::wavy_init, 40);
+  }
+  {
+    GenerateParams p;
+    p.dims = {96, 48, 1};
+    p.inlet_speed = 0.04;
+    check_case<float>("f32 channel2d 96x48 a=16 (V/P boundaries)", generate(GeometryKind::Channel2D, p),
+                      16, m, {}, [](int, int, int) { return std::make_pair(1.0, Eigen::Vector3d::Zero()); },
+                      120);
+    check_case<float>("f32 cavity3d 20^3 a=4", [] {
+      GenerateParams c;
+      c.dims = {20, 20, 20};
+      return generate(GeometryKind::Cavity3D, c);
+    }(), 4, m, {}, [](int, int, int) { return std::make_pair(1.0, Eigen::Vector3d::Zero()); }, 60);
   }
   check_case("closed box 3d a=2", splbm::testing::closed_box(3, {13, 11, 9}), 2, m, {},
              splbm::testing::wavy_init, 30);

@@ -43,6 +43,40 @@ def test_oracle_matches_reference_bitwise(name, ref, oracle):
     assert re.tile_visits() == 30 * oe.T
 
 
+F32 = ["cavity2d_64_a4", "plug_channel_quasi", "plug_channel_incompr", "ras24_periodic",
+       "ras24_periodic_incompr", "random_solids_a3", "cavity3d_odd_incompr", "channel3d_32"]
+
+
+@pytest.mark.parametrize("mrt", [False, True])
+@pytest.mark.parametrize("name", F32)
+def test_oracle_f32_matches_reference_float_engine(name, mrt, ref, oracle):
+    """The float instance of the restatement (oracle/t2c_real.inc) against the reference's own
+    TileEngineT2C<float> (the CLI's precision=f32): every PDF slot and (rho, u) bit for bit."""
+    factory, a, tau, inc, per, init = CASES[name]
+    g = factory()
+    rg = ref.RefGeometry.from_raster(g.d, g.dims, g.types, g.bc.velocity, g.bc.density)
+    re = ref.RefEngine(rg, "t2c", a, tau, incompressible=inc, mrt=mrt, periodic=per, threads=2,
+                       precision="f32")
+    oe = make_oracle(oracle, g, a, tau, inc, per, precision="f32", mrt=mrt)
+    if init == "uniform":
+        re.initialize_uniform()
+        oe.initialize_uniform()
+    else:
+        re.initialize_wavy()
+        oe.initialize_wavy()
+    assert re.pdf().dtype == np.float32
+    assert np.array_equal(re.pdf().view(np.uint32), oe.current_pdf().view(np.uint32))
+    for n in (1, 9, 20):
+        ok_r, _ = re.step(n)
+        ok_o, _ = oe.step(n)
+        assert ok_r and ok_o
+        assert np.array_equal(re.pdf().view(np.uint32), oe.current_pdf().view(np.uint32))
+    fr, fo = re.fields(), oe.fields()
+    for k in ("rho", "ux", "uy", "uz", "mask"):
+        assert np.array_equal(fr[k], fo[k]), k
+    assert fr["mass"] == fo["mass"]
+
+
 def test_oracle_matches_dense_engine(ref, oracle):
     """Dense == T2C in the reference; the oracle agrees with the Dense engine too."""
     g = CASES["plug_channel_quasi"][0]()
