@@ -297,8 +297,10 @@ __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SP
 //   PHASE 2 (swapped state):  f_i = own[opp(i)];  collide; own[i] = f*_i       -> natural state
 // Each node reads and writes exactly the slots of its own set, so the in-place update is race
 // free; phase 2 touches only the node's own slots (no neighbour tables, no cross-tile reads).
+// Register budget: phase 1 keeps the 19 values live across the address recomputation of the
+// scatter; at 3 CTAs/SM (85 registers) it does not spill and measured 7 % faster than at 4.
 template <int D, int LOGA, bool INC, bool MRT, int PHASE, class R>
-__global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2))
+__global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? (PHASE == 1 ? 3 : SPLBM_MINB3) : SPLBM_MINB2))
     t2c_aa_kernel(StepArgs args, const __grid_constant__ MrtMatrix<R, MRT ? Lat<D>::Q : 1> mrt) {
   constexpr int Q = Lat<D>::Q;
   constexpr int A = 1 << LOGA;

@@ -1,6 +1,3 @@
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/ab1_test.log 2>&1; echo test=$?
-tail -2 gpurun_out/ab1_test.log
-timeout 1200 python tools/kernel_sweep.py --run > gpurun_out/ab1_sweep.log 2>&1; echo sweep=$?
-timeout 1200 python tools/kernel_sweep.py --run > gpurun_out/ab1_sweep2.log 2>&1; echo sweep=$?
-grep -v "^{" gpurun_out/ab1_sweep.log gpurun_out/ab1_sweep2.log
+timeout 1200 python tools/ab.py '{"pf0": {"SPLBM_L2PF": 0}, "pf148": {"SPLBM_L2PF": 148}, "pf296": {"SPLBM_L2PF": 296}, "pf592": {"SPLBM_L2PF": 592}}' --rounds 7 --steps 64 > gpurun_out/ab1.log 2>&1; echo ab=$?
+grep -v "^{" gpurun_out/ab1.log
