@@ -60,6 +60,31 @@ __device__ __forceinline__ void st_stream(float* p, float v) {
 #endif
 }
 
+// PDF gather load. B200 measurement (tools/gran_probe.cu): a plain or .nc global load that misses
+// fetches the whole 128-B line from DRAM; the .L2::64B prefetch-size qualifier limits that to
+// 64 B (the device limit cudaLimitMaxL2FetchGranularity has no effect). `hint`: 0 default,
+// 1 .L2::64B, 2 .L2::256B (a runtime switch for A/B timing; uniform across the grid).
+__device__ __forceinline__ double ld_pdf(const double* p, int hint) {
+  double v;
+  if (hint == 1)
+    asm volatile("ld.global.nc.L2::64B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  else if (hint == 2)
+    asm volatile("ld.global.nc.L2::256B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  else
+    v = __ldg(p);
+  return v;
+}
+__device__ __forceinline__ float ld_pdf(const float* p, int hint) {
+  float v;
+  if (hint == 1)
+    asm volatile("ld.global.nc.L2::64B.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  else if (hint == 2)
+    asm volatile("ld.global.nc.L2::256B.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  else
+    v = __ldg(p);
+  return v;
+}
+
 // L2 prefetch of a future CTA's read blocks (the CTA StepArgs::l2pf CTAs ahead, about half a
 // wave): one bulk request per tile block (Q*NTN doubles, contiguous) holds no registers, so more
 // DRAM reads are in flight than the gather alone keeps. Whole blocks measured faster than
@@ -164,7 +189,7 @@ __global__ void __launch_bounds__(kThreads)
       const uint64_t s = __ldg(nbt + delta);
       src = rd + s * tile_stride + i * n_tn + sp;
     }
-    f[i] = __ldg(src);
+    f[i] = ld_pdf(src, args.ldhint);
   }
 
   bool good;
@@ -253,7 +278,7 @@ __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SP
     const int delta = 13 + dx + 3 * dy + 9 * dz;
     const R* src = (delta == 13 ? own : nbp[delta - nb_offset<D>()]) + (i * NTN + sp);
     const R* bb = own + (opp(i) * NTN + p);  // half-way bounce-back (engine.hpp:498-500)
-    f[i] = __ldg(((info >> i) & 1u) ? bb : src);
+    f[i] = ld_pdf(((info >> i) & 1u) ? bb : src, args.ldhint);
   }
 
   bool good;
@@ -366,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? (PHASE == 1 ? 3 
 
   R f[Q];
 #pragma unroll
-  for (int i = 0; i < Q; ++i) f[i] = __ldg(PHASE == 1 ? addr(i) : own + (opp(i) * NTN + p));
+  for (int i = 0; i < Q; ++i) f[i] = ld_pdf(PHASE == 1 ? addr(i) : own + (opp(i) * NTN + p), args.ldhint);
 
   bool good;
   if (type == 1) {
