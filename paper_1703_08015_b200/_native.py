@@ -113,13 +113,19 @@ SIGNATURES = {
 def lib():
     """The loaded native library; raises if it was not built (no fallback path exists)."""
     global _lib
-    if _lib is not None:
-        return _lib
-    if not os.path.exists(LIB_PATH):
+    if _lib is None:
+        _lib = load(LIB_PATH)
+    return _lib
+
+
+def load(path: str):
+    """Loads a build of the library at `path` (an experiment build for A/B timing, or the
+    in-tree one) with every signature bound."""
+    if not os.path.exists(path):
         raise ImportError(
-            f"native library {LIB_PATH} is missing; build it with "
+            f"native library {path} is missing; build it with "
             "`python -m paper_1703_08015_b200.build` (the T2C path has no CPU fallback)")
-    L = C.CDLL(LIB_PATH)
+    L = C.CDLL(path)
     missing = []
     for name, (args, res) in SIGNATURES.items():
         if not hasattr(L, name):  # an older experiment build; tests/test_native_abi.py guards
@@ -129,7 +135,6 @@ def lib():
         fn.argtypes = args
         fn.restype = res
     L.missing_symbols = missing
-    _lib = L
     return L
 
 

@@ -2,7 +2,8 @@
 python tools/ab.py '{"name": {"ENV": "value", ...}, ...}' [case ...] [--rounds R --steps K]
 
 Every variant's engine is created with its environment settings (read at engine creation, e.g.
-SPLBM_L2PF, SPLBM_SINGLE_COPY) and all engines of a case stay resident; the K-step batches are then
+SPLBM_L2PF, SPLBM_SINGLE_COPY; "LIB": "variants/lib_x.so" selects another build of the library)
+and all engines of a case stay resident; the K-step batches are then
 alternated A, B, A, B, ... for R rounds and the median per variant is reported, so box-to-box and
 thermal drift cancel out of the comparison."""
 import json
@@ -36,15 +37,21 @@ def main():
     variants = json.loads(a.variants)
     cases = a.cases or list(CASES)
     out = {}
+    libs = {}
     for case in cases:
         g, per = CASES[case]()
         engines = {}
         for name, env in variants.items():
-            saved = {k: os.environ.get(k) for k in env}
-            os.environ.update({k: str(v) for k, v in env.items()})
+            saved = {k: os.environ.get(k) for k in env if k != "LIB"}
+            os.environ.update({k: str(v) for k, v in env.items() if k != "LIB"})
             single = os.environ.get("SPLBM_SINGLE_COPY") == "1"
             prec = os.environ.get("SPLBM_PRECISION", "f64")
+            from paper_1703_08015_b200 import _native
+            saved_lib = _native._lib
+            if "LIB" in env:  # another build of the library (e.g. variants/lib_old.so)
+                _native._lib = libs.setdefault(env["LIB"], _native.load(os.path.join(ROOT, env["LIB"])))
             e = P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8), per, single_copy=single, precision=prec)
+            _native._lib = saved_lib
             for k, v in saved.items():
                 if v is None:
                     os.environ.pop(k, None)
