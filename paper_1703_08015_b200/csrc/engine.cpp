@@ -104,7 +104,7 @@ struct splbm_dev_engine {
   std::vector<double> mrt_K;  // MRT operator (host copy; passed to the kernels by value), empty = BGK
   uint64_t device_bytes = 0;
   uint32_t l2pf = 0;  // step kernel L2 prefetch distance in CTAs (StepArgs::l2pf)
-  int ldhint = 0;     // StepArgs::ldhint (SPLBM_LDHINT overrides)
+  int ldhint = 1;     // StepArgs::ldhint: .L2::64B gather loads (SPLBM_LDHINT overrides)
   // single-copy (AA) propagation: one PDF array (pdf[0]); `read` is then the state parity
   // (0 natural layout, 1 swapped, see t2c_aa_kernel)
   bool aa = false;
@@ -470,12 +470,17 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
   if (SPLBM_L2_FETCH > 0) CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, SPLBM_L2_FETCH));
   {
     // L2 prefetch distance of the step kernel: one CTA per SM ahead in 3D (a quarter wave at 4
-    // resident CTAs per SM), two in 2D (a third of a wave at 6); interleaved A/B on a B200: +4 %
-    // over no prefetch, while a full wave ahead evicts the blocks before use (-6 %).
-    // SPLBM_L2PF overrides it (0 = off) for tuning sweeps.
+    // resident CTAs per SM), two in 2D (a third of a wave at 6). It pays while the reuse window of
+    // the gather — one tile plane along the last axis, read again by the next plane — stays well
+    // inside L2 (channel 128^3: 10 MB, +4 %; 2D: +5 %); with larger planes the prefetched blocks
+    // evict that window (RAS 256^3: 13-40 MB, -1..-3 %), so it is off there (interleaved A/B on a
+    // B200). SPLBM_L2PF overrides it (0 = off) for tuning sweeps.
     int sms = 148;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device));
-    e->l2pf = static_cast<uint32_t>(sms * (d == 3 ? 1 : 2));
+    const int last = d == 3 ? 2 : 1;
+    const double plane_bytes = static_cast<double>(e->n_own) / std::max(1, e->tm.grid_dims[last]) *
+                               static_cast<double>(e->tile_stride()) * e->es;
+    e->l2pf = plane_bytes <= 12.0e6 ? static_cast<uint32_t>(sms * (d == 3 ? 1 : 2)) : 0u;
     if (const char* v = std::getenv("SPLBM_L2PF")) e->l2pf = static_cast<uint32_t>(std::atoi(v));
     if (const char* v = std::getenv("SPLBM_LDHINT")) e->ldhint = std::atoi(v);
   }
