@@ -378,7 +378,8 @@ def run_big(args):
     peak, peak_kind = measured_peaks()
     t0 = time.time()
     g = P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(1024, 1024, 1024), sphere_diameter=40,
-                                                          target_porosity=args.phi, seed=7))
+                                                          target_porosity=args.phi, seed=7),
+                   device=0)  # the sphere loop on the GPU (same raster as the host generator)
     t_gen = time.time() - t0
     t0 = time.time()
     eng = P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8), (1, 1, 1), single_copy=args.single_copy)

@@ -63,6 +63,13 @@ typedef struct {
 int splbm_generate(int kind, const splbm_generate_params* p, uint8_t* types_out, int* d_out,
                    double bc_velocity_out[3], double* bc_density_out);
 
+/* generate() with the RAS sphere loop on a CUDA device: the same raster, bit for
+ * bit, as splbm_generate (the reference's generate_ras, geometry.cpp:251-326; candidate centres
+ * from the same mt19937_64 stream, accept/skip/retry decided on the device); the other kinds run
+ * the host generator. */
+int splbm_generate_device(int kind, const splbm_generate_params* p, int device, uint8_t* types_out,
+                          int* d_out, double bc_velocity_out[3], double* bc_density_out);
+
 /* SPLB v1 binary / text formats (geometry.cpp:49-191, 347-368). Two-call protocol for load:
  * call with types_out == NULL to get d/dims, then again with a buffer. */
 int splbm_geometry_load(const char* path, int* d_out, int dims_out[3], uint8_t* types_out,

@@ -62,6 +62,8 @@ SIGNATURES = {
     "splbm_version": ([], C.c_char_p),
     "splbm_generate": ([C.c_int, C.POINTER(GenerateParams), _u8, C.POINTER(C.c_int), _dp,
                         C.POINTER(C.c_double)], C.c_int),
+    "splbm_generate_device": ([C.c_int, C.POINTER(GenerateParams), C.c_int, _u8, C.POINTER(C.c_int),
+                               _dp, C.POINTER(C.c_double)], C.c_int),
     "splbm_geometry_load": ([C.c_char_p, C.POINTER(C.c_int), _i32, C.c_void_p, _dp,
                              C.POINTER(C.c_double)], C.c_int),
     "splbm_geometry_save": ([C.c_char_p, C.c_int, C.c_int, _i32, _u8, _dp, C.c_double], C.c_int),

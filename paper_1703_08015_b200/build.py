@@ -15,7 +15,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsplbm_b200.so")
 BUILD = os.path.join(ROOT, "build", "native")
-SOURCES = ["kernels.cu", "engine.cpp", "tiling.cpp", "geometry.cpp", "nccl_api.cpp", "mrt.cpp"]
+SOURCES = ["kernels.cu", "engine.cpp", "tiling.cpp", "geometry.cpp", "geometry_gpu.cu", "nccl_api.cpp",
+           "mrt.cpp"]
 HEADERS = ["kernels.h", "lattice.cuh", "common.h", "tiling.h", "nccl_api.h", "mrt.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -104,8 +104,9 @@ class GenerateParams:  # geometry.hpp:70-78
     seed: int = 0
 
 
-def generate(kind: GeometryKind, p: GenerateParams) -> Geometry:
-    """generate() (geometry.cpp:370-382); deterministic for a fixed seed."""
+def generate(kind: GeometryKind, p: GenerateParams, device: int | None = None) -> Geometry:
+    """generate() (geometry.cpp:370-382); deterministic for a fixed seed. `device` runs the RAS
+    sphere loop on that CUDA device (splbm_generate_device; the same raster bit for bit)."""
     L = _native.lib()
     kind = GeometryKind(kind)
     dims = [int(v) for v in (list(p.dims) + [1, 1, 1])[:3]]
@@ -120,7 +121,11 @@ def generate(kind: GeometryKind, p: GenerateParams) -> Geometry:
     d = C.c_int()
     vel = np.zeros(3)
     rho = C.c_double()
-    _native.check(L.splbm_generate(int(kind), C.byref(cp), types, C.byref(d), vel, C.byref(rho)))
+    if device is None:
+        _native.check(L.splbm_generate(int(kind), C.byref(cp), types, C.byref(d), vel, C.byref(rho)))
+    else:
+        _native.check(L.splbm_generate_device(int(kind), C.byref(cp), int(device), types,
+                                              C.byref(d), vel, C.byref(rho)))
     return Geometry(d.value, tuple(dims), types, BcParams(tuple(float(v) for v in vel), rho.value))
 
 
