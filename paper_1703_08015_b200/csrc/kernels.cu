@@ -23,6 +23,21 @@ namespace splbm_dev {
 
 constexpr uint32_t kEmpty = 0xffffffffu;
 constexpr int kThreads = 256;
+#ifndef SPLBM_STEP_THREADS
+#define SPLBM_STEP_THREADS 64  // CTA size of the 3D power-of-two step kernel
+#endif
+#ifndef SPLBM_AA_THREADS
+#define SPLBM_AA_THREADS 64  // CTA size of the single-copy (AA) kernels
+#endif
+#ifndef SPLBM_STEP_THREADS2
+#define SPLBM_STEP_THREADS2 64  // CTA size of the 2D power-of-two step kernel
+#endif
+// the CTA size of a power-of-two step: SPLBM_STEP_THREADS for 3D, 256 for 2D (whole tiles)
+// (never below one tile: a CTA owns whole tiles)
+template <int D, int NTN>
+__host__ __device__ constexpr int step_threads() {
+  return (D == 3 ? SPLBM_STEP_THREADS : SPLBM_STEP_THREADS2) > NTN ? (D == 3 ? SPLBM_STEP_THREADS : SPLBM_STEP_THREADS2) : NTN;
+}
 // Device neighbour table: the 27 cells of engine.hpp:446-463 in 3D; in 2D only the dz = 0 slice
 // (cells 9..17) is ever addressed, so it is stored compactly with 9 entries per tile.
 template <int D>
@@ -30,10 +45,10 @@ __host__ __device__ constexpr int nb_stride() { return D == 3 ? 27 : 9; }
 template <int D>
 __host__ __device__ constexpr int nb_offset() { return D == 3 ? 0 : 9; }
 #ifndef SPLBM_MINB3
-#define SPLBM_MINB3 4  // resident CTAs per SM the 3D step kernel is register-budgeted for
+#define SPLBM_MINB3 4  // resident 256-thread CTAs per SM the 3D step is budgeted for
 #endif
 #ifndef SPLBM_MINB2
-#define SPLBM_MINB2 6  // resident CTAs per SM the 2D step kernel is register-budgeted for
+#define SPLBM_MINB2 6  // resident 256-thread CTAs per SM the 2D step is budgeted for
 #endif
 #ifndef SPLBM_ZERO_FILL
 #define SPLBM_ZERO_FILL 1  // write 0.0 to solid slots sharing a 32-B sector with fluid slots
@@ -213,20 +228,20 @@ __global__ void __launch_bounds__(kThreads)
 // plus one shared-memory lookup and two selects — no divergent branches, no dependent global load
 // before the PDF gather.
 template <int D, int LOGA, bool INC, bool PEER, bool MRT, class R>
-__global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2))
+__global__ void __launch_bounds__((step_threads<D, (D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA)))>()), (MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2)) * 256 / step_threads<D, (D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA)))>())
     t2c_step_pow2_kernel(StepArgs args, const __grid_constant__ MrtMatrix<R, MRT ? Lat<D>::Q : 1> mrt) {
   constexpr int Q = Lat<D>::Q;
   const R* const rd = static_cast<const R*>(args.read);
   constexpr int A = 1 << LOGA;
   constexpr int NTN = D == 3 ? A * A * A : A * A;
-  constexpr int TILES = kThreads / NTN;
+  constexpr int TILES = step_threads<D, NTN>() / NTN;
   constexpr uint64_t STRIDE = static_cast<uint64_t>(Q) * NTN;
   constexpr int NBS = nb_stride<D>();
   __shared__ const R* s_base[TILES][NBS];
 
   const uint64_t n_tiles = args.n_nodes / NTN;
   const uint64_t tile_blk = static_cast<uint64_t>(blockIdx.x) * TILES;
-  for (int k = threadIdx.x; k < TILES * NBS; k += kThreads) {
+  for (int k = threadIdx.x; k < TILES * NBS; k += step_threads<D, NTN>()) {
     const int tl = k / NBS, dd = k % NBS;
     const uint64_t tt = tile_blk + tl;
     const R* b = nullptr;
@@ -324,13 +339,19 @@ __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SP
 // free; phase 2 touches only the node's own slots (no neighbour tables, no cross-tile reads).
 // Register budget: phase 1 keeps the 19 values live across the address recomputation of the
 // scatter; at 3 CTAs/SM (85 registers) it does not spill and measured 7 % faster than at 4.
+template <int D, int LOGA>
+__host__ __device__ constexpr int aa_threads() {
+  return SPLBM_AA_THREADS > (D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA))) ? SPLBM_AA_THREADS
+                                                                             : (D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA)));
+}
 template <int D, int LOGA, bool INC, bool MRT, int PHASE, class R>
-__global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? (PHASE == 1 ? 3 : SPLBM_MINB3) : SPLBM_MINB2))
+__global__ void __launch_bounds__(aa_threads<D, LOGA>(),
+                                  (MRT ? 2 : (D == 3 ? (PHASE == 1 ? 3 : SPLBM_MINB3) : SPLBM_MINB2)) * 256 / aa_threads<D, LOGA>())
     t2c_aa_kernel(StepArgs args, const __grid_constant__ MrtMatrix<R, MRT ? Lat<D>::Q : 1> mrt) {
   constexpr int Q = Lat<D>::Q;
   constexpr int A = 1 << LOGA;
   constexpr int NTN = D == 3 ? A * A * A : A * A;
-  constexpr int TILES = kThreads / NTN;
+  constexpr int TILES = aa_threads<D, LOGA>() / NTN;
   constexpr uint64_t STRIDE = static_cast<uint64_t>(Q) * NTN;
   constexpr int NBS = nb_stride<D>();
   __shared__ R* s_base[PHASE == 1 ? TILES : 1][NBS];
@@ -339,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, MRT ? 2 : (D == 3 ? (PHASE == 1 ? 3 
   const uint64_t n_tiles = args.n_nodes / NTN;
   const uint64_t tile_blk = static_cast<uint64_t>(blockIdx.x) * TILES;
   if constexpr (PHASE == 1) {
-    for (int k = threadIdx.x; k < TILES * NBS; k += kThreads) {
+    for (int k = threadIdx.x; k < TILES * NBS; k += aa_threads<D, LOGA>()) {
       const int tl = k / NBS, dd = k % NBS;
       const uint64_t tt = tile_blk + tl;
       R* b = nullptr;
@@ -672,14 +693,15 @@ static MrtMatrix<R, Q> mrt_param(const double* K) {
 }
 
 template <class Kern, class M>
-static void launch_maybe_pdl(Kern kern, unsigned blocks, cudaStream_t st, const StepArgs& a, const M& m) {
+static void launch_maybe_pdl(Kern kern, unsigned blocks, cudaStream_t st, const StepArgs& a, const M& m,
+                             int threads = kThreads) {
 #if SPLBM_PDL
   // Overlap the next step's launch and static-table prologue with this step's tail; below a few
   // waves (launch-latency-bound domains) the plain launch measured faster.
-  if (blocks >= 4u * 148u) {
+  if (static_cast<uint64_t>(blocks) * threads >= 4ull * 148 * 256) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(blocks);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(threads);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -690,42 +712,46 @@ static void launch_maybe_pdl(Kern kern, unsigned blocks, cudaStream_t st, const 
     return;
   }
 #endif
-  kern<<<blocks, kThreads, 0, st>>>(a, m);
+  kern<<<blocks, threads, 0, st>>>(a, m);
 }
 
 template <int D, int LOGA, bool INC, int PHASE, class R>
 static void launch_aa(const StepArgs& a, unsigned blocks, cudaStream_t st) {
   if (a.mrt_K)
     launch_maybe_pdl(t2c_aa_kernel<D, LOGA, INC, true, PHASE, R>, blocks, st, a,
-                     mrt_param<R, Lat<D>::Q>(a.mrt_K));
+                     mrt_param<R, Lat<D>::Q>(a.mrt_K), aa_threads<D, LOGA>());
   else
-    launch_maybe_pdl(t2c_aa_kernel<D, LOGA, INC, false, PHASE, R>, blocks, st, a, MrtMatrix<R, 1>{});
+    launch_maybe_pdl(t2c_aa_kernel<D, LOGA, INC, false, PHASE, R>, blocks, st, a, MrtMatrix<R, 1>{},
+                     aa_threads<D, LOGA>());
 }
 
 template <int D, int LOGA, bool INC, class R>
 static void launch_pow2(const StepArgs& a, cudaStream_t st) {
   constexpr int NTN = D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA));
-  constexpr int TILES = kThreads / NTN;
+  constexpr int TILES = step_threads<D, NTN>() / NTN;
   const uint64_t tiles = a.n_nodes / NTN;
   const unsigned blocks = static_cast<unsigned>((tiles + TILES - 1) / TILES);
   const MrtMatrix<R, 1> none{};
   if (a.aa) {
-    if (a.aa == 1) launch_aa<D, LOGA, INC, 1, R>(a, blocks, st);
-    else launch_aa<D, LOGA, INC, 2, R>(a, blocks, st);
+    constexpr int ATILES = aa_threads<D, LOGA>() / NTN;
+    const unsigned ablocks = static_cast<unsigned>((tiles + ATILES - 1) / ATILES);
+    if (a.aa == 1) launch_aa<D, LOGA, INC, 1, R>(a, ablocks, st);
+    else launch_aa<D, LOGA, INC, 2, R>(a, ablocks, st);
     return;
   }
   if (a.mrt_K) {
     t2c_step_pow2_kernel<D, LOGA, INC, false, true, R>
-        <<<blocks, kThreads, 0, st>>>(a, mrt_param<R, Lat<D>::Q>(a.mrt_K));
+        <<<blocks, step_threads<D, NTN>(), 0, st>>>(a, mrt_param<R, Lat<D>::Q>(a.mrt_K));
     return;
   }
   if constexpr (std::is_same<R, double>::value) {
     if (a.peer_up || a.peer_down) {  // slab boundary planes with NVLink peer stores
-      t2c_step_pow2_kernel<D, LOGA, INC, true, false, R><<<blocks, kThreads, 0, st>>>(a, none);
+      t2c_step_pow2_kernel<D, LOGA, INC, true, false, R><<<blocks, step_threads<D, NTN>(), 0, st>>>(a, none);
       return;
     }
   }
-  launch_maybe_pdl(t2c_step_pow2_kernel<D, LOGA, INC, false, false, R>, blocks, st, a, none);
+  launch_maybe_pdl(t2c_step_pow2_kernel<D, LOGA, INC, false, false, R>, blocks, st, a, none,
+                   step_threads<D, NTN>());
 }
 
 template <int D, int A, bool INC, class R>
