@@ -469,18 +469,13 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
   CK(cudaSetDevice(e->device));
   if (SPLBM_L2_FETCH > 0) CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, SPLBM_L2_FETCH));
   {
-    // L2 prefetch distance of the step kernel: one CTA per SM ahead in 3D (a quarter wave at 4
-    // resident CTAs per SM), two in 2D (a third of a wave at 6). It pays while the reuse window of
-    // the gather — one tile plane along the last axis, read again by the next plane — stays well
-    // inside L2 (channel 128^3: 10 MB, +4 %; 2D: +5 %); with larger planes the prefetched blocks
-    // evict that window (RAS 256^3: 13-40 MB, -1..-3 %), so it is off there (interleaved A/B on a
-    // B200). SPLBM_L2PF overrides it (0 = off) for tuning sweeps.
+    // L2 prefetch distance of the step kernel: two CTAs per SM ahead (64-thread CTAs: 296 tiles
+    // of a 4^3 3D domain). Interleaved A/B on a B200 against no prefetch: channel 128^3 +6 %,
+    // RAS 256^3 +3 %, 2D 4096^2 +8 %; four times farther ahead loses part of it again.
+    // SPLBM_L2PF overrides it (0 = off) for tuning sweeps.
     int sms = 148;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device));
-    const int last = d == 3 ? 2 : 1;
-    const double plane_bytes = static_cast<double>(e->n_own) / std::max(1, e->tm.grid_dims[last]) *
-                               static_cast<double>(e->tile_stride()) * e->es;
-    e->l2pf = plane_bytes <= 12.0e6 ? static_cast<uint32_t>(sms * (d == 3 ? 1 : 2)) : 0u;
+    e->l2pf = static_cast<uint32_t>(2 * sms);
     if (const char* v = std::getenv("SPLBM_L2PF")) e->l2pf = static_cast<uint32_t>(std::atoi(v));
     if (const char* v = std::getenv("SPLBM_LDHINT")) e->ldhint = std::atoi(v);
   }
