@@ -46,9 +46,12 @@ def main():
                  f"{r['dram_write_bytes'] / 1e6:.0f} | {r['dram_bytes_per_launch'] / ALG[k]:.3f} | {r['dram_pct_peak']:.1f} | "
                  f"{r['issue_active_pct']:.1f} | {r['warps_active_pct']:.1f} | {r['registers']:.0f} | {st} |")
     L += ["", "Dense cases read DRAM/algorithmic slightly below 1: part of the written copy is still dirty in L2 when a "
-          "single profiled kernel ends; in steady state those writes reach DRAM during the next step. Sparse media read "
-          "whole 32-B sectors of partially solid rows: for RAS 256^3 phi 0.21 the geometric minimum is 1.18x the fluid "
-          "bytes (computed from the tile map), measured 1.28x.", "",
+          "single profiled kernel ends; in steady state those writes reach DRAM during the next step. Sparse media: "
+          "B200 global loads fetch whole 128-B lines (tools/gran_probe.cu; the .L2::64B qualifier on the gather halves "
+          "that), and the L2 bulk prefetch of whole tile blocks pulls the all-solid lines too (RAS 256^3 phi 0.21: "
+          "geometric minimum 1.18x the fluid bytes at 32-B sectors, 1.24x at 64 B, 1.55x whole blocks). The prefetch "
+          "still wins (interleaved A/B): the sparse gather is latency-bound without it (64 % of DRAM peak) and runs at "
+          "78 % with it.", "",
           "## Launch list (bench command)", ""] + launches()
     L += ["", "## Bench line (device-timed batches, steady state)", "",
           f"* configs[1] channel 128^3: **{b['value']} MLUPS**, {b['ms_per_step'] * 1e3:.1f} us/step, {b['roofline']['achieved']} GB/s "
@@ -61,6 +64,22 @@ def main():
     L += ["", "| other config | us/step | MLUPS | GB/s algorithmic | frac |", "|---|---|---|---|---|"]
     for r in b["other_configs"]:
         L.append(f"| {r['config']} | {r['us_per_step']} | {r['mlups']} | {r['achieved_gbs']} | {r['frac_of_measured_peak']} |")
+    L += ["", "## configs[4]: RAS 1024^3 on one B200 (`bench.py --config ras1024 --phi P [--single-copy]`)", "",
+          "| line | phi | storage | device GB | MLUPS | frac of copy peak | SM MHz (median) | throttle | generate s (GPU) | engine build s |",
+          "|---|---|---|---|---|---|---|---|---|---|"]
+    for f in sorted(os.listdir(PR)):
+        if f.startswith("bench_r1_ras1024") and f.endswith(".json"):
+            x = json.load(open(os.path.join(PR, f)))
+            c = x["config"]
+            L.append(f"| `{f}` | {c['phi']} | {'single copy (AA)' if 'single-copy' in c['workload'] else 'two copies'} | "
+                     f"{c['device_gb']} | {x['value']} | {x['roofline']['frac']} | {x['clocks']['sm_mhz']} | "
+                     f"{', '.join(x['clocks']['reasons']) or '-'} | {x['host_seconds']['generate']} | "
+                     f"{x['host_seconds']['engine_build']} |")
+    ref = os.path.join(PR, "bench_ref_r1.json")
+    if os.path.exists(ref):
+        r = json.load(open(ref))
+        L += ["", f"Reference arm (`bench.py --impl reference`, the reference's own TileEngineT2C<double> on "
+              f"{r['cpu_baseline']['cores']} host threads): **{r['value']} MLUPS** on the same 128^3 channel."]
     open(os.path.join(PR, "README.md"), "w").write("\n".join(L) + "\n")
 
 
