@@ -326,7 +326,7 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.gpus > 1:
         from paper_1703_08015_b200 import slab
-        return slab.bench_main(args, P)
+        return slab.bench_main(args, P, clock_sampler=ClockSampler, peak=measured_peaks())
     peak, peak_kind = measured_peaks()
     K, W = args.steps, args.warmup
     dims = (128, 128, 128)

@@ -282,21 +282,32 @@ class SlabRun:
         return self.engine.sync()
 
 
-def bench_main(args, P) -> int:
+def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured")) -> int:
     """bench.py at N>1 (torchrun): weak scaling — each rank owns a 128^3-node slab of one
-    (128 x 128 x 128*N) D3Q19 channel; N_f*K summed over ranks / max-over-ranks device time."""
+    (128 x 128 x 128*N) D3Q19 channel, tile-face halos through the fused NVLink peer stores
+    (SPLBM_SLAB_TRANSPORT=nccl|torch selects the others); value = N_f*K summed over ranks / the
+    max-over-ranks device time. e2e: the same through the public API with host buffers (NodeInit
+    fields H2D, the steps, fields D2H), max-over-ranks wall clock. With fewer GPUs than ranks
+    (validation on a one-GPU box) the ranks share the devices round-robin."""
+    import time
+
+    import numpy as np
     import torch
     import torch.distributed as dist
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(device)
+    dist.init_process_group("nccl" if torch.cuda.device_count() >= world else "gloo",
+                            **({"device_id": torch.device("cuda", device)}
+                               if torch.cuda.device_count() >= world else {}))
+    transport = os.environ.get("SPLBM_SLAB_TRANSPORT", "p2p")
     g = P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=(128, 128, 128 * world)))
     L = g.dims[2] // 4
     slabs = [(r * L // world, (r + 1) * L // world) for r in range(world)]
-    run = SlabRun(g, 4, P.FluidModel(tau=0.8), None, rank, world, local, slabs=slabs,
-                  transport=os.environ.get("SPLBM_SLAB_TRANSPORT", "p2p"))
+    run = SlabRun(g, 4, P.FluidModel(tau=0.8), None, rank, world, device, slabs=slabs,
+                  transport=transport)
     dist.barrier()  # transports up before the first step
     eng = run.engine
     run.initialize()
@@ -306,33 +317,81 @@ def bench_main(args, P) -> int:
     stop = torch.cuda.Event(enable_timing=True)
     dist.barrier()
     torch.cuda.synchronize()
+    launches0 = eng.launch_count()
+    sampler = clock_sampler(device) if (clock_sampler and rank == 0) else None
+    if sampler:
+        sampler.__enter__()
     with torch.cuda.stream(run.stream):
         start.record()
-    launches0 = eng.launch_count()
     run.step_async(args.steps)
     with torch.cuda.stream(run.stream):
         stop.record()
     ok, failed = run.sync()
     torch.cuda.synchronize()
+    if sampler:
+        sampler.__exit__(None, None, None)
     dist.barrier()
-    ms = torch.tensor([start.elapsed_time(stop)], device="cuda")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    nf = torch.tensor([float(eng.fluid_nodes())], device="cuda", dtype=torch.float64)
-    dist.all_reduce(nf)
-    ok_t = torch.tensor([1 if ok else 0], device="cuda")
-    dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
+    launches = eng.launch_count() - launches0
+
+    red_dev = torch.device("cuda", device) if dist.get_backend() == "nccl" else torch.device("cpu")
+
+    def max_over_ranks(v):
+        t = torch.tensor([float(v)], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(v):
+        t = torch.tensor([float(v)], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t)
+        return float(t.item())
+
+    t = max_over_ranks(start.elapsed_time(stop)) * 1e-3
+    nf_local = float(eng.fluid_nodes())
+    nf = sum_over_ranks(nf_local)
+    all_ok = sum_over_ranks(1.0 if ok else 0.0) == world
+    # e2e through the public API with host buffers: pinned NodeInit arrays H2D, the steps, the
+    # (rho, u) fields D2H into pinned rasters; wall clock, max over ranks
+    n_nodes = int(eng.info.n_tiles_stored) * eng.n_tn
+    pinned = [torch.empty(n_nodes, dtype=torch.float64, pin_memory=True).numpy() for _ in range(4)]
+    pinned[0][:] = 1.0
+    for a in pinned[1:]:
+        a[:] = 0.0
+    nr = g.node_count()
+    out = P.FieldData(g.d, g.dims, torch.empty(nr, dtype=torch.uint8, pin_memory=True).numpy(),
+                      *[torch.empty(nr, dtype=torch.float64, pin_memory=True).numpy() for _ in range(4)])
+    dist.barrier()
+    t0 = time.perf_counter()
+    eng.initialize_arrays(*pinned)
+    if world > 1:
+        dist.barrier()  # neighbours store faces into my halos from their first step on
+    run.step_async(args.steps)
+    ok2, _ = run.sync()
+    eng.fields(out=out)
+    wall = max_over_ranks(time.perf_counter() - t0)
     if rank == 0:
-        t = float(ms.item()) * 1e-3
-        mlups = float(nf.item()) * args.steps / t / 1e6
-        print(json.dumps({
+        alg = nf_local * 304.0 / (t / args.steps) / 1e9  # one rank's step kernel traffic, GB/s
+        line = {
             "metric": "MLUPS (D3Q19 fp64 BGK) vs porosity; % of HBM peak GB/s; at 1/2/4/8 B200",
-            "value": round(mlups, 1), "unit": "MLUPS", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(t / args.steps * 1e3, 5),
+            "value": round(nf * args.steps / t / 1e6, 1), "unit": "MLUPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t / args.steps * 1e3, 5),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "ok": bool(ok_t.item()),
+            "data": "synthetic", "ok": bool(all_ok and ok2),
             "config": {"workload": f"D3Q19 BGK fp64 channel 128x128x{128 * world}, z-slab per GPU "
-                                   "(128^3 nodes each), NCCL tile-face halo exchange",
-                       "parallelism": f"zslab{world}", "fluid_nodes": int(nf.item())},
-            "gpu_launches": int(eng.launch_count() - launches0)}))
+                                   f"(128^3 nodes each), tile-face halos via {transport}",
+                       "parallelism": f"zslab{world}", "fluid_nodes": int(nf),
+                       "devices": torch.cuda.device_count(),
+                       "l2": "inputs > L2 (two PDF copies of 1.3 GB per rank); no flush"},
+            "roofline": {"bound": "hbm", "achieved": round(alg, 1), "peak": peak[0], "unit": "GB/s",
+                         "frac": round(alg / peak[0], 4), "peak_source": peak[1],
+                         "per": "one rank (the slowest rank's time)"},
+            "gpu_launches": int(launches),
+            "e2e": {"value": round(nf * args.steps / wall / 1e6, 1), "unit": "MLUPS",
+                    "h2d_bytes_per_step": round(4 * n_nodes * 8 / args.steps, 1),
+                    "d2h_bytes_per_step": round(4 * n_nodes * 8 / args.steps, 1),
+                    "steps": args.steps, "wall_s": round(wall, 4), "per": "rank 0's buffers"},
+        }
+        if sampler:
+            line["clocks"] = sampler.summary()
+        print(json.dumps(line))
     dist.destroy_process_group()
     return 0
