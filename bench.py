@@ -140,6 +140,34 @@ def time_steps(eng, K, W, sampler_index=0):
     return ms, eng.launch_count() - l0, cs.summary()
 
 
+NCU_CASE = {0.2094: "ras256_phi02", 0.509: "ras256_phi05"}  # sweep points with a committed ncu capture
+
+
+def accounting(P, eng, nf, bnode, workload=None):
+    """The paper's ancillary-transfer accounting for one run: the T2C overhead model
+    (overhead_t2c with the measured phi_t and tile ratio, Eqs. 35/41), the geometric lower bounds
+    of the per-tile SoA layout at 32-B sector and 128-B line granularity (B200 loads fetch lines,
+    tools/gran_probe.cu), and the measured overhead = ncu DRAM bytes / algorithmic bytes - 1 where
+    a committed capture of the same workload exists (Table 5 analogue)."""
+    lat = P.solver_lattice(eng.d)
+    g = P.GeometryStats(phi=nf / max(1, int(np.prod(eng.geometry_dims))), phi_t=eng.info.phi_t,
+                        ratio_tiles=eng.info.ratio_tiles)
+    o = P.overhead_t2c(P.CostParams(lat=lat, a=eng.a), g)
+    types = eng.tile_grid().types
+    fl = types != 0
+    T, n = fl.shape
+    es = 8
+    out = {"model_delta_b": round(o.delta_b, 4), "model_delta_b_bt": round(o.delta_b_bt, 4)}
+    for name, nodes in (("sector_bound", 32 // es), ("line_bound", 128 // es)):
+        if n % nodes == 0:
+            out[name] = round(float(fl.reshape(T, n // nodes, nodes).any(axis=2).sum() * nodes / fl.sum()) - 1.0, 4)
+    tr = load_ncu_traffic(workload) if workload else None
+    if tr:
+        out["measured"] = round(tr / (nf * bnode) - 1.0, 4)
+        out["measured_source"] = f"profiles/ncu_step_kernel.json[{workload}]"
+    return out
+
+
 def porosity_sweep(P, K, W, peak):
     out = []
     for phi in (0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 1.0):
@@ -154,10 +182,12 @@ def porosity_sweep(P, K, W, peak):
         nf = eng.fluid_nodes()
         mlups = nf * K / (ms * 1e-3) / 1e6
         gbs = mlups * 1e6 * B_NODE[3] / 1e9
-        out.append({"phi": round(P.porosity(g).phi, 4), "phi_t": round(eng.info.phi_t, 4),
+        ph = round(P.porosity(g).phi, 4)
+        out.append({"phi": ph, "phi_t": round(eng.info.phi_t, 4),
                     "tiles": int(eng.info.n_tiles), "fluid_nodes": nf, "mlups": round(mlups, 1),
                     "achieved_gbs": round(gbs, 1), "frac_of_measured_peak": round(gbs / peak, 4),
-                    "bu_of_8tbs": round(gbs / 8000.0, 4)})
+                    "bu_of_8tbs": round(gbs / 8000.0, 4),
+                    "overhead": accounting(P, eng, nf, B_NODE[3], NCU_CASE.get(ph))})
         del eng
     return out
 
@@ -261,7 +291,12 @@ def cpu_baseline(P, dims, budget_s=15.0):
     e.step(steps)
     sec = e.last_seconds
     nf = g.fluid_count()
+    e1 = R.RefEngine(rg, "t2c", 4, 0.8, threads=1)  # the 1-thread figure
+    e1.initialize_uniform()
+    e1.step(2)
+    single = nf * 2 / e1.last_seconds / 1e6
     return {"value": round(nf * steps / sec / 1e6, 2), "unit": "MLUPS", "cores": threads,
+            "single_thread_mlups": round(single, 2),
             "kind": "reference",
             "sample": f"{steps} T2C steps of the {dims[0]}x{dims[1]}x{dims[2]} channel "
                       f"({'-march=x86-64-v3' if fast else '-O3'} build of /root/reference sources, "
@@ -357,6 +392,7 @@ def run_ours(args):
                      "traffic": load_ncu_traffic(workload)},
         "gpu_launches": int(launches),
         "clocks": clocks,
+        "overhead": accounting(P, eng, nf, B_NODE[3], workload),
     }
     del eng
     if not args.no_sweep:

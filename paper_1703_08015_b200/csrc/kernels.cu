@@ -50,6 +50,12 @@ __host__ __device__ constexpr int nb_offset() { return D == 3 ? 0 : 9; }
 #ifndef SPLBM_MINB2
 #define SPLBM_MINB2 6  // resident 256-thread CTAs per SM the 2D step is budgeted for
 #endif
+#ifndef SPLBM_MINB3F
+#define SPLBM_MINB3F 5  // the f32 engine: 48 registers, 20 CTAs/SM (+3-4 % vs 16, A/B)
+#endif
+#ifndef SPLBM_MINB2F
+#define SPLBM_MINB2F 6
+#endif
 #ifndef SPLBM_ZERO_FILL
 #define SPLBM_ZERO_FILL 1  // write 0.0 to solid slots sharing a 32-B sector with fluid slots
 #endif
@@ -228,7 +234,7 @@ __global__ void __launch_bounds__(kThreads)
 // plus one shared-memory lookup and two selects — no divergent branches, no dependent global load
 // before the PDF gather.
 template <int D, int LOGA, bool INC, bool PEER, bool MRT, class R>
-__global__ void __launch_bounds__((step_threads<D, (D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA)))>()), (MRT ? 2 : (D == 3 ? SPLBM_MINB3 : SPLBM_MINB2)) * 256 / step_threads<D, (D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA)))>())
+__global__ void __launch_bounds__((step_threads<D, (D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA)))>()), (MRT ? 2 : (D == 3 ? (sizeof(R) == 4 ? SPLBM_MINB3F : SPLBM_MINB3) : (sizeof(R) == 4 ? SPLBM_MINB2F : SPLBM_MINB2))) * 256 / step_threads<D, (D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA)))>())
     t2c_step_pow2_kernel(StepArgs args, const __grid_constant__ MrtMatrix<R, MRT ? Lat<D>::Q : 1> mrt) {
   constexpr int Q = Lat<D>::Q;
   const R* const rd = static_cast<const R*>(args.read);
