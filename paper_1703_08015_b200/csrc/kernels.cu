@@ -83,27 +83,28 @@ __device__ __forceinline__ void st_stream(float* p, float v) {
 
 // PDF gather load. B200 measurement (tools/gran_probe.cu): a plain or .nc global load that misses
 // fetches the whole 128-B line from DRAM; the .L2::64B prefetch-size qualifier limits that to
-// 64 B (the device limit cudaLimitMaxL2FetchGranularity has no effect). `hint`: 0 default,
-// 1 .L2::64B, 2 .L2::256B (a runtime switch for A/B timing; uniform across the grid).
-__device__ __forceinline__ double ld_pdf(const double* p, int hint) {
+// 64 B (the device limit cudaLimitMaxL2FetchGranularity has no effect): +1-3 % on every workload
+// (interleaved A/B), most on sparse media. SPLBM_LD_64B=0 builds the plain __ldg variant.
+#ifndef SPLBM_LD_64B
+#define SPLBM_LD_64B 1
+#endif
+__device__ __forceinline__ double ld_pdf(const double* p) {
+#if SPLBM_LD_64B
   double v;
-  if (hint == 1)
-    asm volatile("ld.global.nc.L2::64B.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  else if (hint == 2)
-    asm volatile("ld.global.nc.L2::256B.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  else
-    v = __ldg(p);
+  asm volatile("ld.global.nc.L2::64B.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
+#else
+  return __ldg(p);
+#endif
 }
-__device__ __forceinline__ float ld_pdf(const float* p, int hint) {
+__device__ __forceinline__ float ld_pdf(const float* p) {
+#if SPLBM_LD_64B
   float v;
-  if (hint == 1)
-    asm volatile("ld.global.nc.L2::64B.f32 %0, [%1];" : "=f"(v) : "l"(p));
-  else if (hint == 2)
-    asm volatile("ld.global.nc.L2::256B.f32 %0, [%1];" : "=f"(v) : "l"(p));
-  else
-    v = __ldg(p);
+  asm volatile("ld.global.nc.L2::64B.f32 %0, [%1];" : "=f"(v) : "l"(p));
   return v;
+#else
+  return __ldg(p);
+#endif
 }
 
 // L2 prefetch of a future CTA's read blocks (the CTA StepArgs::l2pf CTAs ahead, about half a
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(kThreads)
       const uint64_t s = __ldg(nbt + delta);
       src = rd + s * tile_stride + i * n_tn + sp;
     }
-    f[i] = ld_pdf(src, args.ldhint);
+    f[i] = ld_pdf(src);
   }
 
   bool good;
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__((step_threads<D, (D == 3 ? (1 << (3 * LOGA)) :
     const int delta = 13 + dx + 3 * dy + 9 * dz;
     const R* src = (delta == 13 ? own : nbp[delta - nb_offset<D>()]) + (i * NTN + sp);
     const R* bb = own + (opp(i) * NTN + p);  // half-way bounce-back (engine.hpp:498-500)
-    f[i] = ld_pdf(((info >> i) & 1u) ? bb : src, args.ldhint);
+    f[i] = ld_pdf(((info >> i) & 1u) ? bb : src);
   }
 
   bool good;
@@ -418,7 +419,7 @@ __global__ void __launch_bounds__(aa_threads<D, LOGA>(),
 
   R f[Q];
 #pragma unroll
-  for (int i = 0; i < Q; ++i) f[i] = ld_pdf(PHASE == 1 ? addr(i) : own + (opp(i) * NTN + p), args.ldhint);
+  for (int i = 0; i < Q; ++i) f[i] = ld_pdf(PHASE == 1 ? addr(i) : own + (opp(i) * NTN + p));
 
   bool good;
   if (type == 1) {
