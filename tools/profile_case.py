@@ -21,10 +21,16 @@ CASES = {
 
 if __name__ == "__main__":
     name = sys.argv[1]
+    if name == "ras_device_generator":  # the RAS sphere loop on the GPU (geometry_gpu.cu)
+        g = P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(40, 36, 32), sphere_diameter=9,
+                                                              target_porosity=0.4, seed=3), device=0)
+        print(name, "phi", P.porosity(g).phi)
+        sys.exit(0)
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 6
     g, a, per = CASES[name]()
     e = P.TileEngineT2C(g, a, P.FluidModel(tau=0.8), per,
-                        single_copy=os.environ.get("SPLBM_SINGLE_COPY") == "1")
+                        single_copy=os.environ.get("SPLBM_SINGLE_COPY") == "1",
+                        precision=os.environ.get("SPLBM_PRECISION", "f64"))
     e.initialize_uniform(1.0, (0.01, 0.0, 0.0))
     ok, _ = e.step_n(steps)
     e.fields()

@@ -1,0 +1,19 @@
+#!/bin/bash
+# compute-sanitizer memcheck / racecheck / initcheck over the step paths (two copies, single copy,
+# f32, pow2 and generic kernels) and the device RAS generator; summary table on stdout.
+mkdir -p gpurun_out/san
+cd "$(dirname "$0")/.."
+run() {  # name env case
+  local name=$1; shift; local envs=$1; shift; local case=$1
+  for t in memcheck racecheck initcheck; do
+    env $envs timeout 900 compute-sanitizer --tool $t --error-exitcode 9 python tools/profile_case.py $case 3 > gpurun_out/san/${t}_$name.log 2>&1
+    echo "$name $t rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' gpurun_out/san/${t}_$name.log | tail -1)"
+  done
+}
+run ras48_f64 "SPLBM_PRECISION=f64" ras48_periodic
+run ras48_single_copy "SPLBM_SINGLE_COPY=1" ras48_periodic
+run ras48_f32 "SPLBM_PRECISION=f32" ras48_periodic
+run channel_single_copy_f32 "SPLBM_SINGLE_COPY=1 SPLBM_PRECISION=f32" channel3d_small
+run cavity2d_a16_single_copy "SPLBM_SINGLE_COPY=1" cavity2d_64_a16
+run random_a3_generic "SPLBM_PRECISION=f64" random_a3
+run ras_device_generator "SPLBM_PRECISION=f64" ras_device_generator
