@@ -7,9 +7,11 @@
 // What parallelises is the work per candidate: counting (and then marking) the nodes of a ~d^3
 // bounding box. The RNG stream is independent of the decisions (every candidate consumes exactly
 // three canonical() draws, geometry.cpp:302-304), so the host draws the candidate centres with the
-// same mt19937_64 and one persistent CTA of 1024 threads runs the accept/skip/retry loop on the
-// device: a block-wide count, the reference's decision (uniform across the block), a marking pass.
-// 1024^3 at phi 0.2: ~50 k spheres, well under a second, instead of ~23 s on the host.
+// same mt19937_64 and one persistent thread-block cluster (16 CTAs x 1024 threads on 16 SMs) runs
+// the accept/skip/retry loop on the device: each CTA counts its share of the box, the 16 partial
+// counts are exchanged through distributed shared memory around one cluster barrier per pass,
+// every CTA takes the reference's decision on the same total, and the marking pass follows.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -52,13 +54,19 @@ struct RasArgs {
   RasState* st;
 };
 
+namespace cg = cooperative_groups;
+
 __device__ __forceinline__ int wrap(int v, int n) { return ((v % n) + n) % n; }
 
 // Count (commit == false) or mark (commit == true) the nodes of the sphere at c, as mark_sphere
 // (geometry.cpp:267-291). Block-wide; returns the count on every thread. `serial` handles boxes
 // wider than the domain (a wrapped node visited twice): the reference's sequential order decides.
 __device__ unsigned long long sphere_pass(const RasArgs& a, const double* c, bool commit,
-                                          unsigned long long* s_red) {
+                                          unsigned long long* s_red, unsigned long long* s_part,
+                                          int& parity) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int nranks = static_cast<int>(cluster.num_blocks());
   const int x0 = static_cast<int>(floor(__dsub_rn(c[0], a.r))), x1 = static_cast<int>(ceil(__dadd_rn(c[0], a.r)));
   const int y0 = static_cast<int>(floor(__dsub_rn(c[1], a.r))), y1 = static_cast<int>(ceil(__dadd_rn(c[1], a.r)));
   const int z0 = static_cast<int>(floor(__dsub_rn(c[2], a.r))), z1 = static_cast<int>(ceil(__dadd_rn(c[2], a.r)));
@@ -67,7 +75,8 @@ __device__ unsigned long long sphere_pass(const RasArgs& a, const double* c, boo
   unsigned long long cnt = 0;
   const long long box = static_cast<long long>(nx) * ny * nz;
   if (!serial) {
-    for (long long k = threadIdx.x; k < box; k += kRasThreads) {
+    for (long long k = static_cast<long long>(rank) * kRasThreads + threadIdx.x; k < box;
+         k += static_cast<long long>(nranks) * kRasThreads) {
       const int x = x0 + static_cast<int>(k % nx);
       const int y = y0 + static_cast<int>((k / nx) % ny);
       const int z = z0 + static_cast<int>(k / (static_cast<long long>(nx) * ny));
@@ -83,7 +92,7 @@ __device__ unsigned long long sphere_pass(const RasArgs& a, const double* c, boo
         if (commit) *p = kSolid;
       }
     }
-  } else if (threadIdx.x == 0) {  // reference loop order z, y, x
+  } else if (threadIdx.x == 0 && rank == 0) {  // reference loop order z, y, x
     for (int z = z0; z <= z1; ++z) {
       const double dz = __dsub_rn(static_cast<double>(z), c[2]);
       for (int y = y0; y <= y1; ++y) {
@@ -110,27 +119,40 @@ __device__ unsigned long long sphere_pass(const RasArgs& a, const double* c, boo
   if (threadIdx.x < 32) {
     unsigned long long v = s_red[threadIdx.x];
     for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
-    if (threadIdx.x == 0) s_red[32] = v;
+    if (threadIdx.x == 0) s_part[parity] = v;
+  }
+  // The marks of this pass and the partial count are published to the whole cluster (release /
+  // acquire barrier); every CTA then sums the same partials in the same order. s_part is double
+  // buffered by pass parity: a slot is rewritten two passes later, after every CTA has passed the
+  // next pass's barrier, i.e. after it read this pass's values.
+  __threadfence();
+  cluster.sync();
+  if (threadIdx.x == 0) {
+    unsigned long long tot = 0;
+    for (int r = 0; r < nranks; ++r) tot += *cluster.map_shared_rank(&s_part[parity], r);
+    s_red[32] = tot;
   }
   __syncthreads();
   const unsigned long long total = s_red[32];
-  __threadfence_block();  // marks visible to the next pass of this block
+  parity ^= 1;
   return total;
 }
 
 // The accept/skip/retry loop of generate_ras (geometry.cpp:296-324) over one batch of candidates.
 __global__ void __launch_bounds__(kRasThreads, 1) ras_kernel(RasArgs a) {
   __shared__ unsigned long long s_red[33];
+  __shared__ unsigned long long s_part[2];
+  int parity = 0;
   RasState s = *a.st;
   unsigned long long k = 0;
   while (static_cast<double>(a.n_total - s.solid) / static_cast<double>(a.n_total) > a.upper) {
     if (k == a.n_cand) break;  // batch exhausted: the host draws more candidates
     const double* c = a.cand + 3 * k;
     ++k;
-    const unsigned long long newly = sphere_pass(a, c, false, s_red);
+    const unsigned long long newly = sphere_pass(a, c, false, s_red, s_part, parity);
     const double phi_after = static_cast<double>(a.n_total - s.solid - newly) / static_cast<double>(a.n_total);
     if (phi_after >= a.lower || s.skips >= 2000) {
-      s.solid += sphere_pass(a, c, true, s_red);
+      s.solid += sphere_pass(a, c, true, s_red, s_part, parity);
       s.skips = 0;
       s.best_err = 2.0;
       continue;
@@ -143,15 +165,42 @@ __global__ void __launch_bounds__(kRasThreads, 1) ras_kernel(RasArgs a) {
       s.best[2] = c[2];
     }
     if (++s.skips == 2000) {
-      s.solid += sphere_pass(a, s.best, true, s_red);
+      s.solid += sphere_pass(a, s.best, true, s_red, s_part, parity);
       s.skips = 0;
       s.best_err = 2.0;
     }
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && cg::this_cluster().block_rank() == 0) {
     s.done = static_cast<double>(a.n_total - s.solid) / static_cast<double>(a.n_total) <= a.upper;
     s.consumed = k;
     *a.st = s;
+  }
+  cg::this_cluster().sync();  // no CTA leaves while another may still read its shared memory
+}
+
+// One cluster of 16 CTAs (non-portable size; 8, then 1, if the device refuses it).
+void launch_cluster(const RasArgs& a) {
+  static int size = 0;
+  if (size == 0) {
+    cudaFuncSetAttribute(ras_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    size = 16;
+  }
+  for (;;) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(size);
+    cfg.blockDim = dim3(kRasThreads);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = size;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, ras_kernel, a);
+    if (e == cudaSuccess) return;
+    cudaGetLastError();  // clear, retry smaller
+    if (size == 1) CK(e);
+    size = size > 8 ? 8 : 1;
   }
 }
 
@@ -217,8 +266,7 @@ extern "C" int splbm_generate_device(int kind, const splbm_generate_params* p, i
             host[3 * k + c] = static_cast<double>(rng() >> 11) * 0x1.0p-53 * dims[c];
         CK(cudaMemcpy(cand, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice));
         a.n_cand = batch;
-        ras_kernel<<<1, kRasThreads>>>(a);
-        CK(cudaGetLastError());
+        launch_cluster(a);
         RasState s{};
         CK(cudaMemcpy(&s, st, sizeof(s), cudaMemcpyDeviceToHost));
         if (s.done) break;
