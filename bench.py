@@ -33,6 +33,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 B_NODE = {2: 144.0, 3: 304.0}  # algorithmic bytes per node update, 2*q*8 (overhead.cpp:59-62)
+WORKLOAD_1 = ("D3Q19 BGK fp64 channel 128^3 (BASELINE configs[1]), bounce-back walls, V inlet / "
+              "P outlet, tiles 4^3, quasi-compressible, tau 0.8")
 
 
 def measured_peaks():
@@ -321,7 +323,9 @@ def run_reference_arm(args):
         return 0
     import paper_1703_08015_b200 as P
     from oracle import ref as R
-    dims = (128, 128, 128)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    n = max(world, args.gpus)
+    dims = (128, 128, 128 * n)  # our arm's workload at this N (one 128^3 slab per GPU)
     fast = R.available(fast=True) and _cpu_has_avx2()
     if not R.available(fast=fast):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
@@ -344,12 +348,15 @@ def run_reference_arm(args):
             "warmup": args.warmup, "ms_per_step": round(sec / args.steps * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": "D3Q19 BGK fp64 channel 128^3, bounce-back walls, tiles 4^3",
-                       "lattice": "D3Q19", "tile": 4, "fluid_nodes": nf},
+            "config": ({"workload": WORKLOAD_1, "fluid_nodes": nf, "tiles": 32768, "phi_t": 0.969,
+                        "parallelism": "reference CPU engine"} if n == 1 else
+                       {"workload": f"D3Q19 BGK fp64 channel 128x128x{128 * n}, z-slab per GPU "
+                                    "(128^3 nodes each)", "parallelism": "reference CPU engine",
+                        "fluid_nodes": nf}),
             "cpu_baseline": {"value": round(mlups, 2), "unit": "MLUPS", "cores": threads,
                              "kind": "reference",
-                             "sample": f"{args.steps} steps of the full 128^3 channel, "
-                                       f"TileEngineT2C<double> + ThreadPool({threads})"},
+                             "sample": f"{args.steps} steps of the full {dims[0]}x{dims[1]}x{dims[2]} "
+                                       f"channel, TileEngineT2C<double> + ThreadPool({threads})"},
             "e2e": {"value": round(mlups, 2), "unit": "MLUPS", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -380,8 +387,7 @@ def run_ours(args):
         "value": round(mlups, 1), "unit": "MLUPS", "n_gpus": 1, "steps": K, "warmup": W,
         "ms_per_step": round(step_ms, 5), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "D3Q19 BGK fp64 channel 128^3 (BASELINE configs[1]), bounce-back "
-                               "walls, V inlet / P outlet, tiles 4^3, quasi-compressible, tau 0.8",
+        "config": {"workload": WORKLOAD_1,
                    "fluid_nodes": nf, "tiles": int(eng.info.n_tiles),
                    "phi_t": round(eng.info.phi_t, 4),
                    "l2": "inputs > L2 (two PDF copies of 1.3 GB); no flush",

@@ -306,8 +306,19 @@ def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured")) -> int:
     g = P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=(128, 128, 128 * world)))
     L = g.dims[2] // 4
     slabs = [(r * L // world, (r + 1) * L // world) for r in range(world)]
-    run = SlabRun(g, 4, P.FluidModel(tau=0.8), None, rank, world, device, slabs=slabs,
-                  transport=transport)
+    try:
+        run = SlabRun(g, 4, P.FluidModel(tau=0.8), None, rank, world, device, slabs=slabs,
+                      transport=transport)
+        ok_setup = 1.0
+    except Exception:  # noqa: BLE001 - e.g. no peer access between these GPUs
+        ok_setup = 0.0
+    flag = torch.tensor([ok_setup], device=torch.device("cuda", device)
+                        if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if flag.item() < 1.0:  # every rank falls back together: native NCCL send/recv halos
+        transport = "nccl"
+        run = SlabRun(g, 4, P.FluidModel(tau=0.8), None, rank, world, device, slabs=slabs,
+                      transport=transport)
     dist.barrier()  # transports up before the first step
     eng = run.engine
     run.initialize()
