@@ -56,6 +56,12 @@ __host__ __device__ constexpr int nb_offset() { return D == 3 ? 0 : 9; }
 #ifndef SPLBM_MINB2F
 #define SPLBM_MINB2F 6
 #endif
+#ifndef SPLBM_X2_THREADS
+#define SPLBM_X2_THREADS 64  // two-nodes-per-thread step (f32): CTA size
+#endif
+#ifndef SPLBM_X2_MINB
+#define SPLBM_X2_MINB 16     // ... and resident CTAs per SM (64 registers)
+#endif
 #ifndef SPLBM_ZERO_FILL
 #define SPLBM_ZERO_FILL 1  // write 0.0 to solid slots sharing a 32-B sector with fluid slots
 #endif
@@ -333,6 +339,97 @@ __global__ void __launch_bounds__((step_threads<D, (D == 3 ? (1 << (3 * LOGA)) :
     for (int i = 0; i < Q; ++i)
       if ((D == 3 ? ez<D>(i) : ey<D>(i)) < 0) dst[i * NTN] = f[i];
   }
+  }
+}
+
+// Two nodes per thread (the f32 engine): a float gather moves half the bytes of a double one, so
+// one node per thread leaves too few bytes in flight; here thread j of a tile's half takes nodes j
+// and j + NTN/2 and issues both gathers (2 x q loads) before either collision: +7-13 % over one
+// node per thread (interleaved A/B). Same addressing, slots and arithmetic as
+// t2c_step_pow2_kernel (BGK, no slab peer stores).
+template <int D, int LOGA, bool INC, class R>
+__global__ void __launch_bounds__(SPLBM_X2_THREADS, SPLBM_X2_MINB)
+    t2c_step_x2_kernel(StepArgs args, const __grid_constant__ MrtMatrix<R, 1> mrt) {
+  constexpr int Q = Lat<D>::Q;
+  const R* const rd = static_cast<const R*>(args.read);
+  constexpr int A = 1 << LOGA;
+  constexpr int NTN = D == 3 ? A * A * A : A * A;
+  constexpr int HALF = NTN / 2;                 // threads per tile
+  constexpr int TILES = SPLBM_X2_THREADS / HALF;
+  constexpr uint64_t STRIDE = static_cast<uint64_t>(Q) * NTN;
+  constexpr int NBS = nb_stride<D>();
+  __shared__ const R* s_base[TILES][NBS];
+
+  const uint64_t n_tiles = args.n_nodes / NTN;
+  const uint64_t tile_blk = static_cast<uint64_t>(blockIdx.x) * TILES;
+  for (int k = threadIdx.x; k < TILES * NBS; k += SPLBM_X2_THREADS) {
+    const int tl = k / NBS, dd = k % NBS;
+    const uint64_t tt = tile_blk + tl;
+    const R* b = nullptr;
+    if (tt < n_tiles) {
+      const uint32_t s = __ldg(args.nb + (args.t0 + tt) * NBS + dd);
+      b = s == kEmpty ? nullptr : rd + static_cast<uint64_t>(s) * STRIDE;
+    }
+    s_base[tl][dd] = b;
+  }
+  const int tl = threadIdx.x / HALF;
+  const int j = threadIdx.x % HALF;
+  const uint64_t tloc = tile_blk + tl;
+  const bool live = tloc < n_tiles;
+  const uint64_t t = args.t0 + tloc;
+  uint32_t info[2];
+  info[0] = live ? __ldg(args.info + t * NTN + j) : 0u;
+  info[1] = live ? __ldg(args.info + t * NTN + j + HALF) : 0u;
+  const uint64_t pf = tile_blk + static_cast<uint64_t>(args.l2pf) * TILES + threadIdx.x;
+  __syncthreads();
+#if SPLBM_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+  l2_prefetch_blocks<Q, NTN, TILES>(rd, args.t0 + pf, args.l2pf && pf < n_tiles);
+  const R* own = rd + t * STRIDE;
+  const R* const* nbp = s_base[tl];
+  R f[2][Q];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int p = j + u * HALF;
+    const int lx = p & (A - 1);
+    const int ly = (p >> LOGA) & (A - 1);
+    const int lz = D == 3 ? (p >> (2 * LOGA)) : 0;
+    const bool act = ((info[u] >> 24) & 3) != 0;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+      const int vx = lx - ex<D>(i), vy = ly - ey<D>(i), vz = lz - ez<D>(i);
+      const int dx = ex<D>(i) ? (vx >> LOGA) : 0;
+      const int dy = ey<D>(i) ? (vy >> LOGA) : 0;
+      const int dz = (D == 3 && ez<D>(i)) ? (vz >> LOGA) : 0;
+      const int sp = (vx & (A - 1)) | ((vy & (A - 1)) << LOGA) | (D == 3 ? ((vz & (A - 1)) << (2 * LOGA)) : 0);
+      const int delta = 13 + dx + 3 * dy + 9 * dz;
+      const R* src = (delta == 13 ? own : nbp[delta - nb_offset<D>()]) + (i * NTN + sp);
+      const R* bb = own + (opp(i) * NTN + p);
+      f[u][i] = act ? ld_pdf(((info[u] >> i) & 1u) ? bb : src) : R(0);
+    }
+  }
+  R* wr0 = static_cast<R*>(args.write) + t * STRIDE + j;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    R* wr = wr0 + u * HALF;
+    const int type = (info[u] >> 24) & 3;
+    if (type == 0) {
+      if (info[u] & (1u << 27)) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) st_stream(wr + i * NTN, R(0));
+      }
+      continue;
+    }
+    bool good;
+    if (type == 1)
+      good = collide_bgk<D, INC>(f[u], static_cast<R>(args.inv_tau));
+    else
+      good = apply_boundary<D, INC>(f[u], type, (info[u] >> 26) & 1u, args.bc);
+    if (!good) atomicMin(args.failed, static_cast<unsigned long long>(*args.step_base + args.rel + 1));
+#pragma unroll
+    for (int i = 0; i < Q; ++i) st_stream(wr + i * NTN, f[u][i]);
   }
 }
 
@@ -754,6 +851,15 @@ static void launch_pow2(const StepArgs& a, cudaStream_t st) {
   if constexpr (std::is_same<R, double>::value) {
     if (a.peer_up || a.peer_down) {  // slab boundary planes with NVLink peer stores
       t2c_step_pow2_kernel<D, LOGA, INC, true, false, R><<<blocks, step_threads<D, NTN>(), 0, st>>>(a, none);
+      return;
+    }
+  }
+  // f32 only: for f64 two nodes per thread need 128 registers and measured 5-11 % slower
+  if constexpr (sizeof(R) == 4 && NTN >= 16 && (SPLBM_X2_THREADS % (NTN / 2)) == 0) {
+    if (a.x2 && a.skip_by == 0) {  // f32: two nodes per thread
+      constexpr int XT = SPLBM_X2_THREADS / (NTN / 2);
+      const unsigned xb = static_cast<unsigned>((tiles + XT - 1) / XT);
+      launch_maybe_pdl(t2c_step_x2_kernel<D, LOGA, INC, R>, xb, st, a, none, SPLBM_X2_THREADS);
       return;
     }
   }

@@ -33,6 +33,7 @@ struct StepArgs {
   // 1 = the step from the natural state (gather from x - e_i, scatter to x + e_i);
   // 2 = the step from the swapped state (own node only: read slot opp(i), write slot i).
   int aa;
+  int x2;  // f32 power-of-two BGK step: two nodes per thread (t2c_step_x2_kernel)
   // Slab mode, NVLink peer stores (power-of-two tile kernel only): the face layer of my top
   // plane tiles [top_begin, ...) is also stored, for the directions leaving upwards, into the
   // upper neighbour's next copy at its low halo tiles (peer_up = that copy's first halo tile);
