@@ -104,6 +104,7 @@ struct splbm_dev_engine {
   std::vector<double> mrt_K;  // MRT operator (host copy; passed to the kernels by value), empty = BGK
   uint64_t device_bytes = 0;
   uint32_t l2pf = 0;  // step kernel L2 prefetch distance in CTAs (StepArgs::l2pf)
+  uint64_t pdl_min_threads = 4ull * 148 * 256;  // StepArgs::pdl_min_threads (SPLBM_PDL_MIN)
   int x2 = 1;         // StepArgs::x2: f32 two nodes per thread (SPLBM_X2=0 disables)
   // single-copy (AA) propagation: one PDF array (pdf[0]); `read` is then the state parity
   // (0 natural layout, 1 swapped, see t2c_aa_kernel)
@@ -208,6 +209,7 @@ struct splbm_dev_engine {
     s.step_base = step_base;
     s.rel = rel;
     s.l2pf = l2pf;
+    s.pdl_min_threads = pdl_min_threads;
     s.x2 = x2;
     if (peer_part1) {
       s.peer_up = peer_pdf_up[1 - rd];
@@ -477,6 +479,7 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device));
     e->l2pf = static_cast<uint32_t>(2 * sms);
     if (const char* v = std::getenv("SPLBM_L2PF")) e->l2pf = static_cast<uint32_t>(std::atoi(v));
+    if (const char* v = std::getenv("SPLBM_PDL_MIN")) e->pdl_min_threads = std::strtoull(v, nullptr, 10);
     if (const char* v = std::getenv("SPLBM_X2")) e->x2 = std::atoi(v);
   }
   CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));

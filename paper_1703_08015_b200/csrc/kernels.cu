@@ -802,7 +802,7 @@ static void launch_maybe_pdl(Kern kern, unsigned blocks, cudaStream_t st, const 
 #if SPLBM_PDL
   // Overlap the next step's launch and static-table prologue with this step's tail; below a few
   // waves (launch-latency-bound domains) the plain launch measured faster.
-  if (static_cast<uint64_t>(blocks) * threads >= 4ull * 148 * 256) {
+  if (static_cast<uint64_t>(blocks) * threads >= a.pdl_min_threads) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(blocks);
     cfg.blockDim = dim3(threads);

@@ -33,6 +33,7 @@ struct StepArgs {
   // 1 = the step from the natural state (gather from x - e_i, scatter to x + e_i);
   // 2 = the step from the swapped state (own node only: read slot opp(i), write slot i).
   int aa;
+  uint64_t pdl_min_threads;  // programmatic dependent launch from this grid size on
   int x2;  // f32 power-of-two BGK step: two nodes per thread (t2c_step_x2_kernel)
   // Slab mode, NVLink peer stores (power-of-two tile kernel only): the face layer of my top
   // plane tiles [top_begin, ...) is also stored, for the directions leaving upwards, into the

@@ -21,6 +21,8 @@ CASES = {
     "ras256_phi05": lambda: (P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(256, 256, 256), sphere_diameter=40, target_porosity=0.5, seed=7)), 7),
     "full256": lambda: (P.Geometry.filled(3, (256, 256, 256)), 7),
     "cavity2d_4096_a4": lambda: (P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(4096, 4096, 1))), 0),
+    "cavity2d_256_a4": lambda: (P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(256, 256, 1))), 0),
+    "cavity2d_256_a16": lambda: (P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(256, 256, 1))), 0),
     "vessel4096": lambda: (P.generate(P.GeometryKind.Vessel2D, P.GenerateParams(dims=(4096, 4096, 1), target_porosity=0.2, seed=1)), 0),
 }
 
@@ -50,7 +52,8 @@ def main():
             saved_lib = _native._lib
             if "LIB" in env:  # another build of the library (e.g. variants/lib_old.so)
                 _native._lib = libs.setdefault(env["LIB"], _native.load(os.path.join(ROOT, env["LIB"])))
-            e = P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8), per, single_copy=single, precision=prec)
+            e = P.TileEngineT2C(g, 16 if case.endswith("_a16") else 4, P.FluidModel(tau=0.8), per,
+                                single_copy=single, precision=prec)
             _native._lib = saved_lib
             for k, v in saved.items():
                 if v is None:
