@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+SPLBM_LIB=variants/lib_gtab.so timeout 900 python -m pytest tests/test_device_single_copy.py -q -x > gpurun_out/gtab2_test.log 2>&1; echo test=$?
+grep -E "passed|failed" gpurun_out/gtab2_test.log | tail -2
+timeout 1500 python tools/ab.py '{"aa": {"SPLBM_SINGLE_COPY": 1}, "aa_gtab": {"LIB": "variants/lib_gtab.so", "SPLBM_SINGLE_COPY": 1}}' channel128 ras256_phi02 full256 cavity2d_4096_a4 --rounds 9 --steps 128 > gpurun_out/gtab2_ab.log 2>&1; echo ab=$?
+grep -v "^{" gpurun_out/gtab2_ab.log | cut -c1-300
