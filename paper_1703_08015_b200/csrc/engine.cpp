@@ -71,9 +71,6 @@ const StreamMemOps& stream_mem_ops() {
 }
 
 constexpr uint64_t kChunkNodes = 1ull << 22;  // init / moments staging (4 x 32 MB)
-#ifndef SPLBM_L2_FETCH
-#define SPLBM_L2_FETCH 0  // L2 fetch granularity hint in bytes (0 = driver default)
-#endif
 constexpr int kGraphSteps = 32;               // steps per captured graph (even)
 
 }  // namespace
@@ -469,7 +466,6 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
     throw Error(SPLBM_ERR_CUDA, "no CUDA device available (the T2C path has no CPU fallback)");
   if (e->device < 0 || e->device >= ndev) throw config_error("invalid CUDA device ordinal");
   CK(cudaSetDevice(e->device));
-  if (SPLBM_L2_FETCH > 0) CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, SPLBM_L2_FETCH));
   {
     // L2 prefetch distance of the step kernel: two CTAs per SM ahead (64-thread CTAs: 296 tiles
     // of a 4^3 3D domain). Interleaved A/B on a B200 against no prefetch: channel 128^3 +6 %,
