@@ -1,3 +1,4 @@
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/gran_probe tools/gran_probe.cu
 // Probe: DRAM bytes and L2 sectors fetched when one 32-B sector out of every 128 B is read, per
 // load flavour (does an L1 miss request 32 B or the whole 128-B line?). Run under ncu with
 // dram__bytes_read.sum and lts__t_sectors_srcunit_tex_op_read.sum; the kernel name carries the
