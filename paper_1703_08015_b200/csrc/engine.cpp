@@ -126,6 +126,10 @@ struct splbm_dev_engine {
   cudaEvent_t ev_packed = nullptr, ev_arrived = nullptr;
   // fused NVLink peer-store halo exchange (splbm_dev_p2p_attach)
   bool p2p = false, peer_part1 = false;
+  cudaStream_t side = nullptr;               // p2p: the boundary planes run here, beside the interior
+  cudaEvent_t ev_int[2] = {nullptr, nullptr};  // interior(s) + bump done, by step parity
+  cudaEvent_t ev_bnd[2] = {nullptr, nullptr};  // boundary planes(s) + flag writes done
+  long long* zero_base = nullptr;  // p2p: failure stamps use the absolute step number as `rel`
   unsigned long long* flags = nullptr;  // [0] faces from below arrived, [1] from above (step seq)
   double* peer_pdf_up[2] = {nullptr, nullptr};
   double* peer_pdf_down[2] = {nullptr, nullptr};
@@ -159,10 +163,17 @@ struct splbm_dev_engine {
     if (ev_packed) cudaEventDestroy(ev_packed);
     if (ev_arrived) cudaEventDestroy(ev_arrived);
     if (comm_stream) cudaStreamDestroy(comm_stream);
+    if (side) cudaStreamSynchronize(side);
+    for (int k = 0; k < 2; ++k) {
+      if (ev_int[k]) cudaEventDestroy(ev_int[k]);
+      if (ev_bnd[k]) cudaEventDestroy(ev_bnd[k]);
+    }
+    if (side) cudaStreamDestroy(side);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     for (void* p : {static_cast<void*>(pdf[0]), static_cast<void*>(pdf[1]),
                     static_cast<void*>(info), static_cast<void*>(nb), static_cast<void*>(failed),
                     static_cast<void*>(step_base), static_cast<void*>(domain_err),
+                    static_cast<void*>(zero_base),
                     static_cast<void*>(halo_dirs), static_cast<void*>(scratch)})
       if (p) cudaFree(p);
     if (pinned) cudaFreeHost(pinned);
@@ -205,6 +216,10 @@ struct splbm_dev_engine {
     s.failed = failed;
     s.step_base = step_base;
     s.rel = rel;
+    if (p2p && zero_base) {  // steps enqueued one by one (no graphs): absolute step, no bump
+      s.step_base = zero_base;
+      s.rel = static_cast<int>(step_count) + rel;
+    }
     s.l2pf = l2pf;
     s.pdl_min_threads = pdl_min_threads;
     s.x2 = x2;
@@ -230,7 +245,7 @@ struct splbm_dev_engine {
 
   // Slab-overlap parts: 1 = the bottom and top owned planes (their faces are exchanged while
   // part 2, the interior planes, runs); part 2 then swaps the copies and counts the step.
-  void step_part(int part) {
+  void step_part(int part, cudaEvent_t before_bump = nullptr) {
     if (aa) throw config_error("the slab step parts need the two-copy scheme");
     const uint64_t b0 = n_low, b1 = n_low + send_low_tiles;          // bottom plane
     const uint64_t t0 = n_low + n_own - send_high_tiles, t1 = n_low + n_own;  // top plane
@@ -253,6 +268,7 @@ struct splbm_dev_engine {
       return;
     }
     if (!merged) launch_range(read, b1, t0);
+    if (before_bump) CK(cudaStreamWaitEvent(stream, before_bump, 0));
     CK(splbm_dev::launch_bump(step_base, 1, stream));
     ++launches;
     read = 1 - read;
@@ -310,21 +326,40 @@ struct splbm_dev_engine {
   // seq+1 wait until both neighbours finished their boundary planes of step seq (so my halos hold
   // their faces and they no longer read the halo copy I am about to overwrite); afterwards publish
   // seq+1 into the neighbours' flags.
+  //
+  // The boundary planes run on a side stream, concurrently with the interior planes of the same
+  // step on the engine stream (SURVEY §8e overlap): step s with parity k
+  //   side:   wait ev_int[k^1] (interior(s-1): the planes read what it wrote next to them, and
+  //           overwrite the copy it read) -> flag waits -> boundary planes (+ peer stores) -> flag
+  //           writes -> record ev_bnd[k]
+  //   engine: wait ev_bnd[k^1] (boundary(s-1), same reasons) -> interior(s) -> record ev_int[k]
+  // Failure stamps carry the absolute step number (no bump kernel between the parts).
   void p2p_step() {
     const StreamMemOps& ops = stream_mem_ops();
+    const int k = static_cast<int>(comm_seq & 1);
+    CK(cudaStreamWaitEvent(side, ev_int[k ^ 1], 0));
     if (peer_pdf_down[0])
-      cu_check(ops.wait(stream, reinterpret_cast<CUdeviceptr>(&flags[0]), comm_seq, CU_STREAM_WAIT_VALUE_GEQ), "cuStreamWaitValue64");
+      cu_check(ops.wait(side, reinterpret_cast<CUdeviceptr>(&flags[0]), comm_seq, CU_STREAM_WAIT_VALUE_GEQ), "cuStreamWaitValue64");
     if (peer_pdf_up[0])
-      cu_check(ops.wait(stream, reinterpret_cast<CUdeviceptr>(&flags[1]), comm_seq, CU_STREAM_WAIT_VALUE_GEQ), "cuStreamWaitValue64");
+      cu_check(ops.wait(side, reinterpret_cast<CUdeviceptr>(&flags[1]), comm_seq, CU_STREAM_WAIT_VALUE_GEQ), "cuStreamWaitValue64");
     peer_part1 = true;
+    std::swap(stream, side);  // part 1 launches on the side stream
     step_part(1);
+    std::swap(stream, side);
     peer_part1 = false;
     ++comm_seq;
     if (peer_pdf_up[0])  // the upper rank's "from below" flag
-      cu_check(ops.write(stream, reinterpret_cast<CUdeviceptr>(&peer_flags_up[0]), comm_seq, CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue64");
+      cu_check(ops.write(side, reinterpret_cast<CUdeviceptr>(&peer_flags_up[0]), comm_seq, CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue64");
     if (peer_pdf_down[0])  // the lower rank's "from above" flag
-      cu_check(ops.write(stream, reinterpret_cast<CUdeviceptr>(&peer_flags_down[1]), comm_seq, CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue64");
-    step_part(2);
+      cu_check(ops.write(side, reinterpret_cast<CUdeviceptr>(&peer_flags_down[1]), comm_seq, CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue64");
+    CK(cudaEventRecord(ev_bnd[k], side));
+    CK(cudaStreamWaitEvent(stream, ev_bnd[k ^ 1], 0));
+    const uint64_t b1 = n_low + send_low_tiles, t0 = n_low + n_own - send_high_tiles;
+    if (b1 < t0) launch_range(read, b1, t0);  // interior planes
+    CK(cudaEventRecord(ev_int[k], stream));
+    read = 1 - read;
+    ++step_count;
+    visits += n_own;
   }
 
   // Enqueue k steps starting from parity rd (direct launches) + the counter bump.
@@ -368,7 +403,13 @@ struct splbm_dev_engine {
       return;
     }
     if (p2p) {  // slab mode with NVLink peer stores
+      // the first waits of both streams: everything enqueued on the engine stream so far
+      CK(cudaEventRecord(ev_int[(comm_seq & 1) ^ 1], stream));
+      CK(cudaEventRecord(ev_bnd[(comm_seq & 1) ^ 1], stream));
       for (long k = 0; k < n; ++k) p2p_step();
+      CK(cudaStreamWaitEvent(stream, ev_bnd[(comm_seq & 1) ^ 1], 0));  // join the last planes
+      CK(splbm_dev::launch_bump(step_base, n, stream));  // keep step_base in step with step_count
+      ++launches;
       return;
     }
     long left = n;
@@ -989,6 +1030,13 @@ int splbm_dev_p2p_attach(splbm_dev_engine* e, const uint8_t* lower_blob, const u
       open(b, e->peer_pdf_up, &e->peer_flags_up);
     }
     stream_mem_ops();
+    CK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+    e->zero_base = e->alloc<long long>(1);
+    CK(cudaMemset(e->zero_base, 0, sizeof(long long)));
+    for (int k = 0; k < 2; ++k) {
+      CK(cudaEventCreateWithFlags(&e->ev_int[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&e->ev_bnd[k], cudaEventDisableTiming));
+    }
     e->p2p = true;
   });
 }
