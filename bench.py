@@ -418,6 +418,10 @@ def run_big(args):
     PDF copies in 180 GB; --single-copy, the in-place AA propagation, fits phi up to ~0.8)."""
     import paper_1703_08015_b200 as P
     peak, peak_kind = measured_peaks()
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:  # strong scaling across ranks (z-slabs)
+        from paper_1703_08015_b200 import slab
+        return slab.bench_main(args, P, clock_sampler=ClockSampler, peak=(peak, peak_kind),
+                               ras1024=True)
     t0 = time.time()
     g = P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(1024, 1024, 1024), sphere_diameter=40,
                                                           target_porosity=args.phi, seed=7),
@@ -469,7 +473,7 @@ def main():
     if args.impl == "reference":
         return run_reference_arm(args)
     if args.config == "ras1024":
-        return run_big(args)
+        return run_big(args)  # N>1 under torchrun: the slab strong-scaling run
     return run_ours(args)
 
 

@@ -8,9 +8,12 @@ and after every step exchanges the tile-face PDFs that cross its two slab faces:
   upward:   my top plane, layer a-1, directions with e_axis = +1  -> upper rank's low halo plane
   downward: my bottom plane, layer 0, directions with e_axis = -1 -> lower rank's high halo plane
 
-The transfers are NCCL point-to-point over NVLink (torch.distributed), enqueued on the engine's own
-CUDA stream so pack -> send/recv -> unpack -> next step are stream-ordered with no host sync. The
-per-node arithmetic is unchanged, so N-GPU results are bitwise equal to the 1-GPU run.
+Transports (SlabRun): "p2p" (default) — the boundary-plane step kernel stores the faces straight
+into the neighbours' halo tiles over NVLink (CUDA IPC), ordered by GPU-side 64-bit flags, on a side
+stream beside the interior planes; "nccl" — native NCCL send/recv from the engine; "torch" — this
+module's HaloExchange over torch.distributed (gloo CPU tests). Everything is stream-ordered with no
+host sync per step. The per-node arithmetic is unchanged, so N-GPU results are bitwise equal to the
+1-GPU run.
 """
 from __future__ import annotations
 
@@ -282,9 +285,11 @@ class SlabRun:
         return self.engine.sync()
 
 
-def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured")) -> int:
-    """bench.py at N>1 (torchrun): weak scaling — each rank owns a 128^3-node slab of one
-    (128 x 128 x 128*N) D3Q19 channel, tile-face halos through the fused NVLink peer stores
+def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured"), ras1024=False) -> int:
+    """bench.py at N>1 (torchrun). Default: weak scaling — each rank owns a 128^3-node slab of one
+    (128 x 128 x 128*N) D3Q19 channel. `ras1024` (bench.py --config ras1024): strong scaling of
+    BASELINE configs[4], the RAS 1024^3 (phi --phi, d 40, seed 7, periodic) split into z-slabs
+    balanced by non-empty tiles. Tile-face halos go through the fused NVLink peer stores
     (SPLBM_SLAB_TRANSPORT=nccl|torch selects the others); value = N_f*K summed over ranks / the
     max-over-ranks device time. e2e: the same through the public API with host buffers (NodeInit
     fields H2D, the steps, fields D2H), max-over-ranks wall clock. With fewer GPUs than ranks
@@ -303,11 +308,21 @@ def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured")) -> int:
                             **({"device_id": torch.device("cuda", device)}
                                if torch.cuda.device_count() >= world else {}))
     transport = os.environ.get("SPLBM_SLAB_TRANSPORT", "p2p")
-    g = P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=(128, 128, 128 * world)))
-    L = g.dims[2] // 4
-    slabs = [(r * L // world, (r + 1) * L // world) for r in range(world)]
+    if ras1024:
+        per = (1, 1, 1)
+        g = P.generate(P.GeometryKind.Ras3D, P.GenerateParams(
+            dims=(1024, 1024, 1024), sphere_diameter=40, target_porosity=args.phi, seed=7), device=device)
+        slabs = plan_slabs(plane_tile_counts(g, 4, Periodicity.of(per)), world)
+        workload = (f"configs[4] RAS 1024^3 d=40 seed 7 periodic, phi target {args.phi}, z-slabs "
+                    f"balanced by non-empty tiles")
+    else:
+        per = None
+        g = P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=(128, 128, 128 * world)))
+        L = g.dims[2] // 4
+        slabs = [(r * L // world, (r + 1) * L // world) for r in range(world)]
+        workload = f"D3Q19 BGK fp64 channel 128x128x{128 * world}, z-slab per GPU (128^3 nodes each)"
     try:
-        run = SlabRun(g, 4, P.FluidModel(tau=0.8), None, rank, world, device, slabs=slabs,
+        run = SlabRun(g, 4, P.FluidModel(tau=0.8), per, rank, world, device, slabs=slabs,
                       transport=transport)
         ok_setup = 1.0
     except Exception:  # noqa: BLE001 - e.g. no peer access between these GPUs
@@ -317,11 +332,15 @@ def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured")) -> int:
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     if flag.item() < 1.0:  # every rank falls back together: native NCCL send/recv halos
         transport = "nccl"
-        run = SlabRun(g, 4, P.FluidModel(tau=0.8), None, rank, world, device, slabs=slabs,
+        run = SlabRun(g, 4, P.FluidModel(tau=0.8), per, rank, world, device, slabs=slabs,
                       transport=transport)
     dist.barrier()  # transports up before the first step
     eng = run.engine
-    run.initialize()
+    if ras1024:
+        eng.initialize_uniform(1.0, (0.01, 0.005, 0.0))
+        dist.barrier()
+    else:
+        run.initialize()
     run.step_async(args.warmup)
     run.sync()
     start = torch.cuda.Event(enable_timing=True)
@@ -363,32 +382,33 @@ def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured")) -> int:
     # e2e through the public API with host buffers: pinned NodeInit arrays H2D, the steps, the
     # (rho, u) fields D2H into pinned rasters; wall clock, max over ranks
     n_nodes = int(eng.info.n_tiles_stored) * eng.n_tn
-    pinned = [torch.empty(n_nodes, dtype=torch.float64, pin_memory=True).numpy() for _ in range(4)]
-    pinned[0][:] = 1.0
-    for a in pinned[1:]:
-        a[:] = 0.0
-    nr = g.node_count()
-    out = P.FieldData(g.d, g.dims, torch.empty(nr, dtype=torch.uint8, pin_memory=True).numpy(),
-                      *[torch.empty(nr, dtype=torch.float64, pin_memory=True).numpy() for _ in range(4)])
-    dist.barrier()
-    t0 = time.perf_counter()
-    eng.initialize_arrays(*pinned)
-    if world > 1:
-        dist.barrier()  # neighbours store faces into my halos from their first step on
-    run.step_async(args.steps)
-    ok2, _ = run.sync()
-    eng.fields(out=out)
-    wall = max_over_ranks(time.perf_counter() - t0)
+    wall, ok2 = None, True
+    if not ras1024:  # (configs[4]: tens of GB of host fields per rank — no e2e leg)
+        pinned = [torch.empty(n_nodes, dtype=torch.float64, pin_memory=True).numpy() for _ in range(4)]
+        pinned[0][:] = 1.0
+        for a in pinned[1:]:
+            a[:] = 0.0
+        nr = g.node_count()
+        out = P.FieldData(g.d, g.dims, torch.empty(nr, dtype=torch.uint8, pin_memory=True).numpy(),
+                          *[torch.empty(nr, dtype=torch.float64, pin_memory=True).numpy() for _ in range(4)])
+        dist.barrier()
+        t0 = time.perf_counter()
+        eng.initialize_arrays(*pinned)
+        if world > 1:
+            dist.barrier()  # neighbours store faces into my halos from their first step on
+        run.step_async(args.steps)
+        ok2, _ = run.sync()
+        eng.fields(out=out)
+        wall = max_over_ranks(time.perf_counter() - t0)
     if rank == 0:
         alg = nf_local * 304.0 / (t / args.steps) / 1e9  # one rank's step kernel traffic, GB/s
         line = {
             "metric": "MLUPS (D3Q19 fp64 BGK) vs porosity; % of HBM peak GB/s; at 1/2/4/8 B200",
             "value": round(nf * args.steps / t / 1e6, 1), "unit": "MLUPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t / args.steps * 1e3, 5),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "ok": bool(all_ok and ok2),
-            "config": {"workload": f"D3Q19 BGK fp64 channel 128x128x{128 * world}, z-slab per GPU "
-                                   f"(128^3 nodes each), tile-face halos via {transport}",
+            "higher_is_better": True, "scaling": "strong" if ras1024 else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "ok": bool(all_ok and ok2),
+            "config": {"workload": f"{workload}, tile-face halos via {transport}",
                        "parallelism": f"zslab{world}", "fluid_nodes": int(nf),
                        "devices": torch.cuda.device_count(),
                        "l2": "inputs > L2 (two PDF copies of 1.3 GB per rank); no flush"},
@@ -396,10 +416,11 @@ def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured")) -> int:
                          "frac": round(alg / peak[0], 4), "peak_source": peak[1],
                          "per": "one rank (the slowest rank's time)"},
             "gpu_launches": int(launches),
-            "e2e": {"value": round(nf * args.steps / wall / 1e6, 1), "unit": "MLUPS",
-                    "h2d_bytes_per_step": round(4 * n_nodes * 8 / args.steps, 1),
-                    "d2h_bytes_per_step": round(4 * n_nodes * 8 / args.steps, 1),
-                    "steps": args.steps, "wall_s": round(wall, 4), "per": "rank 0's buffers"},
+            "e2e": None if wall is None else {
+                "value": round(nf * args.steps / wall / 1e6, 1), "unit": "MLUPS",
+                "h2d_bytes_per_step": round(4 * n_nodes * 8 / args.steps, 1),
+                "d2h_bytes_per_step": round(4 * n_nodes * 8 / args.steps, 1),
+                "steps": args.steps, "wall_s": round(wall, 4), "per": "rank 0's buffers"},
         }
         if sampler:
             line["clocks"] = sampler.summary()
