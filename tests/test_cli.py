@@ -62,3 +62,35 @@ def test_run_and_bench_on_device():
     assert rc == 0 and float(kv["bench.t2c-b200.bgk-quasi.mlups"]) > 0
     mlups = float(kv["bench.t2c-b200.bgk-incompressible.mlups"])
     assert float(kv["bench.t2c-b200.bgk-incompressible.bu"]) == pytest.approx(mlups * 1e6 * 304 / 6.537e12, rel=1e-5)
+
+
+def test_precision_and_storage_keys():
+    """sim.precision (f32|f64, the reference's parse_precision, splbm.cpp:36-40) sets the stats
+    model's s_d; sim.storage selects the single-copy engine; bad values are configuration errors."""
+    c = cli.Config({"sim.storage": "single-copy"})
+    assert cli.build_sim(c).single_copy
+    assert not cli.build_sim(cli.Config()).single_copy
+    assert cli.parse_precision(cli.Config({"sim.precision": "f32"})) == "f32"
+    with pytest.raises(P.ConfigError):
+        cli.parse_precision(cli.Config({"sim.precision": "f16"}))
+    with pytest.raises(P.ConfigError):
+        cli.build_sim(cli.Config({"sim.storage": "triple"}))
+    base = ["stats", "--set", "geometry.kind=channel3d", "--set", "geometry.dims=16 12 12"]
+    rc64, kv64 = run(base)
+    rc32, kv32 = run(base + ["--set", "sim.precision=f32"])
+    assert rc64 == rc32 == 0
+    # delta_b = ((a+2)^d s_t + (q-1) s_ti) / (n_tn phi_t B_node) doubles when s_d halves
+    assert float(kv32["t2c.delta_b"]) == pytest.approx(2 * float(kv64["t2c.delta_b"]), rel=1e-12)
+    assert run(base + ["--set", "sim.precision=f16"])[0] == cli.EXIT_CONFIG
+
+
+@pytest.mark.gpu
+def test_run_f32_and_single_copy_on_device():
+    base = ["run", "--set", "geometry.kind=cavity2d", "--set", "geometry.dims=64 64",
+            "--set", "sim.steps=50", "--set", "sim.tile=16"]
+    rc, kv = run(base)
+    rc1, kv1 = run(base + ["--set", "sim.storage=single-copy"])
+    rc2, kv2 = run(base + ["--set", "sim.precision=f32"])
+    assert rc == rc1 == rc2 == 0
+    assert kv1["mass_final"] == kv["mass_final"]  # bit-identical engines
+    assert float(kv2["mass_final"]) == pytest.approx(float(kv["mass_final"]), rel=1e-5)
