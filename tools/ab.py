@@ -2,7 +2,7 @@
 python tools/ab.py '{"name": {"ENV": "value", ...}, ...}' [case ...] [--rounds R --steps K]
 
 Every variant's engine is created with its environment settings (read at engine creation, e.g.
-SPLBM_L2PF, SPLBM_SINGLE_COPY; "LIB": "variants/lib_x.so" selects another build of the library)
+SPLBM_L2PF, SPLBM_SINGLE_COPY, SPLBM_PRECISION, SPLBM_MODEL=mrt; "LIB": "variants/lib_x.so" selects another build of the library)
 and all engines of a case stay resident; the K-step batches are then
 alternated A, B, A, B, ... for R rounds and the median per variant is reported, so box-to-box and
 thermal drift cancel out of the comparison."""
@@ -52,7 +52,9 @@ def main():
             saved_lib = _native._lib
             if "LIB" in env:  # another build of the library (e.g. variants/lib_old.so)
                 _native._lib = libs.setdefault(env["LIB"], _native.load(os.path.join(ROOT, env["LIB"])))
-            e = P.TileEngineT2C(g, 16 if case.endswith("_a16") else 4, P.FluidModel(tau=0.8), per,
+            coll = P.CollisionKind.MRT if os.environ.get("SPLBM_MODEL") == "mrt" else P.CollisionKind.BGK
+            e = P.TileEngineT2C(g, 16 if case.endswith("_a16") else 4,
+                                P.FluidModel(collision=coll, tau=0.8), per,
                                 single_copy=single, precision=prec)
             _native._lib = saved_lib
             for k, v in saved.items():
