@@ -27,10 +27,15 @@ UNIT = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "msecond": 1e3, "
 
 
 def read(path):
+    """path[@k]: the k-th profiled launch of the report (default the first)."""
+    k = 0
+    if "@" in path:
+        path, k = path.rsplit("@", 1)
+        k = int(k)
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    h, u, v = rows[0], rows[1], rows[2]
+    h, u, v = rows[0], rows[1], rows[2 + k]
     rec = {"kernel": v[h.index("Kernel Name")]}
     for k, m in KEYS.items():
         if m in h:

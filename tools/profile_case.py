@@ -28,7 +28,8 @@ if __name__ == "__main__":
         sys.exit(0)
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 6
     g, a, per = CASES[name]()
-    e = P.TileEngineT2C(g, a, P.FluidModel(tau=0.8), per,
+    coll = P.CollisionKind.MRT if os.environ.get("SPLBM_MODEL") == "mrt" else P.CollisionKind.BGK
+    e = P.TileEngineT2C(g, a, P.FluidModel(collision=coll, tau=0.8), per,
                         single_copy=os.environ.get("SPLBM_SINGLE_COPY") == "1",
                         precision=os.environ.get("SPLBM_PRECISION", "f64"))
     e.initialize_uniform(1.0, (0.01, 0.0, 0.0))

@@ -8,7 +8,9 @@ from collections import defaultdict
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PR = os.path.join(ROOT, "profiles")
 ALG = {"channel3d_128": 2032128 * 304, "ras256_phi05": 8540134 * 304,
-       "ras256_phi02": 3513249 * 304, "cavity2d_4096_a4": 16764930 * 144}
+       "ras256_phi02": 3513249 * 304, "cavity2d_4096_a4": 16764930 * 144,
+       "channel3d_128_f32": 2032128 * 152, "channel3d_128_mrt": 2032128 * 304,
+       "channel3d_128_aa_phase1": 2032128 * 304, "channel3d_128_aa_phase2": 2032128 * 304}
 
 
 def launches():
