@@ -5,7 +5,7 @@
 // tile node types and the 27-neighbour table, derives the per-node gather words on the device
 // and allocates the two PDF copies. step() enqueues fused step kernels on the engine stream
 // (batches are replayed from cached CUDA graphs) and reads back one 8-byte failure stamp per
-// batch. fields() computes moments on the device and scatters them to the raster on the host.
+// batch. fields() assembles the raster FieldData frame on the device and copies it to the caller.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <unistd.h>
@@ -98,6 +98,12 @@ struct splbm_dev_engine {
   int* halo_dirs = nullptr;  // [0..4] ez=+1 set, [5..9] ez=-1 set (or 3+3 in 2D)
   int n_halo_dirs = 0;
   double* scratch = nullptr;
+  uint64_t scratch_count = 0;  // doubles in `scratch`
+  // device FieldData frame (splbm_dev_fields), built on the first fields() call
+  uint32_t* cells = nullptr;            // cell index of each owned tile
+  std::vector<uint64_t> layer_first;    // owned tile index of the first tile at layer >= L
+  uint8_t* frame = nullptr;             // rho, ux, uy, uz (double) + mask (byte) for one chunk
+  uint64_t frame_nodes = 0;             // raster nodes per chunk
   std::vector<double> mrt_K;  // MRT operator (host copy; passed to the kernels by value), empty = BGK
   uint64_t device_bytes = 0;
   uint32_t l2pf = 0;  // step kernel L2 prefetch distance in CTAs (StepArgs::l2pf)
@@ -174,7 +180,8 @@ struct splbm_dev_engine {
                     static_cast<void*>(info), static_cast<void*>(nb), static_cast<void*>(failed),
                     static_cast<void*>(step_base), static_cast<void*>(domain_err),
                     static_cast<void*>(zero_base),
-                    static_cast<void*>(halo_dirs), static_cast<void*>(scratch)})
+                    static_cast<void*>(halo_dirs), static_cast<void*>(scratch),
+                    static_cast<void*>(cells), static_cast<void*>(frame)})
       if (p) cudaFree(p);
     if (pinned) cudaFreeHost(pinned);
     if (ev0) cudaEventDestroy(ev0);
@@ -531,7 +538,9 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
   e->failed = e->alloc<unsigned long long>(1);
   e->step_base = e->alloc<long long>(1);
   e->domain_err = e->alloc<int>(1);
-  e->scratch = e->alloc<double>(std::max<uint64_t>(4 * std::min<uint64_t>(kChunkNodes, std::max<uint64_t>(S * n_tn, 1)), e->tile_stride()));
+  e->scratch_count = std::max<uint64_t>({4 * std::min<uint64_t>(kChunkNodes, std::max<uint64_t>(S * n_tn, 1)),
+                                          e->tile_stride(), 8ull * n_tn});
+  e->scratch = e->alloc<double>(e->scratch_count);
   if (desc->collision == 1) {  // MRT
     e->mrt_K = mrt_kernel(d, desc->tau, desc->mrt_rates);
   } else if (desc->collision != 0) {
@@ -769,7 +778,6 @@ int splbm_dev_fields(splbm_dev_engine* e, double* rho, double* ux, double* uy, d
     checked(e);
     const int* dims = e->tm.dims;
     const std::size_t n = static_cast<std::size_t>(dims[0]) * dims[1] * dims[2];
-    // FieldData frame: zeros, mask at non-solid nodes (engine.hpp:516-534)
     std::vector<double> own_rho;
     std::vector<uint8_t> own_mask;
     if (mass_out && !rho) {
@@ -780,55 +788,86 @@ int splbm_dev_fields(splbm_dev_engine* e, double* rho, double* ux, double* uy, d
       own_mask.resize(n);
       mask = own_mask.data();
     }
+    // The FieldData frame (engine.hpp:516-534: zeros, the moments and mask at non-solid nodes) is
+    // assembled on the device in raster order, a chunk of tile layers (z in 3D, y in 2D: the
+    // slowest axis of the compact tile order, tiling.cpp:113-141) at a time, and copied straight
+    // into the caller's arrays. Layers without owned tiles are zeroed on the host.
+    const int a = e->a, d = e->d;
+    const int* gd = e->tm.grid_dims;
+    const int n_layers = d == 3 ? gd[2] : gd[1];
+    const uint64_t plane = d == 3 ? static_cast<uint64_t>(dims[0]) * dims[1] : static_cast<uint64_t>(dims[0]);
+    const uint64_t layer_nodes = static_cast<uint64_t>(a) * plane;
+    if (!e->frame) {
+      std::vector<uint32_t> cells(std::max<uint64_t>(e->n_own, 1));
+      e->layer_first.assign(n_layers + 1, e->n_own);
+      const int az = d == 3 ? a : 1;
+      for (uint64_t i = e->n_own; i-- > 0;) {
+        const int32_t* o = &e->tm.origins[3 * (e->g_own0 + i)];
+        const uint64_t c = static_cast<uint64_t>(o[0] / a) +
+                           static_cast<uint64_t>(gd[0]) * (o[1] / a + static_cast<uint64_t>(gd[1]) * (o[2] / az));
+        if (c > 0xffffffffull) throw config_error("fields: more than 2^32 tile cells");
+        cells[i] = static_cast<uint32_t>(c);
+        const int layer = d == 3 ? o[2] / az : o[1] / a;
+        e->layer_first[layer] = i;
+      }
+      for (int L = n_layers; L-- > 0;)  // layers without tiles start where the next layer does
+        e->layer_first[L] = std::min(e->layer_first[L], e->layer_first[L + 1]);
+      e->cells = e->alloc<uint32_t>(cells.size());
+      CK(cudaMemcpy(e->cells, cells.data(), cells.size() * 4, cudaMemcpyHostToDevice));
+      constexpr uint64_t kFrameBytes = 256ull << 20;
+      const uint64_t layers = std::max<uint64_t>(1, std::min<uint64_t>(n_layers, kFrameBytes / (33 * layer_nodes)));
+      e->frame_nodes = std::min<uint64_t>(layers * layer_nodes, n);
+      e->frame = e->alloc<uint8_t>(33 * e->frame_nodes);
+    }
+    const int per_chunk = static_cast<int>(std::max<uint64_t>(1, e->frame_nodes / layer_nodes));
     double* out[4] = {rho, ux, uy, uz};
-    parallel_for(n, [&](std::size_t b, std::size_t en) {
-      for (int c = 0; c < 4; ++c)
-        if (out[c]) std::memset(out[c] + b, 0, (en - b) * 8);
-      if (mask) std::memset(mask + b, 0, en - b);
-    }, 1u << 20);
     CK(cudaMemsetAsync(e->domain_err, 0, sizeof(int), e->stream));
-    const int a = e->a, n_tn = e->n_tn;
-    const uint64_t first = e->n_low * n_tn, total = e->n_own * n_tn;
-    const uint64_t chunk = std::max<uint64_t>(n_tn, (kChunkNodes / n_tn) * n_tn);  // whole tiles
-    double* stage = e->host_stage(4 * std::min(chunk, std::max<uint64_t>(total, 1)));
-    for (uint64_t k0 = 0; k0 < total; k0 += chunk) {
-      const uint64_t cnt = std::min(chunk, total - k0);
-      splbm_dev::MomentsArgs ma{};
-      ma.pdf = e->cur_pdf();
-      ma.view = e->view();
-      ma.info = e->info;
-      ma.rho = e->scratch;
-      ma.ux = e->scratch + cnt;
-      ma.uy = e->scratch + 2 * cnt;
-      ma.uz = e->scratch + 3 * cnt;
-      ma.node0 = first + k0;
-      ma.count = cnt;
-      ma.n_tn = n_tn;
-      ma.domain_error = e->domain_err;
-      CK(splbm_dev::launch_moments(e->d, e->incompressible != 0, e->f32, ma, e->stream));
+    for (int L0 = 0; L0 < n_layers; L0 += per_chunk) {
+      const int L1 = std::min(n_layers, L0 + per_chunk);
+      const uint64_t base = L0 * layer_nodes, cnt = std::min<uint64_t>(n, L1 * layer_nodes) - base;
+      const uint64_t i0 = e->layer_first[L0], i1 = e->layer_first[L1];
+      if (i0 == i1) {  // no owned tiles: a zero slice
+        parallel_for(cnt, [&](std::size_t b, std::size_t en) {
+          for (double* o : out)
+            if (o) std::memset(o + base + b, 0, (en - b) * 8);
+          if (mask) std::memset(mask + base + b, 0, en - b);
+        }, 1u << 20);
+        continue;
+      }
+      const uint64_t fn = e->frame_nodes;
+      double* fr = reinterpret_cast<double*>(e->frame);
+      uint8_t* fm = e->frame + 32 * fn;
+      for (int c = 0; c < 4; ++c)
+        if (out[c]) CK(cudaMemsetAsync(fr + c * fn, 0, cnt * 8, e->stream));
+      if (mask) CK(cudaMemsetAsync(fm, 0, cnt, e->stream));
+      splbm_dev::FrameArgs fa{};
+      fa.pdf = e->cur_pdf();
+      fa.info = e->info;
+      fa.view = e->view();
+      fa.cells = e->cells + i0;
+      fa.tile0 = e->n_low + i0;
+      fa.n_tiles = i1 - i0;
+      fa.n_tn = e->n_tn;
+      fa.a = a;
+      fa.gx = gd[0];
+      fa.gy = gd[1];
+      for (int k = 0; k < 3; ++k) fa.dims[k] = dims[k];
+      fa.base = base;
+      fa.rho = rho ? fr : nullptr;
+      fa.ux = ux ? fr + fn : nullptr;
+      fa.uy = uy ? fr + 2 * fn : nullptr;
+      fa.uz = uz ? fr + 3 * fn : nullptr;
+      fa.mask = mask ? fm : nullptr;
+      fa.domain_error = e->domain_err;
+      CK(splbm_dev::launch_frame(d, e->incompressible != 0, e->f32, fa, e->stream));
       ++e->launches;
-      CK(cudaMemcpyAsync(stage, e->scratch, 4 * cnt * 8, cudaMemcpyDeviceToHost, e->stream));
-      CK(cudaStreamSynchronize(e->stream));
-      const uint64_t s0 = (first + k0) / n_tn;  // first stored tile of the chunk
-      parallel_for(cnt / n_tn, [&](std::size_t b, std::size_t en) {
-        for (std::size_t tl = b; tl < en; ++tl) {
-          const uint64_t g = e->g_own0 + (s0 + tl - e->n_low);
-          const int32_t* o = &e->tm.origins[3 * g];
-          const uint8_t* tt = &e->tm.types[g * n_tn];
-          for (int p = 0; p < n_tn; ++p) {
-            if (tt[p] == 0) continue;
-            const int x = o[0] + p % a, y = o[1] + (p / a) % a, z = o[2] + (e->d == 3 ? p / (a * a) : 0);
-            const std::size_t node = raster_index(dims, x, y, z);
-            const std::size_t k = tl * n_tn + p;
-            for (int c = 0; c < 4; ++c)
-              if (out[c]) out[c][node] = stage[c * cnt + k];
-            if (mask) mask[node] = 1;
-          }
-        }
-      }, 256);
+      for (int c = 0; c < 4; ++c)
+        if (out[c]) CK(cudaMemcpyAsync(out[c] + base, fr + c * fn, cnt * 8, cudaMemcpyDeviceToHost, e->stream));
+      if (mask) CK(cudaMemcpyAsync(mask + base, fm, cnt, cudaMemcpyDeviceToHost, e->stream));
     }
     int flag = 0;
-    CK(cudaMemcpy(&flag, e->domain_err, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(&flag, e->domain_err, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
     if (flag) throw domain_error("moments: zero density under the quasi-compressible model");
     if (mass_out) {  // FieldData::total_mass, sequential raster order (fields.hpp:25-31)
       double m = 0.0;

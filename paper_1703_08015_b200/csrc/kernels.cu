@@ -664,6 +664,41 @@ __global__ void moments_kernel(MomentsArgs args) {
   args.uz[k] = static_cast<double>(m2);
 }
 
+template <int D, bool INC, class R>
+__global__ void __launch_bounds__(256) frame_kernel(FrameArgs args) {
+  constexpr int Q = Lat<D>::Q;
+  const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= args.n_tiles * args.n_tn) return;
+  const uint64_t t = args.tile0 + k / args.n_tn;
+  const int p = static_cast<int>(k % args.n_tn);
+  const uint64_t node = t * args.n_tn + p;
+  const uint32_t inf = args.info[node];
+  if (((inf >> 24) & 3) == 0) return;
+  const uint32_t c = args.cells[k / args.n_tn];
+  const int a = args.a;
+  const int x = static_cast<int>(c % args.gx) * a + p % a;
+  const int y = static_cast<int>((c / args.gx) % args.gy) * a + (p / a) % a;
+  const int z = D == 3 ? static_cast<int>(c / (static_cast<uint32_t>(args.gx) * args.gy)) * a + p / (a * a) : 0;
+  const uint64_t o = static_cast<uint64_t>(x) +
+                     static_cast<uint64_t>(args.dims[0]) * (y + static_cast<uint64_t>(args.dims[1]) * z) - args.base;
+  R f[Q];
+  load_state<D>(static_cast<const R*>(args.pdf), inf, args.view, args.n_tn, t, p, f);
+  const R r = density<D>(f);
+  R m0 = momentum<D, 0>(f), m1 = momentum<D, 1>(f), m2 = momentum<D, 2>(f);
+  if (!INC) {
+    if (r == R(0)) {
+      atomicOr(args.domain_error, 1);  // lattice.hpp:105-108
+    } else {
+      divide3(m0, m1, m2, r);
+    }
+  }
+  if (args.rho) args.rho[o] = static_cast<double>(r);
+  if (args.ux) args.ux[o] = static_cast<double>(m0);
+  if (args.uy) args.uy[o] = static_cast<double>(m1);
+  if (args.uz) args.uz[o] = static_cast<double>(m2);
+  if (args.mask) args.mask[o] = 1;
+}
+
 // ---------------------------------------------------------------------------------------------
 // Deterministic reduction over owned non-solid nodes: fixed per-block tree, then one block.
 // Moments in the engine's type, accumulated in double.
@@ -937,6 +972,14 @@ struct MomentsL {
   }
 };
 template <int D, bool INC, class R>
+struct FrameL {
+  static cudaError_t run(const FrameArgs& a, cudaStream_t st) {
+    const unsigned blocks = static_cast<unsigned>((a.n_tiles * a.n_tn + 255) / 256);
+    if (blocks) frame_kernel<D, INC, R><<<blocks, 256, 0, st>>>(a);
+    return cudaGetLastError();
+  }
+};
+template <int D, bool INC, class R>
 struct ReduceL {
   static cudaError_t run(const ReduceArgs& a, int blocks, double* out, cudaStream_t st) {
     reduce_partial_kernel<D, INC, R><<<blocks, kThreads, 0, st>>>(a);
@@ -984,6 +1027,10 @@ cudaError_t launch_init(int d, bool inc, bool f32, const InitArgs& a, cudaStream
 
 cudaError_t launch_moments(int d, bool inc, bool f32, const MomentsArgs& a, cudaStream_t st) {
   return dispatch<MomentsL>(d, inc, f32, a, st);
+}
+
+cudaError_t launch_frame(int d, bool inc, bool f32, const FrameArgs& a, cudaStream_t st) {
+  return dispatch<FrameL>(d, inc, f32, a, st);
 }
 
 cudaError_t launch_reduce(int d, bool inc, bool f32, const ReduceArgs& a, int blocks, double* out,

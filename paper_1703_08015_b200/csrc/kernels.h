@@ -96,6 +96,27 @@ struct MomentsArgs {
   int* domain_error;
 };
 
+// FieldData frame (engine.hpp:516-534) written on the device: moments of stored tiles
+// [tile0, tile0 + n_tiles) scattered to raster order, relative to raster node `base`. The frame
+// slice must be zero-filled beforehand; solid and padding nodes are left untouched.
+struct FrameArgs {
+  const void* pdf;
+  const uint32_t* info;
+  StateView view;
+  const uint32_t* cells;  // cell index (cx + gx (cy + gy cz)) of stored tile tile0 + i
+  uint64_t tile0, n_tiles;
+  int n_tn, a;
+  int gx, gy;
+  int dims[3];
+  uint64_t base;
+  double* rho;
+  double* ux;
+  double* uy;
+  double* uz;
+  uint8_t* mask;
+  int* domain_error;
+};
+
 struct ReduceArgs {
   const void* pdf;
   const uint32_t* info;
@@ -121,6 +142,7 @@ cudaError_t launch_bump(long long* step_base, long long by, cudaStream_t st);
 cudaError_t launch_node_info(int d, const NodeInfoArgs& a, cudaStream_t st);
 cudaError_t launch_init(int d, bool inc, bool f32, const InitArgs& a, cudaStream_t st);
 cudaError_t launch_moments(int d, bool inc, bool f32, const MomentsArgs& a, cudaStream_t st);
+cudaError_t launch_frame(int d, bool inc, bool f32, const FrameArgs& a, cudaStream_t st);
 cudaError_t launch_reduce(int d, bool inc, bool f32, const ReduceArgs& a, int blocks, double* out,
                           cudaStream_t st);
 cudaError_t launch_halo(int d, const HaloArgs& a, cudaStream_t st);
