@@ -15,9 +15,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsplbm_b200.so")
 BUILD = os.path.join(ROOT, "build", "native")
-SOURCES = ["kernels.cu", "engine.cpp", "tiling.cpp", "geometry.cpp", "geometry_gpu.cu", "nccl_api.cpp",
+SOURCES = ["kernels.cu", "engine.cpp", "tiling.cpp", "tiling_gpu.cu", "geometry.cpp", "geometry_gpu.cu", "nccl_api.cpp",
            "mrt.cpp"]
-HEADERS = ["kernels.h", "lattice.cuh", "common.h", "tiling.h", "nccl_api.h", "mrt.h"]
+HEADERS = ["kernels.h", "lattice.cuh", "common.h", "tiling.h", "tiling_gpu.h", "nccl_api.h", "mrt.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",

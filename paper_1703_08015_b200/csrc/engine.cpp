@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -25,6 +26,7 @@
 #include "mrt.h"
 #include "nccl_api.h"
 #include "tiling.h"
+#include "tiling_gpu.h"
 
 using namespace splbm_host;
 
@@ -80,7 +82,9 @@ struct splbm_dev_engine {
   int d = 3, q = 19, a = 4, n_tn = 64, periodic = 0, incompressible = 0, device = 0;
   double tau = 1.0, inv_tau = 1.0;
   splbm_dev::BcParams bc{0, 0, 0, 1};
-  TileMap tm;  // global tile cover
+  TileMap tm;  // global tile cover (GPU-built engines: vectors filled on first use, host_tm())
+  splbm_dev::TileBuildOut tb;  // GPU tile builder outputs not yet downloaded into tm
+  uint64_t tb_bytes = 0;
   // slab (stored = [low halo][owned][high halo], each in compact order)
   int slab_axis = 2, slab_z0 = 0, slab_z1 = 0;
   uint64_t n_low = 0, n_own = 0, n_high = 0, n_stored = 0;
@@ -176,6 +180,7 @@ struct splbm_dev_engine {
     }
     if (side) cudaStreamDestroy(side);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    splbm_dev::free_tile_build(&tb);
     for (void* p : {static_cast<void*>(pdf[0]), static_cast<void*>(pdf[1]),
                     static_cast<void*>(info), static_cast<void*>(nb), static_cast<void*>(failed),
                     static_cast<void*>(step_base), static_cast<void*>(domain_err),
@@ -444,6 +449,16 @@ splbm_dev_engine* checked(splbm_dev_engine* e) {
 
 void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
   if (!desc || !desc->types) throw config_error("null descriptor");
+  // SPLBM_BUILD_TIMING=1: per-phase wall times of the engine build on stderr
+  const bool timing = std::getenv("SPLBM_BUILD_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto phase = [&](const char* name) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[build] %-16s %8.1f ms\n", name,
+                 std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   const int d = desc->d;
   if (d != 2 && d != 3) throw config_error("dimension must be 2 or 3");
   if (!(desc->tau > 0.5)) throw config_error("relaxation time tau must be > 0.5");  // collision.cpp:90
@@ -472,42 +487,6 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
       throw config_error("single-copy propagation is a single-GPU mode (no slab)");
     e->aa = true;
   }
-  e->tm = build_tile_map(desc->types, d, dims, e->a, e->periodic);
-  TileMap& tm = e->tm;
-  e->n_tn = tm.n_tn;
-  const std::vector<uint32_t> nb_global = neighbour_table(tm);
-  const std::vector<uint8_t> deg = degenerate_mask(desc->types, d, dims, e->periodic);
-
-  // PressureBC under the quasi-compressible model needs rho_bc > 0 (lattice.hpp:76-78)
-  if (!e->incompressible && !(desc->bc_density > 0.0)) {
-    bool has_p = false;
-    for (std::size_t i = 0, n = static_cast<std::size_t>(dims[0]) * dims[1] * dims[2]; i < n && !has_p; ++i)
-      has_p = desc->types[i] == 3;
-    if (has_p) throw domain_error("equilibrium requires rho > 0 for the quasi-compressible model");
-  }
-
-  // ---- slab of tile planes along the last axis ---------------------------------
-  const SlabLayout sl = slab_layout(tm, desc->slab_z0, desc->slab_z1);
-  e->slab_axis = sl.axis;
-  e->slab_z0 = sl.z0;
-  e->slab_z1 = sl.z1;
-  e->n_low = sl.n_low;
-  e->n_own = sl.n_own;
-  e->n_high = sl.n_high;
-  e->g_low0 = sl.g_low0;
-  e->g_own0 = sl.g_own0;
-  e->g_high0 = sl.g_high0;
-  e->n_stored = sl.stored();
-  e->send_low_tiles = sl.send_low_tiles;
-  e->send_high_tiles = sl.send_high_tiles;
-  auto global_of = [&](uint64_t s) { return sl.global_of(s); };
-  const uint64_t S = e->n_stored;
-  const int n_tn = e->n_tn;
-  std::vector<uint32_t> nb_local;
-  std::vector<uint8_t> types_local;
-  slab_tables(tm, sl, nb_global, deg, nb_local, types_local);
-  for (uint64_t s = e->n_low; s < e->n_low + e->n_own; ++s) e->fluid_nodes += tm.fluid_count[global_of(s)];
-
   // ---- device ------------------------------------------------------------------------------
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -526,7 +505,79 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
     if (const char* v = std::getenv("SPLBM_PDL_MIN")) e->pdl_min_threads = std::strtoull(v, nullptr, 10);
     if (const char* v = std::getenv("SPLBM_X2")) e->x2 = std::atoi(v);
   }
+  phase("device_select");
   CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+  const bool slab_mode = desc->slab_z0 != 0 || desc->slab_z1 != 0;
+  // Whole-domain engines build the tile map on the GPU (tiling_gpu.cu; SPLBM_HOST_TILES=1 forces
+  // the host builder); slab engines use the host builder and its slab tables.
+  const bool gpu_tiles = !slab_mode && std::getenv("SPLBM_HOST_TILES") == nullptr;
+  TileMap& tm = e->tm;
+  SlabLayout sl;
+  std::vector<uint32_t> nb_local;
+  std::vector<uint8_t> types_local;
+  if (gpu_tiles) {
+    validate_tiling(d, dims, e->a, e->periodic);
+    tm.d = d;
+    tm.a = e->a;
+    tm.periodic = e->periodic;
+    for (int k = 0; k < 3; ++k) tm.dims[k] = dims[k];
+    tile_dims(d, dims, e->a, tm.grid_dims, tm.padded_dims);
+    tm.n_tn = e->a * e->a * (d == 3 ? e->a : 1);
+    const std::size_t n = static_cast<std::size_t>(dims[0]) * dims[1] * dims[2];
+    uint8_t* raster_d = nullptr;
+    CK(cudaMalloc(&raster_d, n));
+    cudaError_t err = cudaMemcpy(raster_d, desc->types, n, cudaMemcpyHostToDevice);
+    if (err == cudaSuccess)
+      err = splbm_dev::build_tiles_device(raster_d, d, dims, e->a, e->periodic, tm.grid_dims, e->stream, &e->tb);
+    cudaFree(raster_d);
+    CK(err);
+    tm.n_tiles = e->tb.n_tiles;
+    e->tb_bytes = tm.n_tiles * (12ull + 2ull * tm.n_tn) +
+                  static_cast<uint64_t>(tm.grid_dims[0]) * tm.grid_dims[1] * tm.grid_dims[2] * 4;
+    e->device_bytes += e->tb_bytes;
+    sl.axis = d == 3 ? 2 : 1;
+    sl.z1 = tm.grid_dims[sl.axis];
+    sl.n_own = tm.n_tiles;
+    e->fluid_nodes = e->tb.fluid_nodes;
+    e->n_tn = tm.n_tn;
+    phase("gpu_tiles");
+  } else {
+    tm = build_tile_map(desc->types, d, dims, e->a, e->periodic);
+    phase("tile_map");
+    e->n_tn = tm.n_tn;
+    const std::vector<uint32_t> nb_global = neighbour_table(tm);
+    phase("neighbour_table");
+    const std::vector<uint8_t> deg = degenerate_mask(desc->types, d, dims, e->periodic);
+    phase("degenerate_mask");
+    // ---- slab of tile planes along the last axis -------------------------------
+    sl = slab_layout(tm, desc->slab_z0, desc->slab_z1);
+    slab_tables(tm, sl, nb_global, deg, nb_local, types_local);
+    phase("slab_tables");
+    for (uint64_t s = sl.n_low; s < sl.n_low + sl.n_own; ++s) e->fluid_nodes += tm.fluid_count[sl.global_of(s)];
+  }
+
+  // PressureBC under the quasi-compressible model needs rho_bc > 0 (lattice.hpp:76-78)
+  if (!e->incompressible && !(desc->bc_density > 0.0)) {
+    bool has_p = false;
+    for (std::size_t i = 0, n = static_cast<std::size_t>(dims[0]) * dims[1] * dims[2]; i < n && !has_p; ++i)
+      has_p = desc->types[i] == 3;
+    if (has_p) throw domain_error("equilibrium requires rho > 0 for the quasi-compressible model");
+  }
+
+  e->slab_axis = sl.axis;
+  e->slab_z0 = sl.z0;
+  e->slab_z1 = sl.z1;
+  e->n_low = sl.n_low;
+  e->n_own = sl.n_own;
+  e->n_high = sl.n_high;
+  e->g_low0 = sl.g_low0;
+  e->g_own0 = sl.g_own0;
+  e->g_high0 = sl.g_high0;
+  e->n_stored = sl.stored();
+  e->send_low_tiles = sl.send_low_tiles;
+  e->send_high_tiles = sl.send_high_tiles;
+  const uint64_t S = e->n_stored;
+  const int n_tn = e->n_tn;
   CK(cudaEventCreate(&e->ev0));
   CK(cudaEventCreate(&e->ev1));
   const uint64_t nslots = S * e->tile_stride();
@@ -534,7 +585,13 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
   if (!e->aa) e->pdf[1] = e->alloc<char>(nslots * e->es);
   e->info = e->alloc<uint32_t>(S * n_tn);
   const int nbs = d == 3 ? 27 : 9;  // 2D keeps only the dz = 0 slice (cells 9..17)
-  e->nb = e->alloc<uint32_t>(S * nbs);
+  if (gpu_tiles) {  // the builder's table is already in the device layout
+    e->nb = e->tb.nb;
+    e->tb.nb = nullptr;
+    e->device_bytes += std::max<uint64_t>(S, 1) * nbs * 4;
+  } else {
+    e->nb = e->alloc<uint32_t>(S * nbs);
+  }
   e->failed = e->alloc<unsigned long long>(1);
   e->step_base = e->alloc<long long>(1);
   e->domain_err = e->alloc<int>(1);
@@ -561,23 +618,64 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
   CK(cudaMemsetAsync(e->step_base, 0, sizeof(long long), e->stream));
   CK(cudaMemsetAsync(e->pdf[0], 0, nslots * e->es, e->stream));
   if (e->pdf[1]) CK(cudaMemsetAsync(e->pdf[1], 0, nslots * e->es, e->stream));
-  if (d == 2) {
-    std::vector<uint32_t> nb2(S * 9);
-    for (uint64_t t = 0; t < S; ++t)
-      for (int k = 0; k < 9; ++k) nb2[t * 9 + k] = nb_local[t * 27 + 9 + k];
-    nb_local.swap(nb2);
+  if (!gpu_tiles) {
+    if (d == 2) {
+      std::vector<uint32_t> nb2(S * 9);
+      for (uint64_t t = 0; t < S; ++t)
+        for (int k = 0; k < 9; ++k) nb2[t * 9 + k] = nb_local[t * 27 + 9 + k];
+      nb_local.swap(nb2);
+    }
+    CK(cudaMemcpyAsync(e->nb, nb_local.data(), nb_local.size() * 4, cudaMemcpyHostToDevice, e->stream));
   }
-  CK(cudaMemcpyAsync(e->nb, nb_local.data(), nb_local.size() * 4, cudaMemcpyHostToDevice, e->stream));
   {
-    uint8_t* types_d = nullptr;
-    CK(cudaMalloc(&types_d, std::max<std::size_t>(types_local.size(), 1)));
-    CK(cudaMemcpyAsync(types_d, types_local.data(), types_local.size(), cudaMemcpyHostToDevice, e->stream));
+    uint8_t* types_d = e->tb.types_bc;
+    if (!gpu_tiles) {
+      CK(cudaMalloc(&types_d, std::max<std::size_t>(types_local.size(), 1)));
+      CK(cudaMemcpyAsync(types_d, types_local.data(), types_local.size(), cudaMemcpyHostToDevice, e->stream));
+    }
     splbm_dev::NodeInfoArgs ni{types_d, e->nb, e->info, S, e->a, 32 / e->es};
     CK(splbm_dev::launch_node_info(d, ni, e->stream));
     ++e->launches;
     CK(cudaStreamSynchronize(e->stream));
     cudaFree(types_d);
+    if (gpu_tiles) {
+      e->tb.types_bc = nullptr;
+      e->device_bytes -= S * n_tn;
+      e->tb_bytes -= S * n_tn;
+    }
   }
+  phase("device_tables");
+}
+
+// GPU-built engines keep the tile cover on the device until a caller needs the host TileMap
+// (tile-grid export, fields); then it is downloaded once and the device copies are released.
+void host_tm(splbm_dev_engine* e) {
+  if (!e->tb.tile_map) return;
+  TileMap& tm = e->tm;
+  const uint64_t T = tm.n_tiles;
+  const uint64_t C = static_cast<uint64_t>(tm.grid_dims[0]) * tm.grid_dims[1] * tm.grid_dims[2];
+  tm.tile_map.resize(C);
+  tm.origins.resize(T * 3);
+  tm.fluid_count.resize(T);
+  tm.types.resize(T * tm.n_tn);
+  std::vector<uint32_t> cell(T);
+  CK(cudaMemcpy(tm.tile_map.data(), e->tb.tile_map, C * 4, cudaMemcpyDeviceToHost));
+  if (T) {
+    CK(cudaMemcpy(cell.data(), e->tb.cell_of, T * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(tm.fluid_count.data(), e->tb.fluid_count, T * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(tm.types.data(), e->tb.types, T * tm.n_tn, cudaMemcpyDeviceToHost));
+  }
+  const int* gd = tm.grid_dims;
+  const int az = tm.d == 3 ? tm.a : 1;
+  for (uint64_t t = 0; t < T; ++t) {
+    const uint64_t c = cell[t];
+    tm.origins[3 * t] = static_cast<int32_t>(c % gd[0]) * tm.a;
+    tm.origins[3 * t + 1] = static_cast<int32_t>((c / gd[0]) % gd[1]) * tm.a;
+    tm.origins[3 * t + 2] = static_cast<int32_t>(c / (static_cast<uint64_t>(gd[0]) * gd[1])) * az;
+  }
+  splbm_dev::free_tile_build(&e->tb);
+  e->device_bytes -= e->tb_bytes;
+  e->tb_bytes = 0;
 }
 
 void check_domain_flag(splbm_dev_engine* e, const char* msg) {
@@ -641,6 +739,8 @@ int splbm_dev_get_tile_grid(const splbm_dev_engine* e, uint32_t* tile_map, int32
                             uint8_t* tile_types, uint32_t* fluid_count, uint32_t* nb) {
   return guarded([&] {
     if (!e) throw config_error("null engine");
+    CK(cudaSetDevice(e->device));
+    host_tm(const_cast<splbm_dev_engine*>(e));
     const TileMap& tm = e->tm;
     if (tile_map) std::memcpy(tile_map, tm.tile_map.data(), tm.tile_map.size() * 4);
     if (origins) std::memcpy(origins, tm.origins.data(), tm.origins.size() * 4);
@@ -798,6 +898,7 @@ int splbm_dev_fields(splbm_dev_engine* e, double* rho, double* ux, double* uy, d
     const uint64_t plane = d == 3 ? static_cast<uint64_t>(dims[0]) * dims[1] : static_cast<uint64_t>(dims[0]);
     const uint64_t layer_nodes = static_cast<uint64_t>(a) * plane;
     if (!e->frame) {
+      host_tm(e);
       std::vector<uint32_t> cells(std::max<uint64_t>(e->n_own, 1));
       e->layer_first.assign(n_layers + 1, e->n_own);
       const int az = d == 3 ? a : 1;
