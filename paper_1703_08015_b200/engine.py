@@ -195,10 +195,10 @@ class TileEngineT2C:
         else:
             rho, ux, uy, uz = (np.empty(n) for _ in range(4))
             mask = np.empty(n, np.uint8)
-        mass = C.c_double()
+        mass = C.c_double()  # the sequential host mass sum only when asked for
         _native.check(self._L.splbm_dev_fields(self._h, _native.ptr(rho), _native.ptr(ux),
                                                _native.ptr(uy), _native.ptr(uz),
-                                               _native.ptr(mask), C.byref(mass)))
+                                               _native.ptr(mask), C.byref(mass) if with_mass else None))
         f = FieldData(self.d, self.geometry_dims, mask, rho, ux, uy, uz)
         return (f, mass.value) if with_mass else f
 
