@@ -20,6 +20,7 @@ CASES = {
     "ras256_phi02": lambda: (P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(256, 256, 256), sphere_diameter=40, target_porosity=0.2, seed=7)), 7),
     "ras256_phi05": lambda: (P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(256, 256, 256), sphere_diameter=40, target_porosity=0.5, seed=7)), 7),
     "full256": lambda: (P.Geometry.filled(3, (256, 256, 256)), 7),
+    "channel64": lambda: (P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=(64, 64, 64))), 0),  # L2-resident
     "cavity2d_4096_a4": lambda: (P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(4096, 4096, 1))), 0),
     "cavity2d_256_a4": lambda: (P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(256, 256, 1))), 0),
     "cavity2d_256_a16": lambda: (P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(256, 256, 1))), 0),
