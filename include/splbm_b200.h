@@ -259,6 +259,8 @@ int splbm_mrt_kernel(int d, double tau, const double* rates, double* K_out);
 /* Runs the step kernel's velocity division u_k = m_k / rho (collision.hpp:48) on the device for n
  * (m0, m1, m2, rho) tuples; every quotient must equal IEEE division bit for bit. */
 int splbm_selftest_divide(uint64_t n, const double* m3, const double* rho, double* out3);
+/* The same for the f32 engine (TileEngineT2C<float>): IEEE binary32 division, bit for bit. */
+int splbm_selftest_divide_f32(uint64_t n, const float* m3, const float* rho, float* out3);
 
 #ifdef __cplusplus
 }

@@ -108,6 +108,7 @@ SIGNATURES = {
     "splbm_dev_comm_attach": ([_vp, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int], C.c_int),
     "splbm_dev_halo_pack_next": ([_vp, C.c_void_p, C.c_void_p], C.c_int),
     "splbm_selftest_divide": ([C.c_uint64, _dp, _dp, _dp], C.c_int),
+    "splbm_selftest_divide_f32": ([C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "splbm_mrt_kernel": ([C.c_int, C.c_double, C.c_void_p, _dp], C.c_int),
 }
 

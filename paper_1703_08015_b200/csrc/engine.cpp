@@ -1237,4 +1237,25 @@ int splbm_selftest_divide(uint64_t n, const double* m3, const double* rho, doubl
   });
 }
 
+int splbm_selftest_divide_f32(uint64_t n, const float* m3, const float* rho, float* out3) {
+  return guarded([&] {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw Error(SPLBM_ERR_CUDA, "no CUDA device available");
+    float *dm = nullptr, *dr = nullptr, *dout = nullptr;
+    const std::size_t nb = std::max<uint64_t>(n, 1) * 4;
+    CK(cudaMalloc(&dm, 3 * nb));
+    CK(cudaMalloc(&dr, nb));
+    CK(cudaMalloc(&dout, 3 * nb));
+    cudaError_t err = cudaMemcpy(dm, m3, 3 * n * 4, cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = cudaMemcpy(dr, rho, n * 4, cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = splbm_dev::launch_divide_selftest_f32(n, dm, dr, dout, nullptr);
+    if (err == cudaSuccess) err = cudaMemcpy(out3, dout, 3 * n * 4, cudaMemcpyDeviceToHost);
+    cudaFree(dm);
+    cudaFree(dr);
+    cudaFree(dout);
+    CK(err);
+  });
+}
+
 }  // extern "C"

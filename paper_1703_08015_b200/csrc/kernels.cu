@@ -817,10 +817,11 @@ __global__ void unswap_kernel(const R* pdf, const uint32_t* info, StateView v, i
 }
 
 // Self-test of the shared-reciprocal division against IEEE division (tests/test_device_division.py).
-__global__ void divide_selftest_kernel(uint64_t n, const double* m, const double* rho, double* out) {
+template <class R>
+__global__ void divide_selftest_kernel(uint64_t n, const R* m, const R* rho, R* out) {
   const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  double a = m[3 * k], b = m[3 * k + 1], c = m[3 * k + 2];
+  R a = m[3 * k], b = m[3 * k + 1], c = m[3 * k + 2];
   divide3(a, b, c, rho[k]);
   out[3 * k] = a;
   out[3 * k + 1] = b;
@@ -1046,7 +1047,14 @@ cudaError_t launch_unswap(int d, bool f32, const void* pdf, const uint32_t* info
 cudaError_t launch_divide_selftest(uint64_t n, const double* m, const double* rho, double* out,
                                    cudaStream_t st) {
   const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
-  if (blocks) divide_selftest_kernel<<<blocks, 256, 0, st>>>(n, m, rho, out);
+  if (blocks) divide_selftest_kernel<double><<<blocks, 256, 0, st>>>(n, m, rho, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_divide_selftest_f32(uint64_t n, const float* m, const float* rho, float* out,
+                                       cudaStream_t st) {
+  const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
+  if (blocks) divide_selftest_kernel<float><<<blocks, 256, 0, st>>>(n, m, rho, out);
   return cudaGetLastError();
 }
 

@@ -151,5 +151,7 @@ cudaError_t launch_unswap(int d, bool f32, const void* pdf, const uint32_t* info
                           int n_tn, uint64_t tile0, uint64_t n_tiles, void* out, cudaStream_t st);
 cudaError_t launch_divide_selftest(uint64_t n, const double* m, const double* rho, double* out,
                                    cudaStream_t st);
+cudaError_t launch_divide_selftest_f32(uint64_t n, const float* m, const float* rho, float* out,
+                                       cudaStream_t st);
 
 }  // namespace splbm_dev
