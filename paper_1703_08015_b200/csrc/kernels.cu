@@ -353,7 +353,7 @@ __global__ void __launch_bounds__((step_threads<D, (D == 3 ? (1 << (3 * LOGA)) :
 // and j + NTN/2 and issues both gathers (2 x q loads) before either collision: +7-13 % over one
 // node per thread (interleaved A/B). Same addressing, slots and arithmetic as
 // t2c_step_pow2_kernel (BGK, no slab peer stores).
-template <int D, int LOGA, bool INC, class R>
+template <int D, int LOGA, bool INC, class R, bool O32>
 __global__ void __launch_bounds__(SPLBM_X2_THREADS, SPLBM_X2_MINB)
     t2c_step_x2_kernel(StepArgs args, const __grid_constant__ MrtMatrix<R, 1> mrt) {
   constexpr int Q = Lat<D>::Q;
@@ -364,7 +364,8 @@ __global__ void __launch_bounds__(SPLBM_X2_THREADS, SPLBM_X2_MINB)
   constexpr int TILES = SPLBM_X2_THREADS / HALF;
   constexpr uint64_t STRIDE = static_cast<uint64_t>(Q) * NTN;
   constexpr int NBS = nb_stride<D>();
-  __shared__ const R* s_base[TILES][NBS];
+  __shared__ const R* s_base[TILES][O32 ? 1 : NBS];
+  __shared__ uint32_t s_off[TILES][O32 ? NBS : 1];  // O32: neighbour tile offsets in elements
 
   const uint64_t n_tiles = args.n_nodes / NTN;
   const uint64_t tile_blk = static_cast<uint64_t>(blockIdx.x) * TILES;
@@ -375,8 +376,9 @@ __global__ void __launch_bounds__(SPLBM_X2_THREADS, SPLBM_X2_MINB)
     if (tt < n_tiles) {
       const uint32_t s = __ldg(args.nb + (args.t0 + tt) * NBS + dd);
       b = s == kEmpty ? nullptr : rd + static_cast<uint64_t>(s) * STRIDE;
+      if constexpr (O32) s_off[tl][dd] = s == kEmpty ? 0u : s * static_cast<uint32_t>(STRIDE);
     }
-    s_base[tl][dd] = b;
+    if constexpr (!O32) s_base[tl][dd] = b;
   }
   const int tl = threadIdx.x / HALF;
   const int j = threadIdx.x % HALF;
@@ -394,6 +396,7 @@ __global__ void __launch_bounds__(SPLBM_X2_THREADS, SPLBM_X2_MINB)
 #endif
   l2_prefetch_blocks<Q, NTN, TILES>(rd, args.t0 + pf, args.l2pf && pf < n_tiles);
   const R* own = rd + t * STRIDE;
+  const uint32_t own_off = static_cast<uint32_t>(t * STRIDE);
   const R* const* nbp = s_base[tl];
   R f[2][Q];
 #pragma unroll
@@ -411,9 +414,15 @@ __global__ void __launch_bounds__(SPLBM_X2_THREADS, SPLBM_X2_MINB)
       const int dz = (D == 3 && ez<D>(i)) ? (vz >> LOGA) : 0;
       const int sp = (vx & (A - 1)) | ((vy & (A - 1)) << LOGA) | (D == 3 ? ((vz & (A - 1)) << (2 * LOGA)) : 0);
       const int delta = 13 + dx + 3 * dy + 9 * dz;
-      const R* src = (delta == 13 ? own : nbp[delta - nb_offset<D>()]) + (i * NTN + sp);
-      const R* bb = own + (opp(i) * NTN + p);
-      f[u][i] = act ? ld_pdf(((info[u] >> i) & 1u) ? bb : src) : R(0);
+      if constexpr (O32) {  // 32-bit element offsets: one select and one wide add per load
+        const uint32_t so = (delta == 13 ? own_off : s_off[tl][delta - nb_offset<D>()]) + (i * NTN + sp);
+        const uint32_t bo = own_off + (opp(i) * NTN + p);
+        f[u][i] = act ? ld_pdf(rd + (((info[u] >> i) & 1u) ? bo : so)) : R(0);
+      } else {
+        const R* src = (delta == 13 ? own : nbp[delta - nb_offset<D>()]) + (i * NTN + sp);
+        const R* bb = own + (opp(i) * NTN + p);
+        f[u][i] = act ? ld_pdf(((info[u] >> i) & 1u) ? bb : src) : R(0);
+      }
     }
   }
   R* wr0 = static_cast<R*>(args.write) + t * STRIDE + j;
@@ -901,7 +910,10 @@ static void launch_pow2(const StepArgs& a, cudaStream_t st) {
     if (a.x2 && a.skip_by == 0) {  // f32: two nodes per thread
       constexpr int XT = SPLBM_X2_THREADS / (NTN / 2);
       const unsigned xb = static_cast<unsigned>((tiles + XT - 1) / XT);
-      launch_maybe_pdl(t2c_step_x2_kernel<D, LOGA, INC, R>, xb, st, a, none, SPLBM_X2_THREADS);
+      if (a.off32)
+        launch_maybe_pdl(t2c_step_x2_kernel<D, LOGA, INC, R, true>, xb, st, a, none, SPLBM_X2_THREADS);
+      else
+        launch_maybe_pdl(t2c_step_x2_kernel<D, LOGA, INC, R, false>, xb, st, a, none, SPLBM_X2_THREADS);
       return;
     }
   }

@@ -35,6 +35,7 @@ struct StepArgs {
   int aa;
   uint64_t pdl_min_threads;  // programmatic dependent launch from this grid size on
   int x2;  // f32 power-of-two BGK step: two nodes per thread (t2c_step_x2_kernel)
+  int off32;  // every stored slot index fits 32 bits: 32-bit gather offsets (x2 kernel)
   // Slab mode, NVLink peer stores (power-of-two tile kernel only): the face layer of my top
   // plane tiles [top_begin, ...) is also stored, for the directions leaving upwards, into the
   // upper neighbour's next copy at its low halo tiles (peer_up = that copy's first halo tile);
