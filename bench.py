@@ -402,9 +402,9 @@ def run_ours(args):
     }
     del eng
     if not args.no_sweep:
-        line["porosity_sweep"] = porosity_sweep(P, min(K, 50), max(W, 3), peak)
+        line["porosity_sweep"] = porosity_sweep(P, min(K, 64), max(W, 3), peak)  # whole 32-step graphs
     if not args.no_other:
-        line["other_configs"] = other_configs(P, min(K, 50), max(W, 3), peak)
+        line["other_configs"] = other_configs(P, min(K, 64), max(W, 3), peak)
     line["e2e"] = e2e_public_api(P, g, 1000)
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(P, dims)

@@ -118,8 +118,31 @@ __device__ __forceinline__ void divide3(double& m0, double& m1, double& m2, doub
   m1 = ddiv(m1, rho);
   m2 = ddiv(m2, rho);
 }
-// f32 engine: IEEE single division per component (__fdiv_rn)
+// f32 engine: the same shared correctly rounded reciprocal + Markstein correction in binary32
+// (the theorem is format-independent); the guard keeps every intermediate normal (|q| within
+// 2^+-100, the residual above 2^-126), anything else takes IEEE __fdiv_rn. Besides saving two
+// reciprocals, it keeps zero momenta (a domain started from rest) off __fdiv_rn's slow path.
+__device__ __forceinline__ bool div_safe(float v) {
+  const float av = fabsf(v);
+  return av == 0.0f || (av >= 0x1p-50f && av <= 0x1p50f);
+}
 __device__ __forceinline__ void divide3(float& m0, float& m1, float& m2, float rho) {
+#if SPLBM_FAST_DIV
+  const float ar = fabsf(rho);
+  if (ar >= 0x1p-50f && ar <= 0x1p50f && div_safe(m0) && div_safe(m1) && div_safe(m2)) {
+    const float y = __frcp_rn(rho);
+    auto q = [&](float m) {
+      const float q0 = __fmul_rn(m, y);
+      if (m == 0.0f) return q0;
+      const float r = __fmaf_rn(-rho, q0, m);
+      return __fmaf_rn(r, y, q0);
+    };
+    m0 = q(m0);
+    m1 = q(m1);
+    m2 = q(m2);
+    return;
+  }
+#endif
   m0 = ddiv(m0, rho);
   m1 = ddiv(m1, rho);
   m2 = ddiv(m2, rho);
