@@ -16,4 +16,5 @@ run ras48_f32 "SPLBM_PRECISION=f32" ras48_periodic
 run channel_single_copy_f32 "SPLBM_SINGLE_COPY=1 SPLBM_PRECISION=f32" channel3d_small
 run cavity2d_a16_single_copy "SPLBM_SINGLE_COPY=1" cavity2d_64_a16
 run random_a3_generic "SPLBM_PRECISION=f64" random_a3
+run ras48_mrt "SPLBM_MODEL=mrt" ras48_periodic
 run ras_device_generator "SPLBM_PRECISION=f64" ras_device_generator
