@@ -72,7 +72,7 @@ const StreamMemOps& stream_mem_ops() {
   return ops;
 }
 
-constexpr uint64_t kChunkNodes = 1ull << 22;  // init / moments staging (4 x 32 MB)
+constexpr uint64_t kChunkNodes = 1ull << 22;  // initialize_arrays staging (4 x 32 MB)
 constexpr int kGraphSteps = 32;               // steps per captured graph (even)
 
 }  // namespace
@@ -149,19 +149,6 @@ struct splbm_dev_engine {
   uint64_t peer_down_halo0 = 0;  // first high-halo tile of the lower neighbour
   unsigned long long comm_seq = 0;
   std::vector<void*> ipc_opened;
-  double* pinned = nullptr;  // host staging for fields() (page-locked, grown on demand)
-  std::size_t pinned_count = 0;
-
-  double* host_stage(std::size_t count) {
-    if (count > pinned_count) {
-      if (pinned) cudaFreeHost(pinned);
-      pinned = nullptr;
-      pinned_count = 0;
-      CK(cudaMallocHost(&pinned, count * sizeof(double)));
-      pinned_count = count;
-    }
-    return pinned;
-  }
 
   ~splbm_dev_engine() {
     if (device >= 0) cudaSetDevice(device);
@@ -189,7 +176,6 @@ struct splbm_dev_engine {
                     static_cast<void*>(halo_dirs), static_cast<void*>(scratch),
                     static_cast<void*>(cells), static_cast<void*>(frame)})
       if (p) cudaFree(p);
-    if (pinned) cudaFreeHost(pinned);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);

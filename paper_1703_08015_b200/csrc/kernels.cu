@@ -640,39 +640,8 @@ __global__ void init_kernel(InitArgs args) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// moments<T> per stored tile node (lattice.hpp:94-112), tile-node order; solid nodes -> 0; the
-// FieldData doubles are static_cast<double>(m) (engine.hpp:383-386).
-template <int D, bool INC, class R>
-__global__ void moments_kernel(MomentsArgs args) {
-  constexpr int Q = Lat<D>::Q;
-  const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= args.count) return;
-  const uint64_t node = args.node0 + k;
-  const uint64_t t = node / args.n_tn;
-  const int p = static_cast<int>(node % args.n_tn);
-  const int type = (args.info[node] >> 24) & 3;
-  R r = R(0), m0 = R(0), m1 = R(0), m2 = R(0);
-  if (type != 0) {
-    R f[Q];
-    load_state<D>(static_cast<const R*>(args.pdf), args.info[node], args.view, args.n_tn, t, p, f);
-    r = density<D>(f);
-    m0 = momentum<D, 0>(f);
-    m1 = momentum<D, 1>(f);
-    m2 = momentum<D, 2>(f);
-    if (!INC) {
-      if (r == R(0)) {
-        atomicOr(args.domain_error, 1);  // lattice.hpp:105-108
-      } else {
-        divide3(m0, m1, m2, r);
-      }
-    }
-  }
-  args.rho[k] = static_cast<double>(r);
-  args.ux[k] = static_cast<double>(m0);
-  args.uy[k] = static_cast<double>(m1);
-  args.uz[k] = static_cast<double>(m2);
-}
-
+// fields(): moments<T> (lattice.hpp:94-112) of every non-solid stored node, written as
+// static_cast<double>(m) (engine.hpp:383-386) at its raster index in the FieldData frame slice.
 template <int D, bool INC, class R>
 __global__ void __launch_bounds__(256) frame_kernel(FrameArgs args) {
   constexpr int Q = Lat<D>::Q;
@@ -977,14 +946,6 @@ struct InitL {
   }
 };
 template <int D, bool INC, class R>
-struct MomentsL {
-  static cudaError_t run(const MomentsArgs& a, cudaStream_t st) {
-    const unsigned blocks = static_cast<unsigned>((a.count + 255) / 256);
-    if (blocks) moments_kernel<D, INC, R><<<blocks, 256, 0, st>>>(a);
-    return cudaGetLastError();
-  }
-};
-template <int D, bool INC, class R>
 struct FrameL {
   static cudaError_t run(const FrameArgs& a, cudaStream_t st) {
     const unsigned blocks = static_cast<unsigned>((a.n_tiles * a.n_tn + 255) / 256);
@@ -1036,10 +997,6 @@ cudaError_t launch_node_info(int d, const NodeInfoArgs& a, cudaStream_t st) {
 
 cudaError_t launch_init(int d, bool inc, bool f32, const InitArgs& a, cudaStream_t st) {
   return dispatch<InitL>(d, inc, f32, a, st);
-}
-
-cudaError_t launch_moments(int d, bool inc, bool f32, const MomentsArgs& a, cudaStream_t st) {
-  return dispatch<MomentsL>(d, inc, f32, a, st);
 }
 
 cudaError_t launch_frame(int d, bool inc, bool f32, const FrameArgs& a, cudaStream_t st) {

@@ -84,19 +84,6 @@ struct StateView {
   int swapped;
 };
 
-struct MomentsArgs {
-  const void* pdf;
-  const uint32_t* info;
-  StateView view;
-  double* rho;
-  double* ux;
-  double* uy;
-  double* uz;
-  uint64_t node0, count;
-  int n_tn;
-  int* domain_error;
-};
-
 // FieldData frame (engine.hpp:516-534) written on the device: moments of stored tiles
 // [tile0, tile0 + n_tiles) scattered to raster order, relative to raster node `base`. The frame
 // slice must be zero-filled beforehand; solid and padding nodes are left untouched.
@@ -142,7 +129,6 @@ cudaError_t launch_step(int d, bool inc, bool f32, const StepArgs& a, cudaStream
 cudaError_t launch_bump(long long* step_base, long long by, cudaStream_t st);
 cudaError_t launch_node_info(int d, const NodeInfoArgs& a, cudaStream_t st);
 cudaError_t launch_init(int d, bool inc, bool f32, const InitArgs& a, cudaStream_t st);
-cudaError_t launch_moments(int d, bool inc, bool f32, const MomentsArgs& a, cudaStream_t st);
 cudaError_t launch_frame(int d, bool inc, bool f32, const FrameArgs& a, cudaStream_t st);
 cudaError_t launch_reduce(int d, bool inc, bool f32, const ReduceArgs& a, int blocks, double* out,
                           cudaStream_t st);
