@@ -4,6 +4,9 @@ total work on the same GPU, so the wall-time ratio is the slab mode's own overhe
 plane launch, flag waits/writes), an upper bound for the per-GPU overhead of the N-GPU run.
 With `asym` the split is (all but one tile plane | one plane): the big engine's time then stands for
 one GPU of an N-GPU run, and the overhead is measured against its share of the whole-engine time.
+The slab engines' steps are enqueued interleaved one step at a time (every rank of a real run
+enqueues its own steps concurrently; enqueueing one engine's K steps before the next would stall
+the first on its neighbour's flags for the whole enqueue time).
 usage: python tools/slab_overhead.py [W] [K] [asym]"""
 import os
 import sys
@@ -46,8 +49,9 @@ def main():
         whole.step_async(K)
         whole.sync()
         t1 = time.perf_counter()
-        for e in ranks:
-            e.step_async(K)
+        for _ in range(K):  # interleaved, as each rank of a real run enqueues its own steps
+            for e in ranks:
+                e.step_async(1)
         for e in ranks:
             assert e.sync()[0]
         t2 = time.perf_counter()
