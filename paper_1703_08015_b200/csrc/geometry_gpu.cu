@@ -11,12 +11,16 @@
 // the accept/skip/retry loop on the device: each CTA counts its share of the box, the 16 partial
 // counts are exchanged through distributed shared memory around one cluster barrier per pass,
 // every CTA takes the reference's decision on the same total, and the marking pass follows.
+// Until the first skip (near the end, and only when one sphere moves phi by ~0.02 or more) every
+// candidate is accepted, so batches of candidates are first painted in parallel (see the batch
+// fast path below): 1024^3 in 0.3-1.0 s instead of 2.5-4 s.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <random>
 #include <string>
 #include <vector>
@@ -178,6 +182,52 @@ __global__ void __launch_bounds__(kRasThreads, 1) ras_kernel(RasArgs a) {
   cg::this_cluster().sync();  // no CTA leaves while another may still read its shared memory
 }
 
+// ---- batch fast path -----------------------------------------------------------------------
+// While every candidate is accepted (the reference skips one only when it would push phi below
+// target - 0.01, i.e. near the end and only if one sphere moves phi by more than that), the
+// raster after candidate j is the union of spheres 0..j and candidate j's count is the number of
+// still-fluid nodes it covers that no earlier sphere covers. A batch is therefore painted in
+// parallel: every fluid node inside sphere j takes owner = min(j) (atomicMin), a histogram of
+// owners gives each candidate's count, the host replays the reference's decisions on those counts
+// and the accepted prefix is marked. At the first skip the sequential cluster loop takes over with
+// the identical state. Requires boxes no wider than the domain (no node visited twice).
+__global__ void __launch_bounds__(256) paint_kernel(RasArgs a, uint32_t* owner) {
+  const unsigned long long j = blockIdx.x;
+  const double* c = a.cand + 3 * j;
+  const int x0 = static_cast<int>(floor(__dsub_rn(c[0], a.r))), x1 = static_cast<int>(ceil(__dadd_rn(c[0], a.r)));
+  const int y0 = static_cast<int>(floor(__dsub_rn(c[1], a.r))), y1 = static_cast<int>(ceil(__dadd_rn(c[1], a.r)));
+  const int z0 = static_cast<int>(floor(__dsub_rn(c[2], a.r))), z1 = static_cast<int>(ceil(__dadd_rn(c[2], a.r)));
+  const int nx = x1 - x0 + 1, ny = y1 - y0 + 1, nz = z1 - z0 + 1;
+  const long long box = static_cast<long long>(nx) * ny * nz;
+  for (long long k = threadIdx.x; k < box; k += blockDim.x) {
+    const int x = x0 + static_cast<int>(k % nx);
+    const int y = y0 + static_cast<int>((k / nx) % ny);
+    const int z = z0 + static_cast<int>(k / (static_cast<long long>(nx) * ny));
+    const double dx = __dsub_rn(static_cast<double>(x), c[0]);
+    const double dy = __dsub_rn(static_cast<double>(y), c[1]);
+    const double dz = __dsub_rn(static_cast<double>(z), c[2]);
+    const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    if (d2 > a.r2) continue;
+    const size_t idx = (static_cast<size_t>(wrap(z, a.dims[2])) * a.dims[1] + wrap(y, a.dims[1])) *
+                           static_cast<size_t>(a.dims[0]) + wrap(x, a.dims[0]);
+    if (a.t[idx] != kSolid) atomicMin(owner + idx, static_cast<uint32_t>(j));
+  }
+}
+
+__global__ void owner_hist_kernel(const uint32_t* owner, size_t n, uint32_t* hist) {
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const uint32_t o = owner[i];
+    if (o != 0xffffffffu) atomicAdd(hist + o, 1u);
+  }
+}
+
+__global__ void owner_mark_kernel(uint8_t* t, const uint32_t* owner, size_t n, uint32_t accepted) {
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    if (owner[i] < accepted) t[i] = kSolid;
+}
+
 // One cluster of 16 CTAs (non-portable size; 8, then 1, if the device refuses it).
 void launch_cluster(const RasArgs& a) {
   static int size = 0;
@@ -238,10 +288,14 @@ extern "C" int splbm_generate_device(int kind, const splbm_generate_params* p, i
     uint8_t* t = nullptr;
     double* cand = nullptr;
     RasState* st = nullptr;
+    uint32_t* owner = nullptr;
+    uint32_t* hist = nullptr;
     auto cleanup = [&] {
       cudaFree(t);
       cudaFree(cand);
       cudaFree(st);
+      cudaFree(owner);
+      cudaFree(hist);
     };
     try {
       CK(cudaMalloc(&t, n));
@@ -260,17 +314,70 @@ extern "C" int splbm_generate_device(int kind, const splbm_generate_params* p, i
       a.st = st;
       a.t = t;
       a.cand = cand;
+      // batch fast path while no box can wrap onto itself (SPLBM_RAS_SEQ=1: sequential only)
+      bool fast = p->sphere_diameter + 2 <= min_dim && std::getenv("SPLBM_RAS_SEQ") == nullptr;
+      unsigned long long solid = 0;
+      std::vector<uint32_t> hist_h;
+      if (fast) {
+        CK(cudaMalloc(&owner, n * sizeof(uint32_t)));
+        CK(cudaMalloc(&hist, batch * sizeof(uint32_t)));
+        hist_h.resize(batch);
+      }
+      int sms = 148;
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+      const unsigned sweep_blocks = static_cast<unsigned>(sms) * 8;
       for (;;) {
         for (size_t k = 0; k < batch; ++k)
           for (int c = 0; c < 3; ++c)
             host[3 * k + c] = static_cast<double>(rng() >> 11) * 0x1.0p-53 * dims[c];
         CK(cudaMemcpy(cand, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice));
-        a.n_cand = batch;
+        size_t start = 0;
+        if (fast) {
+          a.cand = cand;
+          a.n_cand = batch;
+          CK(cudaMemset(owner, 0xff, n * sizeof(uint32_t)));
+          CK(cudaMemset(hist, 0, batch * sizeof(uint32_t)));
+          paint_kernel<<<static_cast<unsigned>(batch), 256>>>(a, owner);
+          CK(cudaGetLastError());
+          owner_hist_kernel<<<sweep_blocks, 256>>>(owner, n, hist);
+          CK(cudaGetLastError());
+          CK(cudaMemcpy(hist_h.data(), hist, batch * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+          // the reference's loop (geometry.cpp:296-324) on the counts; skips == 0 throughout
+          size_t accepted = 0;
+          bool done = false, skip = false;
+          for (; accepted < batch; ++accepted) {
+            if (!(static_cast<double>(n - solid) / static_cast<double>(n) > a.upper)) {
+              done = true;
+              break;
+            }
+            const unsigned long long newly = hist_h[accepted];
+            const double phi_after = static_cast<double>(n - solid - newly) / static_cast<double>(n);
+            if (!(phi_after >= a.lower)) {
+              skip = true;
+              break;
+            }
+            solid += newly;
+          }
+          owner_mark_kernel<<<sweep_blocks, 256>>>(t, owner, n, static_cast<uint32_t>(accepted));
+          CK(cudaGetLastError());
+          if (!done && !skip && !(static_cast<double>(n - solid) / static_cast<double>(n) > a.upper)) done = true;
+          if (done) break;
+          if (!skip) continue;
+          // first skip: the sequential loop resumes at this candidate with the same state
+          fast = false;
+          RasState s1{};
+          s1.solid = solid;
+          s1.best_err = 2.0;
+          CK(cudaMemcpy(st, &s1, sizeof(s1), cudaMemcpyHostToDevice));
+          start = accepted;
+        }
+        a.cand = cand + 3 * start;
+        a.n_cand = batch - start;
         launch_cluster(a);
         RasState s{};
         CK(cudaMemcpy(&s, st, sizeof(s), cudaMemcpyDeviceToHost));
         if (s.done) break;
-        if (s.consumed != batch) throw Error(SPLBM_ERR_CUDA, "RAS generator stopped early");
+        if (s.consumed != batch - start) throw Error(SPLBM_ERR_CUDA, "RAS generator stopped early");
       }
       CK(cudaMemcpy(types_out, t, n, cudaMemcpyDeviceToHost));
     } catch (...) {

@@ -12,7 +12,11 @@ pytestmark = pytest.mark.gpu
 
 CASES = [((32, 32, 32), 10, 0.5, 1), ((48, 40, 36), 12, 0.3, 3), ((64, 64, 64), 16, 0.8, 7),
          ((24, 24, 24), 23, 0.5, 5), ((30, 20, 25), 19, 0.6, 11), ((40, 40, 40), 4, 0.2, 2),
-         ((256, 256, 256), 40, 0.2, 7), ((128, 96, 160), 40, 0.5, 9)]
+         ((256, 256, 256), 40, 0.2, 7), ((128, 96, 160), 40, 0.5, 9),
+         # one sphere moves phi by several percent: the batch path hands over to the sequential
+         # loop at the first skip
+         ((20, 20, 20), 10, 0.5, 4), ((28, 28, 28), 12, 0.7, 6), ((36, 36, 36), 14, 0.4, 8),
+         ((22, 26, 24), 11, 0.25, 12)]
 
 
 @pytest.mark.parametrize("dims,d,phi,seed", CASES)
