@@ -25,4 +25,5 @@ du -sh gpurun_out
 timeout 900 python bench.py --config ras1024 --phi 0.2 --steps 20 --warmup 4 > gpurun_out/prof/ras1024_phi02.json.log 2>&1; echo big02=$?
 timeout 900 python bench.py --config ras1024 --phi 0.5 --single-copy --steps 20 --warmup 4 > gpurun_out/prof/ras1024_phi05_aa.json.log 2>&1; echo big05=$?
 timeout 900 python bench.py --config ras1024 --phi 0.8 --single-copy --steps 20 --warmup 4 > gpurun_out/prof/ras1024_phi08_aa.json.log 2>&1; echo big08=$?
+for a in "2 128" "4 128" "1 128 asym" "2 128 asym"; do timeout 300 python tools/slab_overhead.py $a 2>&1 | tail -1; done > gpurun_out/prof/slab_overhead.txt
 tail -3 gpurun_out/prof/pytest_gpu.log
