@@ -86,3 +86,26 @@ def test_config4_ras_1024_properties():
     assert a0 == b0 and a1 == b1 and sa == sb and va == vb
     assert a1["non_finite"] == 0
     assert abs(a1["mass"] - a0["mass"]) <= 1e-12 * a0["mass"]
+
+
+@pytest.mark.parametrize("variant", ["mrt", "f32", "f32_incompressible", "single_copy"])
+def test_config1_channel_128_model_variants(oracle, variant):
+    """configs[1] at full size for the paper's Table 2 model rows and the single-copy storage:
+    MRT, the f32 engine (quasi-compressible and incompressible) and the in-place AA pair, each
+    bit for bit against the oracle after 12 steps from rest (the bench's workload)."""
+    g = P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=(128, 128, 128)))
+    inc = variant == "f32_incompressible"
+    prec = "f32" if variant.startswith("f32") else "f64"
+    mrt = variant == "mrt"
+    model = P.FluidModel(P.Compressibility.Incompressible if inc else P.Compressibility.QuasiCompressible,
+                         collision=P.CollisionKind.MRT if mrt else P.CollisionKind.BGK, tau=0.8)
+    de = P.TileEngineT2C(g, 4, model, 0, precision=prec, single_copy=variant == "single_copy")
+    oe = make_oracle(oracle, g, 4, 0.8, inc, 0, precision=prec, mrt=mrt)
+    oe.threads = 16
+    de.initialize_uniform()
+    oe.initialize_uniform()
+    assert de.step_n(12)[0] and oe.step(12)[0]
+    mask = fluid_slot_mask(oe.tiles["types"], oe.q)
+    width = np.uint32 if prec == "f32" else np.uint64
+    assert np.array_equal(de.get_pdf()[mask].view(width), oe.current_pdf()[mask].view(width))
+    assert_fields_equal(oe.fields(), de.fields())
