@@ -419,7 +419,7 @@ def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured"), ras1024=F
             "e2e": None if wall is None else {
                 "value": round(nf * args.steps / wall / 1e6, 1), "unit": "MLUPS",
                 "h2d_bytes_per_step": round(4 * n_nodes * 8 / args.steps, 1),
-                "d2h_bytes_per_step": round(4 * n_nodes * 8 / args.steps, 1),
+                "d2h_bytes_per_step": round((4 * g.node_count() * 8 + g.node_count() + 8) / args.steps, 1),
                 "steps": args.steps, "wall_s": round(wall, 4), "per": "rank 0's buffers"},
         }
         if sampler:
