@@ -33,6 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 B_NODE = {2: 144.0, 3: 304.0}  # algorithmic bytes per node update, 2*q*8 (overhead.cpp:59-62)
+METRIC = "MLUPS (D3Q19 fp64 BGK) vs porosity; % of HBM peak GB/s; at 1/2/4/8 B200"
 WORKLOAD_1 = ("D3Q19 BGK fp64 channel 128^3 (BASELINE configs[1]), bounce-back walls, V inlet / "
               "P outlet, tiles 4^3, quasi-compressible, tau 0.8")
 
@@ -314,13 +315,26 @@ def _cpu_has_avx2():
 
 
 # ---------------------------------------------------------------------------------------------
+def workload_config(n, nf):
+    """The `config` object of the JSON line, identical for both arms (the driver compares them):
+    N=1 is BASELINE configs[1]; N>1 is the weak-scaled duct, one 128^3-node z-slab per GPU."""
+    if n == 1:
+        return {"workload": WORKLOAD_1, "fluid_nodes": int(nf),
+                "l2": "inputs > L2 (two PDF copies of 1.3 GB); no flush", "parallelism": "single GPU"}
+    return {"workload": f"D3Q19 BGK fp64 channel 128x128x{128 * n}, z-slab per GPU (128^3 nodes each)",
+            "fluid_nodes": int(nf),
+            "l2": "inputs > L2 (two PDF copies of 1.3 GB per rank); no flush",
+            "parallelism": f"zslab{n}"}
+
+
 def run_reference_arm(args):
-    """--impl reference: the reference's own CPU T2C implementation (oracle/_ref) on the host cores,
-    same metric/config; rank 0 only."""
+    """--impl reference: the reference's own CPU T2C implementation (oracle/_ref, the unmodified
+    /root/reference sources) on the host cores, same metric/config; rank 0 only. The geometry is
+    built in numpy (oracle/configs.py): nothing of the product package is loaded on this arm."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import paper_1703_08015_b200 as P
+    from oracle import configs as CF
     from oracle import ref as R
     world = int(os.environ.get("WORLD_SIZE", "1"))
     n = max(world, args.gpus)
@@ -330,8 +344,8 @@ def run_reference_arm(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return 0
     threads = os.cpu_count() or 1
-    g = channel_geometry(P, dims)
-    rg = R.RefGeometry.from_raster(3, g.dims, g.types, g.bc.velocity, g.bc.density, fast=fast)
+    types = CF.channel3d_raster(dims)
+    rg = R.RefGeometry.from_raster(3, dims, types, fast=fast, **CF.CHANNEL_BC)
     e = R.RefEngine(rg, "t2c", 4, 0.8, threads=threads)
     e.initialize_uniform()
     e.step(max(args.warmup, 1))
@@ -340,18 +354,17 @@ def run_reference_arm(args):
         e.step(1)
         times.append(e.last_seconds)
     sec = float(np.sum(times))
-    nf = g.fluid_count()
+    nf = int(np.count_nonzero(types))
     mlups = nf * args.steps / sec / 1e6
-    line = {"metric": "MLUPS (D3Q19 fp64 BGK) vs porosity; % of HBM peak GB/s; at 1/2/4/8 B200",
+    build = "-march=x86-64-v3" if fast else "-O3 (CMake Release flags)"
+    line = {"metric": METRIC,
             "value": round(mlups, 2), "unit": "MLUPS", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(sec / args.steps * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": ({"workload": WORKLOAD_1, "fluid_nodes": nf, "tiles": 32768, "phi_t": 0.969,
-                        "parallelism": "reference CPU engine"} if n == 1 else
-                       {"workload": f"D3Q19 BGK fp64 channel 128x128x{128 * n}, z-slab per GPU "
-                                    "(128^3 nodes each)", "parallelism": "reference CPU engine",
-                        "fluid_nodes": nf}),
+            "config": workload_config(n, nf),
+            "reference_engine": f"TileEngineT2C<double> + ThreadPool({threads}), {build} build of "
+                                "/root/reference/proj/src (oracle/_ref)",
             "cpu_baseline": {"value": round(mlups, 2), "unit": "MLUPS", "cores": threads,
                              "kind": "reference",
                              "sample": f"{args.steps} steps of the full {dims[0]}x{dims[1]}x{dims[2]} "
@@ -367,7 +380,8 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.gpus > 1:
         from paper_1703_08015_b200 import slab
-        return slab.bench_main(args, P, clock_sampler=ClockSampler, peak=measured_peaks())
+        return slab.bench_main(args, P, clock_sampler=ClockSampler, peak=measured_peaks(),
+                               config_fn=workload_config)
     peak, peak_kind = measured_peaks()
     K, W = args.steps, args.warmup
     dims = (128, 128, 128)
@@ -382,15 +396,12 @@ def run_ours(args):
     achieved = alg_bytes / (step_ms * 1e-3) / 1e9
     workload = "channel3d_128"
     line = {
-        "metric": "MLUPS (D3Q19 fp64 BGK) vs porosity; % of HBM peak GB/s; at 1/2/4/8 B200",
+        "metric": METRIC,
         "value": round(mlups, 1), "unit": "MLUPS", "n_gpus": 1, "steps": K, "warmup": W,
         "ms_per_step": round(step_ms, 5), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD_1,
-                   "fluid_nodes": nf, "tiles": int(eng.info.n_tiles),
-                   "phi_t": round(eng.info.phi_t, 4),
-                   "l2": "inputs > L2 (two PDF copies of 1.3 GB); no flush",
-                   "parallelism": "single GPU"},
+        "config": workload_config(1, nf),
+        "geometry_stats": {"tiles": int(eng.info.n_tiles), "phi_t": round(eng.info.phi_t, 4)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_source": peak_kind,
                      "algorithmic_bytes_per_launch": alg_bytes,
@@ -436,7 +447,7 @@ def run_big(args):
     gbs = mlups * 1e6 * B_NODE[3] / 1e9
     red = eng.reduce()
     print(json.dumps({
-        "metric": "MLUPS (D3Q19 fp64 BGK) vs porosity; % of HBM peak GB/s; at 1/2/4/8 B200",
+        "metric": METRIC,
         "value": round(mlups, 1), "unit": "MLUPS", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
         "dtype": "f64", "data": "synthetic",

@@ -285,7 +285,8 @@ class SlabRun:
         return self.engine.sync()
 
 
-def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured"), ras1024=False) -> int:
+def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured"), ras1024=False,
+               config_fn=None) -> int:
     """bench.py at N>1 (torchrun). Default: weak scaling — each rank owns a 128^3-node slab of one
     (128 x 128 x 128*N) D3Q19 channel. `ras1024` (bench.py --config ras1024): strong scaling of
     BASELINE configs[4], the RAS 1024^3 (phi --phi, d 40, seed 7, periodic) split into z-slabs
@@ -408,10 +409,11 @@ def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured"), ras1024=F
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t / args.steps * 1e3, 5),
             "higher_is_better": True, "scaling": "strong" if ras1024 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "ok": bool(all_ok and ok2),
-            "config": {"workload": f"{workload}, tile-face halos via {transport}",
-                       "parallelism": f"zslab{world}", "fluid_nodes": int(nf),
-                       "devices": torch.cuda.device_count(),
-                       "l2": "inputs > L2 (two PDF copies of 1.3 GB per rank); no flush"},
+            "config": (config_fn(world, nf) if config_fn else
+                       {"workload": workload, "fluid_nodes": int(nf),
+                        "l2": "inputs > L2 (PDF copies of several GB per rank); no flush",
+                        "parallelism": f"zslab{world}"}),
+            "transport": f"tile-face halos via {transport}", "devices": torch.cuda.device_count(),
             "roofline": {"bound": "hbm", "achieved": round(alg, 1), "peak": peak[0], "unit": "GB/s",
                          "frac": round(alg / peak[0], 4), "peak_source": peak[1],
                          "per": "one rank (the slowest rank's time)"},
