@@ -244,9 +244,11 @@ def other_configs(P, K, W, peak):
     return rows
 
 
-def e2e_public_api(P, g, steps):
+def e2e_public_api(P, g, steps, bench_steps=None, samples=3):
     """End to end through the public API with host buffers: NodeInit fields H2D from pinned host
-    memory, `steps` LBM steps (first-failure check), the final (rho, u) FieldData D2H."""
+    memory, `steps` LBM steps (first-failure check), the final (rho, u) FieldData D2H; wall clock,
+    median of `samples` runs. `steps` is the workload's run length (BASELINE configs[1]: 1000
+    steps); the same measurement at the bench's own --steps is reported beside it."""
     import torch
     eng = P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8))
     n = int(eng.info.n_tiles_stored) * eng.n_tn
@@ -261,38 +263,66 @@ def e2e_public_api(P, g, steps):
     eng.initialize_arrays(*pinned)  # warm: the 32-step CUDA graph of this parity is built here
     eng.step_n(64)
     eng.fields(out=out)
-    t0 = time.perf_counter()
-    eng.initialize_arrays(*pinned)
-    ok, failed = eng.step_n(steps)
-    f = eng.fields(out=out)  # Engine::fields() (the caller sums mass separately, engine.hpp:640)
-    wall = time.perf_counter() - t0
-    assert ok and np.isfinite(f.rho).all()
     nf = eng.fluid_nodes()
+
+    def run(k):
+        t0 = time.perf_counter()
+        eng.initialize_arrays(*pinned)
+        ok, failed = eng.step_n(k)
+        f = eng.fields(out=out)  # Engine::fields() (the caller sums mass separately, engine.hpp:640)
+        wall = time.perf_counter() - t0
+        assert ok and np.isfinite(f.rho).all()
+        return wall
+
+    walls = sorted(run(steps) for _ in range(samples))
+    wall = walls[len(walls) // 2]
     h2d = 4 * n * 8  # NodeInit (rho, u) at every stored tile node
     d2h = 4 * nr * 8 + nr + 8  # the raster FieldData (rho, u, mask; assembled on the device) + the failure stamp
-    return {"value": round(nf * steps / wall / 1e6, 1), "unit": "MLUPS",
-            "h2d_bytes_per_step": round(h2d / steps, 1), "d2h_bytes_per_step": round(d2h / steps, 1),
-            "steps": steps, "wall_s": round(wall, 4)}
+    out_d = {"value": round(nf * steps / wall / 1e6, 1), "unit": "MLUPS",
+             "h2d_bytes_per_step": round(h2d / steps, 1), "d2h_bytes_per_step": round(d2h / steps, 1),
+             "steps": steps, "wall_s": round(wall, 4), "samples": samples,
+             "wall_s_all": [round(w, 4) for w in walls]}
+    if bench_steps and bench_steps != steps:
+        wk = sorted(run(bench_steps) for _ in range(samples))[samples // 2]
+        out_d["at_bench_steps"] = {"steps": bench_steps, "value": round(nf * bench_steps / wk / 1e6, 1),
+                                   "wall_s": round(wk, 4),
+                                   "h2d_bytes_per_step": round(h2d / bench_steps, 1),
+                                   "d2h_bytes_per_step": round(d2h / bench_steps, 1)}
+    return out_d
 
 
-def cpu_baseline(P, dims, budget_s=15.0):
-    """The reference's own T2C engine (oracle/_ref, built from /root/reference) on all host cores,
-    on a bounded sample of the same workload (same geometry, fewer steps)."""
+def _ref_build():
+    """(fast-variant key, description) of the reference timing build this host runs best."""
     from oracle import ref as R
-    fast = R.available(fast=True) and _cpu_has_avx2()
+    v = R.best_timing_build()
+    if v is None:
+        return False, "-O3 (CMake Release flags, baseline x86-64)"
+    return v, f"-O3 -march=x86-64-{v}"
+
+
+def cpu_baseline(dims, budget_s=15.0, samples=3):
+    """The reference's own T2C engine (oracle/_ref, built from /root/reference) on all host cores,
+    on a bounded sample of the same workload (same geometry, fewer steps): best of `samples`
+    timed batches, plus the 1-thread figure."""
+    from oracle import configs as CF
+    from oracle import ref as R
+    fast, build = _ref_build()
     if not R.available(fast=fast):
         return None
     threads = os.cpu_count() or 1
-    g = channel_geometry(P, dims)
-    rg = R.RefGeometry.from_raster(3, g.dims, g.types, g.bc.velocity, g.bc.density, fast=fast)
+    types = CF.channel3d_raster(dims)
+    rg = R.RefGeometry.from_raster(3, dims, types, fast=fast, **CF.CHANNEL_BC)
     e = R.RefEngine(rg, "t2c", 4, 0.8, threads=threads)
     e.initialize_uniform()
     e.step(1)
     probe = max(e.last_seconds, 1e-3)
-    steps = int(max(2, min(200, budget_s / probe)))
-    e.step(steps)
-    sec = e.last_seconds
-    nf = g.fluid_count()
+    steps = int(max(2, min(100, budget_s / samples / probe)))
+    secs = []
+    for _ in range(samples):
+        e.step(steps)
+        secs.append(e.last_seconds)
+    sec = min(secs)
+    nf = int(np.count_nonzero(types))
     e1 = R.RefEngine(rg, "t2c", 4, 0.8, threads=1)  # the 1-thread figure (SURVEY §8d)
     e1.initialize_uniform()
     e1.step(2)
@@ -300,18 +330,10 @@ def cpu_baseline(P, dims, budget_s=15.0):
     return {"value": round(nf * steps / sec / 1e6, 2), "unit": "MLUPS", "cores": threads,
             "single_thread_mlups": round(single, 2),
             "kind": "reference",
-            "sample": f"{steps} T2C steps of the {dims[0]}x{dims[1]}x{dims[2]} channel "
-                      f"({'-march=x86-64-v3' if fast else '-O3'} build of /root/reference sources, "
-                      f"ThreadPool({threads}))",
+            "sample": f"best of {samples} x {steps} T2C steps of the {dims[0]}x{dims[1]}x{dims[2]} "
+                      f"channel ({build} build of /root/reference sources, ThreadPool({threads}))",
+            "samples_mlups": [round(nf * steps / s / 1e6, 2) for s in secs],
             "seconds": round(sec, 3)}
-
-
-def _cpu_has_avx2():
-    try:
-        flags = open("/proc/cpuinfo").read()
-        return " avx2" in flags and " fma" in flags
-    except OSError:
-        return False
 
 
 # ---------------------------------------------------------------------------------------------
@@ -339,7 +361,7 @@ def run_reference_arm(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     n = max(world, args.gpus)
     dims = (128, 128, 128 * n)  # our arm's workload at this N (one 128^3 slab per GPU)
-    fast = R.available(fast=True) and _cpu_has_avx2()
+    fast, build = _ref_build()
     if not R.available(fast=fast):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return 0
@@ -356,7 +378,6 @@ def run_reference_arm(args):
     sec = float(np.sum(times))
     nf = int(np.count_nonzero(types))
     mlups = nf * args.steps / sec / 1e6
-    build = "-march=x86-64-v3" if fast else "-O3 (CMake Release flags)"
     line = {"metric": METRIC,
             "value": round(mlups, 2), "unit": "MLUPS", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(sec / args.steps * 1e3, 3),
@@ -405,7 +426,9 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_source": peak_kind,
                      "algorithmic_bytes_per_launch": alg_bytes,
-                     "traffic": load_ncu_traffic(workload)},
+                     "traffic": load_ncu_traffic(workload),
+                     "traffic_source": "committed ncu --set full capture (profiles/ncu_step_kernel.json), "
+                                       "dram__bytes_read.sum + dram__bytes_write.sum per launch"},
         "gpu_launches": int(launches),
         "clocks": clocks,
         "overhead": accounting(P, eng, nf, B_NODE[3], workload),
@@ -415,9 +438,9 @@ def run_ours(args):
         line["porosity_sweep"] = porosity_sweep(P, min(K, 64), max(W, 3), peak)  # whole 32-step graphs
     if not args.no_other:
         line["other_configs"] = other_configs(P, min(K, 64), max(W, 3), peak)
-    line["e2e"] = e2e_public_api(P, g, 1000)
+    line["e2e"] = e2e_public_api(P, g, 1000, bench_steps=K)  # configs[1] is a 1000-step run
     if not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(P, dims)
+        line["cpu_baseline"] = cpu_baseline(dims)
     print(json.dumps(line))
     return 0
 

@@ -32,16 +32,33 @@ class RefError(RuntimeError):
         self.code = code
 
 
-def available(fast: bool = False) -> bool:
+def available(fast=False) -> bool:
     return os.path.exists(_path(fast))
 
 
-def _path(fast: bool) -> str:
-    return os.path.join(REF_DIR, "libsplbm_ref_fast.so" if fast else "libsplbm_ref.so")
+def _path(fast) -> str:
+    """fast: False = the bitwise oracle build; True / "v3" = -march=x86-64-v3; "v4" = x86-64-v4."""
+    name = {False: "libsplbm_ref.so", True: "libsplbm_ref_fast.so", "v3": "libsplbm_ref_fast.so",
+            "v4": "libsplbm_ref_v4.so"}[fast]
+    return os.path.join(REF_DIR, name)
 
 
-def lib(fast: bool = False) -> C.CDLL:
-    key = "fast" if fast else "exact"
+def best_timing_build():
+    """The highest ISA-level timing build of the reference this host can run (None = only the
+    baseline-x86-64 oracle build): x86-64-v4 needs AVX-512 F/BW/CD/DQ/VL, v3 needs AVX2+FMA."""
+    try:
+        flags = set(open("/proc/cpuinfo").read().split())
+    except OSError:
+        flags = set()
+    if {"avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl"} <= flags and available("v4"):
+        return "v4"
+    if {"avx2", "fma", "bmi2"} <= flags and available("v3"):
+        return "v3"
+    return None
+
+
+def lib(fast=False) -> C.CDLL:
+    key = {False: "exact", True: "v3", "v3": "v3", "v4": "v4"}[fast]
     if key in _libs:
         return _libs[key]
     L = C.CDLL(_path(fast))

@@ -220,7 +220,7 @@ def cmd_bench(cfg, out):  # splbm.cpp:295-366 for method t2c-b200
         eng.step_async(steps)
         ok, failed = eng.sync()
         if not ok:
-            raise NumericalError("non-finite state", warmup + failed)
+            raise NumericalError("non-finite state", failed)  # already absolute (splbm.cpp:250)
         wall = eng.last_batch_ms() * 1e-3
         mlups = g.fluid_count() * steps / (wall * 1e6) if wall > 0 else 0.0
         cost = O.CostParams(lat=solver_lattice(g.d), s_d=4.0 if precision == "f32" else 8.0)

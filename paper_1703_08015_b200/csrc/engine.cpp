@@ -103,6 +103,7 @@ struct splbm_dev_engine {
   int n_halo_dirs = 0;
   double* scratch = nullptr;
   uint64_t scratch_count = 0;  // doubles in `scratch`
+  double* reduce_buf = nullptr;  // splbm_dev_reduce partials (allocated on first use)
   // device FieldData frame (splbm_dev_fields), built on the first fields() call
   uint32_t* cells = nullptr;            // cell index of each owned tile
   std::vector<uint64_t> layer_first;    // owned tile index of the first tile at layer >= L
@@ -148,7 +149,12 @@ struct splbm_dev_engine {
   unsigned long long* peer_flags_down = nullptr;
   uint64_t peer_down_halo0 = 0;  // first high-halo tile of the lower neighbour
   unsigned long long comm_seq = 0;
+  // p2p halo-arrival wait: cuStreamWaitValue64 with CU_STREAM_WAIT_VALUE_FLUSH where the device
+  // can flush remote writes (CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES), else the acquire-polling
+  // wait_flags_kernel; SPLBM_P2P_WAIT=kernel|flush forces one (flush must be supported)
+  bool wait_flush = false;
   std::vector<void*> ipc_opened;
+  std::vector<int> peer_enabled;  // devices this engine's device enabled peer access to
 
   ~splbm_dev_engine() {
     if (device >= 0) cudaSetDevice(device);
@@ -174,6 +180,7 @@ struct splbm_dev_engine {
                     static_cast<void*>(step_base), static_cast<void*>(domain_err),
                     static_cast<void*>(zero_base),
                     static_cast<void*>(halo_dirs), static_cast<void*>(scratch),
+                    static_cast<void*>(reduce_buf),
                     static_cast<void*>(cells), static_cast<void*>(frame)})
       if (p) cudaFree(p);
     if (ev0) cudaEventDestroy(ev0);
@@ -338,10 +345,18 @@ struct splbm_dev_engine {
     const StreamMemOps& ops = stream_mem_ops();
     const int k = static_cast<int>(comm_seq & 1);
     CK(cudaStreamWaitEvent(side, ev_int[k ^ 1], 0));
-    if (peer_pdf_down[0])
-      cu_check(ops.wait(side, reinterpret_cast<CUdeviceptr>(&flags[0]), comm_seq, CU_STREAM_WAIT_VALUE_GEQ), "cuStreamWaitValue64");
-    if (peer_pdf_up[0])
-      cu_check(ops.wait(side, reinterpret_cast<CUdeviceptr>(&flags[1]), comm_seq, CU_STREAM_WAIT_VALUE_GEQ), "cuStreamWaitValue64");
+    const unsigned long long* f_below = peer_pdf_down[0] ? &flags[0] : nullptr;
+    const unsigned long long* f_above = peer_pdf_up[0] ? &flags[1] : nullptr;
+    if (wait_flush) {  // GPU front-end wait + flush of outstanding remote writes
+      for (const unsigned long long* f : {f_below, f_above})
+        if (f)
+          cu_check(ops.wait(side, reinterpret_cast<CUdeviceptr>(f), comm_seq,
+                            CU_STREAM_WAIT_VALUE_GEQ | CU_STREAM_WAIT_VALUE_FLUSH),
+                   "cuStreamWaitValue64");
+    } else if (f_below || f_above) {  // system-scope acquire polling (wait_flags_kernel)
+      CK(splbm_dev::launch_wait_flags(f_below, f_above, comm_seq, side));
+      ++launches;
+    }
     peer_part1 = true;
     std::swap(stream, side);  // part 1 launches on the side stream
     step_part(1);
@@ -620,18 +635,23 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
     CK(cudaMemcpyAsync(e->nb, nb_local.data(), nb_local.size() * 4, cudaMemcpyHostToDevice, e->stream));
   }
   {
+    // the tile node types (GPU builder output or a host upload) are freed on every exit path
     uint8_t* types_d = e->tb.types_bc;
+    if (gpu_tiles) e->tb.types_bc = nullptr;
+    std::unique_ptr<uint8_t, cudaError_t (*)(void*)> types_guard(nullptr, cudaFree);
     if (!gpu_tiles) {
       CK(cudaMalloc(&types_d, std::max<std::size_t>(types_local.size(), 1)));
+      types_guard.reset(types_d);
       CK(cudaMemcpyAsync(types_d, types_local.data(), types_local.size(), cudaMemcpyHostToDevice, e->stream));
+    } else {
+      types_guard.reset(types_d);
     }
     splbm_dev::NodeInfoArgs ni{types_d, e->nb, e->info, S, e->a, 32 / e->es};
     CK(splbm_dev::launch_node_info(d, ni, e->stream));
     ++e->launches;
     CK(cudaStreamSynchronize(e->stream));
-    cudaFree(types_d);
+    types_guard.reset();
     if (gpu_tiles) {
-      e->tb.types_bc = nullptr;
       e->device_bytes -= S * n_tn;
       e->tb_bytes -= S * n_tn;
     }
@@ -975,7 +995,8 @@ int splbm_dev_reduce(splbm_dev_engine* e, double out[3]) {
   return guarded([&] {
     checked(e);
     const int blocks = 1184;  // 8 x 148 SMs, fixed so the summation order is fixed
-    double* dev = e->alloc<double>(3 * blocks + 3);
+    if (!e->reduce_buf) e->reduce_buf = e->alloc<double>(3 * blocks + 3);  // kept: no per-call cudaMalloc
+    double* dev = e->reduce_buf;
     splbm_dev::ReduceArgs ra{e->cur_pdf(), e->info, e->view(), e->n_low * e->n_tn,
                              e->n_own * e->n_tn, e->n_tn, dev};
     cudaError_t err = splbm_dev::launch_reduce(e->d, e->incompressible != 0, e->f32, ra, blocks,
@@ -984,8 +1005,6 @@ int splbm_dev_reduce(splbm_dev_engine* e, double out[3]) {
     if (err == cudaSuccess)
       err = cudaMemcpyAsync(out, dev + 3 * blocks, 3 * sizeof(double), cudaMemcpyDeviceToHost, e->stream);
     if (err == cudaSuccess) err = cudaStreamSynchronize(e->stream);
-    cudaFree(dev);
-    e->device_bytes -= (3 * blocks + 3) * sizeof(double);
     CK(err);
   });
 }
@@ -1132,6 +1151,18 @@ int splbm_dev_p2p_attach(splbm_dev_engine* e, const uint8_t* lower_blob, const u
       if (b.magic != 0x53504c42u || b.version != 1 || b.tile_stride != e->tile_stride())
         throw config_error("incompatible peer blob");
       if (b.pid == static_cast<int32_t>(getpid())) {
+        if (b.device != e->device) {  // one process driving several GPUs: direct peer access
+          int can = 0;
+          CK(cudaDeviceCanAccessPeer(&can, e->device, b.device));
+          if (!can)
+            throw Error(SPLBM_ERR_CUDA, "device " + std::to_string(e->device) +
+                                            " cannot access peer device " + std::to_string(b.device));
+          const cudaError_t pe = cudaDeviceEnablePeerAccess(b.device, 0);
+          if (pe == cudaErrorPeerAccessAlreadyEnabled)
+            (void)cudaGetLastError();  // enabled by an earlier engine: fine
+          else
+            CK(pe);
+        }
         pdf[0] = reinterpret_cast<double*>(b.raw_pdf[0]);
         pdf[1] = reinterpret_cast<double*>(b.raw_pdf[1]);
         *fl = reinterpret_cast<unsigned long long*>(b.raw_flags);
@@ -1162,6 +1193,31 @@ int splbm_dev_p2p_attach(splbm_dev_engine* e, const uint8_t* lower_blob, const u
       open(b, e->peer_pdf_up, &e->peer_flags_up);
     }
     stream_mem_ops();
+    {
+      CUdevice cu_dev = 0;
+      int can_flush = 0;
+      CUresult (*get_dev)(CUdevice*, int) = nullptr;
+      CUresult (*get_attr)(int*, CUdevice_attribute, CUdevice) = nullptr;
+      cudaDriverEntryPointQueryResult q1, q2;
+      void* p1 = nullptr;
+      void* p2 = nullptr;
+      if (cudaGetDriverEntryPoint("cuDeviceGet", &p1, cudaEnableDefault, &q1) == cudaSuccess &&
+          cudaGetDriverEntryPoint("cuDeviceGetAttribute", &p2, cudaEnableDefault, &q2) == cudaSuccess &&
+          p1 && p2 && q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess) {
+        get_dev = reinterpret_cast<decltype(get_dev)>(p1);
+        get_attr = reinterpret_cast<decltype(get_attr)>(p2);
+        if (get_dev(&cu_dev, e->device) == CUDA_SUCCESS)
+          get_attr(&can_flush, CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES, cu_dev);
+      }
+      e->wait_flush = can_flush != 0;
+      if (const char* v = std::getenv("SPLBM_P2P_WAIT")) {
+        if (std::strcmp(v, "kernel") == 0) e->wait_flush = false;
+        else if (std::strcmp(v, "flush") == 0) {
+          if (!can_flush) throw config_error("SPLBM_P2P_WAIT=flush: device cannot flush remote writes");
+          e->wait_flush = true;
+        }
+      }
+    }
     CK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
     e->zero_base = e->alloc<long long>(1);
     CK(cudaMemset(e->zero_base, 0, sizeof(long long)));

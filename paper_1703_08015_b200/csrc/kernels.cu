@@ -121,6 +121,20 @@ __device__ __forceinline__ float ld_pdf(const float* p) {
 #endif
 }
 
+// Coherent variant for the single-copy (AA) kernels, which read and write the same array in one
+// launch: `.nc` is only defined for data that stays read-only for the whole kernel, so these keep
+// the L2::64B fetch size but go through the coherent path.
+__device__ __forceinline__ double ld_pdf_rw(const double* p) {
+  double v;
+  asm volatile("ld.global.L2::64B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ld_pdf_rw(const float* p) {
+  float v;
+  asm volatile("ld.global.L2::64B.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+
 // L2 prefetch of a future CTA's read blocks (the CTA StepArgs::l2pf CTAs ahead, about half a
 // wave): one bulk request per tile block (Q*NTN doubles, contiguous) holds no registers, so more
 // DRAM reads are in flight than the gather alone keeps. Whole blocks measured faster than
@@ -533,7 +547,7 @@ __global__ void __launch_bounds__(aa_threads<D, LOGA>(),
 
   R f[Q];
 #pragma unroll
-  for (int i = 0; i < Q; ++i) f[i] = ld_pdf(PHASE == 1 ? addr(i) : own + (opp(i) * NTN + p));
+  for (int i = 0; i < Q; ++i) f[i] = ld_pdf_rw(PHASE == 1 ? addr(i) : own + (opp(i) * NTN + p));
 
   bool good;
   if (type == 1) {
@@ -551,6 +565,30 @@ __global__ void __launch_bounds__(aa_threads<D, LOGA>(),
 
 // Advances the step counter the failure stamps are relative to (one per enqueued batch).
 __global__ void bump_kernel(long long* step_base, long long by) { *step_base += by; }
+
+// Slab halo-arrival wait (p2p transport): one thread polls the "faces arrived" flags with
+// system-scope acquire loads until both reach `seq`. The neighbours publish a flag only after
+// their boundary planes (whose peer stores into my halo tiles precede it: stream write-value with
+// its default system-scope fence); the acquire makes those remote stores visible here, and the
+// boundary-plane kernel that follows in stream order reads them. This is the PTX memory-model
+// release/acquire pattern, valid also when the receiving GPU reorders remote writes (the reason a
+// plain cuStreamWaitValue64 would need CU_STREAM_WAIT_VALUE_FLUSH).
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__global__ void wait_flags_kernel(const unsigned long long* f0, const unsigned long long* f1,
+                                  unsigned long long seq) {
+  unsigned ns = 32;
+  for (const unsigned long long* f : {f0, f1}) {
+    if (!f) continue;
+    while (ld_acquire_sys(f) < seq) {
+      __nanosleep(ns);
+      ns = ns < 1024 ? 2 * ns : ns;
+    }
+  }
+}
 
 // ---------------------------------------------------------------------------------------------
 // Gather words (see file header). Mirrors the blocked test of the sweep (engine.hpp:485-500).
@@ -982,6 +1020,12 @@ cudaError_t launch_step(int d, bool inc, bool f32, const StepArgs& a, cudaStream
 
 cudaError_t launch_bump(long long* step_base, long long by, cudaStream_t st) {
   bump_kernel<<<1, 1, 0, st>>>(step_base, by);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wait_flags(const unsigned long long* f0, const unsigned long long* f1,
+                              unsigned long long seq, cudaStream_t st) {
+  wait_flags_kernel<<<1, 1, 0, st>>>(f0, f1, seq);
   return cudaGetLastError();
 }
 

@@ -127,6 +127,9 @@ struct HaloArgs {
 
 cudaError_t launch_step(int d, bool inc, bool f32, const StepArgs& a, cudaStream_t st);
 cudaError_t launch_bump(long long* step_base, long long by, cudaStream_t st);
+// Slab p2p: wait (system-scope acquire polling) until the non-null flags reach seq.
+cudaError_t launch_wait_flags(const unsigned long long* f0, const unsigned long long* f1,
+                              unsigned long long seq, cudaStream_t st);
 cudaError_t launch_node_info(int d, const NodeInfoArgs& a, cudaStream_t st);
 cudaError_t launch_init(int d, bool inc, bool f32, const InitArgs& a, cudaStream_t st);
 cudaError_t launch_frame(int d, bool inc, bool f32, const FrameArgs& a, cudaStream_t st);

@@ -150,8 +150,15 @@ class TileEngineT2C:
         self.initialize_arrays(*arr)
 
     def initialize_arrays(self, rho, ux, uy, uz) -> None:
+        """NodeInit values at every stored tile node (node_coords() order), one array per moment;
+        the C side copies n_tiles_stored * n_tn doubles from each."""
+        n = int(self.info.n_tiles_stored) * self.n_tn
         c = lambda v: np.ascontiguousarray(v, np.float64).ravel()
-        _native.check(self._L.splbm_dev_initialize(self._h, c(rho), c(ux), c(uy), c(uz)))
+        arrs = [c(v) for v in (rho, ux, uy, uz)]
+        if any(a.size != n for a in arrs):
+            raise ConfigError(f"initialize_arrays needs {n} values per moment "
+                              f"(got {[a.size for a in arrs]})")
+        _native.check(self._L.splbm_dev_initialize(self._h, *arrs))
 
     def initialize_uniform(self, rho0: float = 1.0, u0=(0.0, 0.0, 0.0)) -> None:  # engine.hpp:72-75
         _native.check(self._L.splbm_dev_initialize_uniform(self._h, float(rho0),
@@ -192,6 +199,8 @@ class TileEngineT2C:
             rho, ux, uy, uz, mask = out.rho, out.ux, out.uy, out.uz, out.mask
             if any(a.size != n or not a.flags.c_contiguous for a in (rho, ux, uy, uz, mask)):
                 raise ConfigError("fields(out=...) arrays must be contiguous raster-sized")
+            if any(a.dtype != np.float64 for a in (rho, ux, uy, uz)) or mask.dtype != np.uint8:
+                raise ConfigError("fields(out=...) needs float64 rho/ux/uy/uz and a uint8 mask")
         else:
             rho, ux, uy, uz = (np.empty(n) for _ in range(4))
             mask = np.empty(n, np.uint8)

@@ -40,10 +40,10 @@ def linf_rel_diff(a: FieldData, b: FieldData) -> float:
     worst = 0.0
     for fa, fb in ((a.rho, b.rho), (a.ux, b.ux), (a.uy, b.uy), (a.uz, b.uz)):
         xa, xb = fa[m], fb[m]
-        if xa.size == 0:
-            continue
-        scale = max(float(np.max(np.abs(xa))), float(np.max(np.abs(xb))))
-        diff = float(np.max(np.abs(xa - xb)))
+        # std::max(x, NaN) keeps x (the comparison is false), so NaN entries never raise scale or
+        # diff; np.fmax skips NaN the same way.
+        scale = float(np.fmax.reduce(np.abs(np.concatenate([xa, xb])), initial=0.0))
+        diff = float(np.fmax.reduce(np.abs(xa - xb), initial=0.0))
         if scale > 0.0:
             worst = max(worst, diff / scale)
     return worst

@@ -40,20 +40,30 @@ def plane_tile_counts(g: Geometry, a: int, periodic=None) -> np.ndarray:
     return out
 
 
-def plan_slabs(counts, world: int) -> list[tuple[int, int]]:
+def min_planes(world: int, periodic, d: int) -> int:
+    """Fewest tile planes a rank may own. Two ranks on a periodic slab axis are each other's lower
+    AND upper neighbour: a one-plane slab would make the other rank's low and high halo the same
+    plane, which the slab layout does not store twice (splbm_slab_layout rejects it)."""
+    axis = 2 if d == 3 else 1
+    return 2 if world == 2 and Periodicity.of(periodic).axis(axis) else 1
+
+
+def plan_slabs(counts, world: int, min_planes: int = 1) -> list[tuple[int, int]]:
     """Contiguous plane ranges [z0, z1), one per rank, minimising the largest per-rank count of
-    non-empty tiles (equal z-extents would be load-imbalanced on sparse media). Linear partition:
-    binary search on the capacity with a greedy sweep, then split groups until every rank owns at
-    least one plane."""
+    non-empty tiles (equal z-extents would be load-imbalanced on sparse media), each at least
+    `min_planes` planes thick. Linear partition: binary search on the capacity with a greedy
+    sweep, then split groups until every rank owns a range."""
     counts = [int(c) for c in np.asarray(counts).ravel()]
     L = len(counts)
-    if world < 1 or world > L:
-        raise ValueError(f"cannot split {L} tile planes over {world} ranks")
+    m = max(1, int(min_planes))
+    if world < 1 or world * m > L:
+        raise ValueError(f"cannot split {L} tile planes over {world} ranks "
+                         f"(at least {m} plane(s) each)")
 
     def greedy(cap):
         cuts, load = [0], 0
         for z, c in enumerate(counts):
-            if load + c > cap and z > cuts[-1]:
+            if load + c > cap and z - cuts[-1] >= m and L - z >= m:
                 cuts.append(z)
                 load = 0
             load += c
@@ -67,18 +77,18 @@ def plan_slabs(counts, world: int) -> list[tuple[int, int]]:
         else:
             lo = mid + 1
     cuts = greedy(lo)
-    while len(cuts) - 1 < world:  # split the heaviest multi-plane group at its balance point
+    while len(cuts) - 1 < world:  # split the heaviest splittable group at its balance point
         groups = [(sum(counts[cuts[i]:cuts[i + 1]]), i) for i in range(len(cuts) - 1)
-                  if cuts[i + 1] - cuts[i] > 1]
+                  if cuts[i + 1] - cuts[i] >= 2 * m]
         _, i = max(groups)
         a, b = cuts[i], cuts[i + 1]
-        half, acc, z = sum(counts[a:b]) / 2.0, 0, a + 1
-        for zz in range(a, b - 1):
+        half, acc, z = sum(counts[a:b]) / 2.0, 0, a + m
+        for zz in range(a, b - m):
             acc += counts[zz]
-            z = zz + 1
+            z = max(a + m, zz + 1)
             if acc >= half:
                 break
-        cuts.insert(i + 1, z)
+        cuts.insert(i + 1, min(z, b - m))
     return [(cuts[r], cuts[r + 1]) for r in range(world)]
 
 
@@ -219,7 +229,8 @@ class SlabRun:
         from .engine import TileEngineT2C
         per = Periodicity.of(periodic)
         self.rank, self.world = rank, world
-        self.slabs = slabs or plan_slabs(plane_tile_counts(g, a, per), world)
+        self.slabs = slabs or plan_slabs(plane_tile_counts(g, a, per), world,
+                                         min_planes(world, per, g.d))
         z0, z1 = self.slabs[rank]
         self.engine = TileEngineT2C(g, a, model, per, device=device,
                                     slab=None if world == 1 else (z0, z1))
@@ -313,7 +324,8 @@ def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured"), ras1024=F
         per = (1, 1, 1)
         g = P.generate(P.GeometryKind.Ras3D, P.GenerateParams(
             dims=(1024, 1024, 1024), sphere_diameter=40, target_porosity=args.phi, seed=7), device=device)
-        slabs = plan_slabs(plane_tile_counts(g, 4, Periodicity.of(per)), world)
+        slabs = plan_slabs(plane_tile_counts(g, 4, Periodicity.of(per)), world,
+                           min_planes(world, per, g.d))
         workload = (f"configs[4] RAS 1024^3 d=40 seed 7 periodic, phi target {args.phi}, z-slabs "
                     f"balanced by non-empty tiles")
     else:

@@ -115,3 +115,30 @@ def test_slab_layout_partitions_tiles():
     assert owned == T
     with pytest.raises(P.ConfigError):
         slab.slab_layout(g, 4, 7, 0, 7)  # halo planes would overlap the slab
+
+
+def test_plan_slabs_two_ranks_periodic_skewed():
+    """Two ranks on a periodic axis never get a one-plane slab (the other rank's low and high halo
+    would be the same plane); every such plan builds a valid layout."""
+    g = P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(16, 16, 24), sphere_diameter=6,
+                                                          target_porosity=0.6, seed=3))
+    counts = slab.plane_tile_counts(g, 4, 7)
+    skew = np.array(counts, dtype=np.int64)
+    skew[-1] *= 50  # one very heavy plane: the unconstrained plan isolates it
+    assert slab.plan_slabs(skew, 2)[1] == (5, 6)
+    m = slab.min_planes(2, 7, 3)
+    assert m == 2 and slab.min_planes(3, 7, 3) == 1 and slab.min_planes(2, 3, 3) == 1
+    for c in (counts, skew):
+        sl = slab.plan_slabs(c, 2, m)
+        assert all(b - a >= 2 for a, b in sl) and sl[0][0] == 0 and sl[-1][1] == 6
+        for z0, z1 in sl:
+            slab.slab_layout(g, 4, 7, z0, z1)
+    with pytest.raises(ValueError):
+        slab.plan_slabs([1, 1, 1], 2, 2)
+    for world in range(1, 7):
+        for mm in (1, 2, 3):
+            if world * mm > 6:
+                continue
+            sl = slab.plan_slabs(skew, world, mm)
+            assert len(sl) == world and all(b - a >= mm for a, b in sl)
+            assert all(sl[i][1] == sl[i + 1][0] for i in range(world - 1))

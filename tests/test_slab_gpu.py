@@ -94,20 +94,19 @@ def test_native_comm_attach_single_rank():
     assert e2.current_step() == 33 and e2.tile_visits() == e1.tile_visits()
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
-@pytest.mark.parametrize("name", sorted(CASES))
-def test_p2p_peer_store_slabs_match_whole(name, world):
-    """Fused exchange: the boundary-plane kernel stores its faces straight into the neighbours'
-    halo tiles, ordered by GPU-side flag waits/writes (same-process peers on one GPU; across
-    processes the blob carries CUDA IPC handles). Bitwise equal to the single engine."""
+def _p2p_slabs_vs_whole(name, world, devices, monkeypatch, wait=None):
     from oracle import oracle as O
+    if wait:
+        monkeypatch.setenv("SPLBM_P2P_WAIT", wait)
     factory, a, per = CASES[name]
     g = factory()
     m = P.FluidModel(tau=0.8)
     whole = P.TileEngineT2C(g, a, m, per)
     whole.initialize(O.wavy)
-    slabs = slab.plan_slabs(slab.plane_tile_counts(g, a, per), world)
-    ranks = [P.TileEngineT2C(g, a, m, per, slab=s) for s in slabs]
+    slabs = slab.plan_slabs(slab.plane_tile_counts(g, a, per), world,
+                            min_planes=slab.min_planes(world, P.Periodicity.of(per), g.d))
+    ranks = [P.TileEngineT2C(g, a, m, per, slab=s, device=devices[r % len(devices)])
+             for r, s in enumerate(slabs)]
     blobs = [e.ipc_blob() for e in ranks]
     ax_per = P.Periodicity.of(per).axis(2 if g.d == 3 else 1)
     for r, e in enumerate(ranks):
@@ -129,3 +128,28 @@ def test_p2p_peer_store_slabs_match_whole(name, world):
         mine = e.get_pdf()[lay["n_low"] * st:(lay["n_low"] + n) * st]
         fluid = np.broadcast_to((tg.types[g0:g0 + n] != 0)[:, None, :], (n, whole.q, whole.n_tn)).ravel()
         assert np.array_equal(mine[fluid].view(np.uint64), wp[g0 * st:(g0 + n) * st][fluid].view(np.uint64))
+
+
+@pytest.mark.parametrize("wait", ["auto", "kernel"])
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_p2p_peer_store_slabs_match_whole(name, world, wait, monkeypatch):
+    """Fused exchange: the boundary-plane kernel stores its faces straight into the neighbours'
+    halo tiles, ordered by GPU-side flag waits/writes (same-process peers on one GPU; across
+    processes the blob carries CUDA IPC handles). Bitwise equal to the single engine. `wait`:
+    the halo-arrival wait the device supports (stream wait + remote-write flush, else the
+    acquire-polling kernel) or the polling kernel forced."""
+    _p2p_slabs_vs_whole(name, world, [0], monkeypatch, None if wait == "auto" else wait)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_p2p_slabs_on_distinct_devices(name, world, monkeypatch):
+    """One process driving two or more physical GPUs: slab engines on distinct devices store their
+    faces into each other's halos over NVLink (peer access enabled by p2p_attach). Skips on a
+    one-GPU box."""
+    import torch
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs two or more GPUs")
+    _p2p_slabs_vs_whole(name, world, list(range(n)), monkeypatch)

@@ -29,7 +29,7 @@ def _geom(name):
     return P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=(24, 20, 48))), 4, 0
 
 
-def _worker(rank, world, port, name, transport, q):
+def _worker(rank, world, port, name, transport, q, spread=False):
     try:
         import torch.distributed as dist
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -39,10 +39,12 @@ def _worker(rank, world, port, name, transport, q):
         from paper_1703_08015_b200 import slab
         g, a, per = _geom(name)
         m = P.FluidModel(tau=0.8)
+        import torch
+        dev = rank % torch.cuda.device_count() if spread else 0
         if transport == "p2p":  # CUDA IPC peer stores between the processes
-            run = slab.SlabRun(g, a, m, per, rank, world, 0, transport="p2p")
+            run = slab.SlabRun(g, a, m, per, rank, world, dev, transport="p2p")
         else:  # torch HaloExchange over gloo through host memory
-            run = slab.SlabRun(g, a, m, per, rank, world, 0, host_staged=True)
+            run = slab.SlabRun(g, a, m, per, rank, world, dev, host_staged=True)
         run.initialize(O.wavy)
         run.step_async(STEPS)
         ok, _ = run.sync()
@@ -65,15 +67,13 @@ def _worker(rank, world, port, name, transport, q):
         q.put((rank, False, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("transport", ["torch", "p2p"])
-@pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("name", ["ras40_periodic", "channel3d"])
-def test_slabrun_processes_match_whole(name, world, transport):
+def _run(name, world, transport, spread=False):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, name, transport, q)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, name, transport, q, spread))
+          for r in range(world)]
     for p in ps:
         p.start()
     res = [q.get(timeout=600) for _ in ps]
@@ -81,3 +81,21 @@ def test_slabrun_processes_match_whole(name, world, transport):
         p.join(timeout=60)
     assert all(r[1] for r in res), res
     assert all(r[2] == STEPS for r in res)
+
+
+@pytest.mark.parametrize("transport", ["torch", "p2p"])
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name", ["ras40_periodic", "channel3d"])
+def test_slabrun_processes_match_whole(name, world, transport):
+    _run(name, world, transport)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("name", ["ras40_periodic", "channel3d"])
+def test_slabrun_processes_on_distinct_devices(name, world):
+    """One process per physical GPU (rank r on device r mod N), faces stored across processes
+    and devices over CUDA IPC + NVLink. Skips on a one-GPU box."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two or more GPUs")
+    _run(name, world, "p2p", spread=True)
