@@ -439,51 +439,66 @@ def run_ours(args):
     if not args.no_other:
         line["other_configs"] = other_configs(P, min(K, 64), max(W, 3), peak)
     line["e2e"] = e2e_public_api(P, g, 1000, bench_steps=K)  # configs[1] is a 1000-step run
+    if not args.no_configs4:  # the north-star 1024^3 point (BASELINE configs[4], N=1)
+        line["configs4"] = configs4_point(P, args.c4_size, args.c4_phi, K, W, False,
+                                          (peak, peak_kind))
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(dims)
     print(json.dumps(line))
     return 0
 
 
-def run_big(args):
-    """--config ras1024: BASELINE configs[4] on ONE B200 (the 1-GPU point of the 1024^3 curve):
-    RAS 1024^3, d=40, seed 7, periodic, tiles 4^3, porosity --phi (only phi <~ 0.35 fits with two
-    PDF copies in 180 GB; --single-copy, the in-place AA propagation, fits phi up to ~0.8)."""
-    import paper_1703_08015_b200 as P
-    peak, peak_kind = measured_peaks()
-    if int(os.environ.get("WORLD_SIZE", "1")) > 1:  # strong scaling across ranks (z-slabs)
-        from paper_1703_08015_b200 import slab
-        return slab.bench_main(args, P, clock_sampler=ClockSampler, peak=(peak, peak_kind),
-                               ras1024=True)
+def configs4_point(P, size, phi, steps, warmup, single_copy=False, peak=(6547.2, "measured")):
+    """BASELINE configs[4] on ONE B200 (the N=1 point of the 1024^3 curve): RAS size^3, d=40,
+    seed 7, periodic, tiles 4^3, porosity target `phi`, the raster generated on the GPU (same bytes
+    as the host generator). Two PDF copies fit phi <~ 0.35 in 180 GB; single copy (AA) up to ~0.8."""
     t0 = time.time()
-    g = P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(1024, 1024, 1024), sphere_diameter=40,
-                                                          target_porosity=args.phi, seed=7),
-                   device=0)  # the sphere loop on the GPU (same raster as the host generator)
+    g = P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(size, size, size), sphere_diameter=40,
+                                                          target_porosity=phi, seed=7), device=0)
     t_gen = time.time() - t0
     t0 = time.time()
-    eng = P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8), (1, 1, 1), single_copy=args.single_copy)
+    eng = P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8), (1, 1, 1), single_copy=single_copy)
     t_build = time.time() - t0
     eng.initialize_uniform(1.0, (0.01, 0.005, 0.0))
-    ms, launches, clocks = time_steps(eng, args.steps, args.warmup)
+    ms, launches, clocks = time_steps(eng, steps, warmup)
     nf = eng.fluid_nodes()
-    mlups = nf * args.steps / (ms * 1e-3) / 1e6
+    mlups = nf * steps / (ms * 1e-3) / 1e6
     gbs = mlups * 1e6 * B_NODE[3] / 1e9
     red = eng.reduce()
-    print(json.dumps({
-        "metric": METRIC,
-        "value": round(mlups, 1), "unit": "MLUPS", "n_gpus": 1, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
-        "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"configs[4] RAS 1024^3 d=40 seed 7 periodic, phi target {args.phi}"
-                               + (", single-copy (AA) propagation" if args.single_copy else ""),
-                   "phi": round(P.porosity(g).phi, 4), "phi_t": round(eng.info.phi_t, 4),
-                   "tiles": int(eng.info.n_tiles), "fluid_nodes": nf,
-                   "device_gb": round(eng.info.device_bytes / 1e9, 1)},
-        "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(gbs / peak, 4), "peak_source": peak_kind},
-        "gpu_launches": int(launches), "clocks": clocks, "mass": red["mass"],
-        "non_finite": red["non_finite"], "host_seconds": {"generate": round(t_gen, 1),
-                                                         "engine_build": round(t_build, 1)}}))
+    out = {"workload": f"configs[4] RAS {size}^3 d=40 seed 7 periodic, phi target {phi}, tiles 4^3, "
+                       + ("single-copy (AA) propagation" if single_copy else "two PDF copies"),
+           "value": round(mlups, 1), "unit": "MLUPS", "steps": steps, "warmup": warmup,
+           "ms_per_step": round(ms / steps, 4),
+           "phi": round(P.porosity(g).phi, 4), "phi_t": round(eng.info.phi_t, 4),
+           "tiles": int(eng.info.n_tiles), "fluid_nodes": nf,
+           "device_gb": round(eng.info.device_bytes / 1e9, 1),
+           "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak[0], "unit": "GB/s",
+                        "frac": round(gbs / peak[0], 4), "peak_source": peak[1],
+                        "bu_of_8tbs": round(gbs / 8000.0, 4)},
+           "gpu_launches": int(launches), "clocks": clocks, "mass": red["mass"],
+           "non_finite": red["non_finite"],
+           "host_seconds": {"generate": round(t_gen, 2), "engine_build": round(t_build, 2)}}
+    del eng
+    return out
+
+
+def run_big(args):
+    """--config ras1024: BASELINE configs[4] on ONE B200 (see configs4_point); under torchrun
+    the slab strong-scaling run of the same domain."""
+    import paper_1703_08015_b200 as P
+    peak = measured_peaks()
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:  # strong scaling across ranks (z-slabs)
+        from paper_1703_08015_b200 import slab
+        return slab.bench_main(args, P, clock_sampler=ClockSampler, peak=peak, ras1024=True)
+    c = configs4_point(P, args.c4_size, args.phi, args.steps, args.warmup, args.single_copy, peak)
+    line = {"metric": METRIC, "value": c.pop("value"), "unit": c.pop("unit"), "n_gpus": 1,
+            "steps": c.pop("steps"), "warmup": c.pop("warmup"), "ms_per_step": c.pop("ms_per_step"),
+            "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": c.pop("workload"), "phi": c.pop("phi"), "phi_t": c.pop("phi_t"),
+                       "tiles": c.pop("tiles"), "fluid_nodes": c.pop("fluid_nodes"),
+                       "device_gb": c.pop("device_gb")}}
+    line.update(c)
+    print(json.dumps(line))
     return 0
 
 
@@ -500,6 +515,10 @@ def main():
     ap.add_argument("--phi", type=float, default=0.2)
     ap.add_argument("--single-copy", action="store_true",
                     help="ras1024: in-place AA propagation (one PDF array)")
+    ap.add_argument("--no-configs4", action="store_true",
+                    help="skip the BASELINE configs[4] point (N=1) / strong-scaling key (N>1)")
+    ap.add_argument("--c4-size", type=int, default=1024, help="configs[4] RAS edge (validation runs)")
+    ap.add_argument("--c4-phi", type=float, default=0.2, help="configs[4] porosity target")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

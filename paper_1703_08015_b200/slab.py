@@ -296,6 +296,86 @@ class SlabRun:
         return self.engine.sync()
 
 
+def configs4_strong(P, rank, world, device, size=1024, phi=0.2, steps=20, warmup=5,
+                    transport="p2p", single_copy_ref=False):
+    """BASELINE configs[4] strong scaling inside a torchrun job: the RAS size^3 (d 40, seed 7,
+    periodic, phi target `phi`) split into z-slabs balanced by non-empty tiles, `steps` timed steps
+    (CUDA events on the engine stream, max over ranks), then rank 0 alone steps the whole domain
+    on its GPU (the N=1 point of the same job) so the efficiency is against a same-box N=1.
+    Returns the dict rank 0 attaches as `configs4_strong` (None on the other ranks)."""
+    import torch
+    import torch.distributed as dist
+    red = torch.device("cuda", device) if dist.get_backend() == "nccl" else torch.device("cpu")
+
+    def allred(v, op):
+        t = torch.tensor([float(v)], dtype=torch.float64, device=red)
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    per = (1, 1, 1)
+    params = P.GenerateParams(dims=(size, size, size), sphere_diameter=40, target_porosity=phi,
+                              seed=7)
+    g = P.generate(P.GeometryKind.Ras3D, params, device=device)
+    slabs = plan_slabs(plane_tile_counts(g, 4, Periodicity.of(per)), world,
+                       min_planes(world, per, g.d))
+    run = SlabRun(g, 4, P.FluidModel(tau=0.8), per, rank, world, device, slabs=slabs,
+                  transport=transport)
+    eng = run.engine
+    eng.initialize_uniform(1.0, (0.01, 0.005, 0.0))
+    dist.barrier()
+    run.step_async(warmup)
+    ok_w, _ = run.sync()
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(run.stream):
+        start.record()
+    run.step_async(steps)
+    with torch.cuda.stream(run.stream):
+        stop.record()
+    ok, _ = run.sync()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = allred(start.elapsed_time(stop), dist.ReduceOp.MAX) * 1e-3
+    nf_local = eng.fluid_nodes()
+    nf = allred(nf_local, dist.ReduceOp.SUM)
+    tiles = allred(eng.info.n_tiles, dist.ReduceOp.SUM)
+    all_ok = allred(1.0 if (ok and ok_w) else 0.0, dist.ReduceOp.MIN) == 1.0
+    loads = [None] * world
+    dist.all_gather_object(loads, (int(nf_local), int(eng.info.n_tiles)))
+    del run, eng
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    dist.barrier()
+    out = None
+    if rank == 0:
+        whole = P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8), per, device=device)
+        whole.initialize_uniform(1.0, (0.01, 0.005, 0.0))
+        ok1, _ = whole.step_n(warmup)
+        whole.step_async(steps)
+        ok2, _ = whole.sync()
+        t1 = whole.last_batch_ms() * 1e-3
+        v1 = nf * steps / t1 / 1e6
+        vN = nf * steps / t / 1e6
+        out = {"workload": f"configs[4] RAS {size}^3 d=40 seed 7 periodic, phi target {phi}, "
+                           f"tiles 4^3, two PDF copies, z-slabs balanced by non-empty tiles",
+               "scaling": "strong", "n_gpus": world, "steps": steps, "warmup": warmup,
+               "value": round(vN, 1), "unit": "MLUPS", "ms_per_step": round(t / steps * 1e3, 4),
+               "n1_value": round(v1, 1), "n1_ms_per_step": round(t1 / steps * 1e3, 4),
+               "efficiency": round(vN / (world * v1), 4), "ok": bool(all_ok and ok1 and ok2),
+               "phi": round(P.porosity(g).phi, 4), "fluid_nodes": int(nf), "tiles": int(tiles),
+               "per_rank": [{"slab": list(slabs[r]), "fluid_nodes": loads[r][0],
+                             "tiles": loads[r][1]} for r in range(world)],
+               "transport": transport, "devices": torch.cuda.device_count(),
+               "achieved_gbs_per_gpu": round(vN * 1e6 * 304 / world / 1e9, 1)}
+        del whole
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+    dist.barrier()
+    return out
+
+
 def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured"), ras1024=False,
                config_fn=None) -> int:
     """bench.py at N>1 (torchrun). Default: weak scaling — each rank owns a 128^3-node slab of one
@@ -438,6 +518,14 @@ def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured"), ras1024=F
         }
         if sampler:
             line["clocks"] = sampler.summary()
+    if not ras1024 and not getattr(args, "no_configs4", False):
+        # the north-star curve (BASELINE configs[4]) beside the weak-scaled headline value
+        c4 = configs4_strong(P, rank, world, device, size=getattr(args, "c4_size", 1024),
+                             phi=getattr(args, "c4_phi", 0.2), steps=args.steps,
+                             warmup=args.warmup, transport=transport)
+        if rank == 0:
+            line["configs4_strong"] = c4
+    if rank == 0:
         print(json.dumps(line))
     dist.destroy_process_group()
     return 0

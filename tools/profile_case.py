@@ -27,7 +27,13 @@ if __name__ == "__main__":
         print(name, "phi", P.porosity(g).phi)
         sys.exit(0)
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 6
-    g, a, per = CASES[name]()
+    if name.startswith("ras1024_phi"):  # BASELINE configs[4] on one GPU (device-generated raster)
+        phi = float("0." + name.split("phi0")[1])
+        g = P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(1024, 1024, 1024), sphere_diameter=40,
+                                                              target_porosity=phi, seed=7), device=0)
+        a, per = 4, 7
+    else:
+        g, a, per = CASES[name]()
     coll = P.CollisionKind.MRT if os.environ.get("SPLBM_MODEL") == "mrt" else P.CollisionKind.BGK
     e = P.TileEngineT2C(g, a, P.FluidModel(collision=coll, tau=0.8), per,
                         single_copy=os.environ.get("SPLBM_SINGLE_COPY") == "1",
