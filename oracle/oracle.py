@@ -48,6 +48,10 @@ def lib():
     L.oracle_t2c_step.argtypes = [C.c_int, C.c_int, C.c_int64, _u8, _u32, _u8, _dp, _dp,
                                   C.c_double, C.c_int, _dp, C.c_double, C.c_int, C.c_void_p]
     L.oracle_mrt_kernel.argtypes = [C.c_int, C.c_double, C.c_void_p, _dp]
+    # host model of the product's single-copy (AA) ordering (slab-exchange tests)
+    L.oracle_aa_step.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, _u8, _u32, _u8, _dp,
+                                 C.c_int, C.c_double, C.c_int, _dp, C.c_double]
+    L.oracle_aa_step.restype = C.c_int
     L.oracle_t2c_step.restype = C.c_int
     L.oracle_fields.argtypes = [C.c_int, C.c_int, C.c_int64, _i32, _u8, _i32, _dp, C.c_int, _dp,
                                 _dp, _dp, _dp, _u8]

@@ -17,7 +17,12 @@ def face_dirs(d):
 
 
 class HostSlabRank:
-    def __init__(self, O, g, a, tau, per, z0, z1, inc=False):
+    """single_copy=True: one PDF array stepped with the AA ordering (oracle_aa_step, owned tiles
+    only); before a phase-1 step the owners' natural-state faces go to the neighbours' halos
+    (pack/unpack), after it the halo face slots the scatter wrote go back to their owners
+    (pack_back/unpack_back) — the schedule of SlabRun's torch transport in single-copy mode."""
+
+    def __init__(self, O, g, a, tau, per, z0, z1, inc=False, single_copy=False):
         self.O, self.g, self.a = O, g, a
         self.d = g.d
         self.q = 9 if g.d == 2 else 19
@@ -41,11 +46,22 @@ class HostSlabRank:
         O.lib().oracle_t2c_initialize(g.d, self.S, self.n_tn, int(inc), rho, ux, uy, uz,
                                       self.pdf[0], self.pdf[1])
         self.read = 0
+        self.single_copy = single_copy
+        self.state = 0  # single copy: 0 natural layout, 1 swapped
         self.inv_tau = 1.0 / tau
         self.inc = int(inc)
         self.ups, self.downs = face_dirs(g.d)
 
     def step(self):
+        if self.single_copy:
+            L = self.lay
+            ok = self.O.lib().oracle_aa_step(self.d, self.a, L["n_low"], L["n_low"] + L["n_own"],
+                                             self.ttypes, self.nb, self.bcdeg, self.pdf[0],
+                                             1 + self.state, self.inv_tau, self.inc,
+                                             np.asarray(self.g.bc.velocity, np.float64),
+                                             self.g.bc.density)
+            self.state ^= 1
+            return ok
         ok = self.O.lib().oracle_t2c_step(self.d, self.a, self.S, self.ttypes, self.nb, self.bcdeg,
                                           self.pdf[self.read], self.pdf[1 - self.read], self.inv_tau,
                                           self.inc, np.asarray(self.g.bc.velocity, np.float64),
@@ -75,6 +91,60 @@ class HostSlabRank:
             cur[self._slots(0, L["n_low"], self.a - 1, self.ups)] = lo.numpy()
         if hi is not None and hi.numel():
             cur[self._slots(L["n_low"] + L["n_own"], L["n_high"], 0, self.downs)] = hi.numpy()
+
+    def pack_back(self, lo, hi):
+        """Single copy, after a phase-1 step: the halo face slots my scatter wrote (low halo top
+        layer, upward dirs; high halo bottom layer, downward dirs) go back to their owners."""
+        L = self.lay
+        cur = self.pdf[0]
+        if lo.numel():
+            lo.numpy()[:] = cur[self._slots(0, L["n_low"], self.a - 1, self.ups)]
+        if hi.numel():
+            hi.numpy()[:] = cur[self._slots(L["n_low"] + L["n_own"], L["n_high"], 0, self.downs)]
+
+    def _written_by_neighbour(self, tile0, ntiles, layer, dirs):
+        """Per slot (x, k) of an owned face: did the neighbour's phase-1 scatter write it? Only
+        when the downstream node x + e_k exists and is non-solid (its gather of k from x is not
+        blocked); otherwise x's own bounce-back owns the slot and it must not be overwritten."""
+        lat = P.solver_lattice(self.d)
+        a, d = self.a, self.d
+        out = np.zeros((ntiles, len(dirs), self.face), bool)
+        for ti in range(ntiles):
+            t = tile0 + ti
+            for jn, k in enumerate(dirs):
+                e = lat.e[k]
+                for f in range(self.face):
+                    p = layer * self.face + f
+                    l = [p % a, (p // a) % a, p // (a * a)] if d == 3 else [p % a, p // a, 0]
+                    dc = [0, 0, 0]
+                    for c in range(d):
+                        l[c] += e[c]
+                        if l[c] < 0:
+                            dc[c], l[c] = -1, l[c] + a
+                        elif l[c] >= a:
+                            dc[c], l[c] = 1, l[c] - a
+                    s = self.nb[t * 27 + (dc[0] + 1) + 3 * ((dc[1] + 1) + 3 * (dc[2] + 1))]
+                    if s != 0xFFFFFFFF:
+                        out[ti, jn, f] = self.ttypes[s * self.n_tn + l[0] + a * (l[1] + a * l[2])] != 0
+        return out.ravel()
+
+    def unpack_back(self, lo, hi):
+        L = self.lay
+        cur = self.pdf[0]
+        if lo is not None and lo.numel():
+            args = (L["n_low"], L["send_low_tiles"], 0, self.downs)
+            m = self._written_by_neighbour(*args)
+            cur[self._slots(*args)[m]] = lo.numpy()[m]
+        if hi is not None and hi.numel():
+            args = (L["n_low"] + L["n_own"] - L["send_high_tiles"], L["send_high_tiles"], self.a - 1,
+                    self.ups)
+            m = self._written_by_neighbour(*args)
+            cur[self._slots(*args)[m]] = hi.numpy()[m]
+
+    def sizes_back(self):
+        f = self.sizes()
+        return {"send_low": f["recv_low"], "send_high": f["recv_high"], "recv_low": f["send_low"],
+                "recv_high": f["send_high"]}
 
     def sizes(self):
         L = self.lay

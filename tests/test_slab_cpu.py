@@ -28,7 +28,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, name, q):
+def _worker(rank, world, port, name, q, single_copy=False):
     try:
         import torch
         import torch.distributed as dist
@@ -40,13 +40,23 @@ def _worker(rank, world, port, name, q):
         g = factory()
         slabs = slab.plan_slabs(slab.plane_tile_counts(g, a, per), world)
         z0, z1 = slabs[rank]
-        m = HostSlabRank(O, g, a, 0.8, per, z0, z1)
+        m = HostSlabRank(O, g, a, 0.8, per, z0, z1, single_copy=single_copy)
         ax_per = P.Periodicity.of(per).axis(2 if g.d == 3 else 1)
-        xchg = slab.HaloExchange(rank, world, ax_per, m.sizes(),
-                                 lambda n: torch.zeros(n, dtype=torch.float64), slab.TorchComm())
-        for _ in range(STEPS):
-            assert m.step()
-            xchg.exchange(m.pack, m.unpack)
+        alloc = lambda n: torch.zeros(n, dtype=torch.float64)
+        xchg = slab.HaloExchange(rank, world, ax_per, m.sizes(), alloc, slab.TorchComm())
+        if single_copy:
+            xback = slab.HaloExchange(rank, world, ax_per, m.sizes_back(), alloc, slab.TorchComm())
+            for _ in range(STEPS):  # STEPS is even: the final state is in the natural layout
+                if m.state == 0:
+                    xchg.exchange(m.pack, m.unpack)
+                    assert m.step()
+                    xback.exchange(m.pack_back, m.unpack_back)
+                else:
+                    assert m.step()
+        else:
+            for _ in range(STEPS):
+                assert m.step()
+                xchg.exchange(m.pack, m.unpack)
         # full-domain oracle
         full = O.OracleT2C(g.types, g.d, g.dims, a, 0.8, periodic=per, bc_velocity=g.bc.velocity,
                            bc_density=g.bc.density)
@@ -66,14 +76,16 @@ def _worker(rank, world, port, name, q):
         q.put((rank, False, repr(ex), traceback.format_exc()))
 
 
+@pytest.mark.parametrize("single_copy", [False, True], ids=["two_copy", "single_copy"])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_slab_exchange_matches_single_domain(name, world, oracle):
+def test_slab_exchange_matches_single_domain(name, world, single_copy, oracle):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q, single_copy))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in procs]
