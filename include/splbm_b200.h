@@ -232,6 +232,17 @@ int splbm_dev_halo_pack(splbm_dev_engine* e, void* low_dev, void* high_dev);
 int splbm_dev_step_part(splbm_dev_engine* e, int part);
 int splbm_dev_halo_pack_next(splbm_dev_engine* e, void* low_dev, void* high_dev);
 int splbm_dev_halo_unpack(splbm_dev_engine* e, const void* low_dev, const void* high_dev);
+/* Single-copy (single_copy = 1) slab engines. Before a step from the natural layout (current_step
+ * even) the faces go forward as above (pack / unpack). After that step the halo slots its scatter
+ * wrote go back to their owners: pack_back writes the low halo plane's layer a-1, upward dirs
+ * (low, to the lower neighbour; size = recv low bytes) and the high halo plane's layer 0, downward
+ * dirs (high, to the upper neighbour); unpack_back stores what the lower neighbour sent as `high`
+ * into my bottom plane's layer 0 and what the upper neighbour sent as `low` into my top plane's
+ * layer a-1 — only the slots whose downstream node is non-solid (the others belong to this node's
+ * own bounce-back). Steps from the swapped layout need no exchange. fields/get_pdf/reduce of a
+ * slab engine need the natural layout (an even step count). */
+int splbm_dev_halo_pack_back(splbm_dev_engine* e, void* low_dev, void* high_dev);
+int splbm_dev_halo_unpack_back(splbm_dev_engine* e, const void* low_dev, const void* high_dev);
 
 /* Native exchange (no per-step host work beyond enqueueing): rank 0 creates an NCCL unique id
  * (128 bytes) and every rank passes it to splbm_dev_comm_attach with its lower/upper slab
@@ -246,7 +257,9 @@ int splbm_dev_comm_attach(splbm_dev_engine* e, const uint8_t* id, int world, int
  * flags with GPU-side stream waits/writes — no pack, no unpack, no host synchronisation. Every rank
  * exports its blob (SPLBM_IPC_BLOB_BYTES bytes), the blobs reach the neighbours out of band, then
  * each rank attaches its lower/upper neighbour's blob (NULL at a non-periodic edge). All ranks
- * must initialize before any rank steps. */
+ * must initialize before any rank steps. Single-copy engines: the boundary planes' steps from the
+ * natural layout read and write the halo nodes' slots in place in the neighbours' owned tiles
+ * (each slot has exactly one reader/writer), so no halo copy is involved at all. */
 #define SPLBM_IPC_BLOB_BYTES 512
 int splbm_dev_ipc_blob(splbm_dev_engine* e, uint8_t* blob_out);
 int splbm_dev_p2p_attach(splbm_dev_engine* e, const uint8_t* lower_blob, const uint8_t* upper_blob);

@@ -101,6 +101,8 @@ SIGNATURES = {
     "splbm_dev_halo_recv_bytes": ([_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)], C.c_int),
     "splbm_dev_halo_pack": ([_vp, C.c_void_p, C.c_void_p], C.c_int),
     "splbm_dev_halo_unpack": ([_vp, C.c_void_p, C.c_void_p], C.c_int),
+    "splbm_dev_halo_pack_back": ([_vp, C.c_void_p, C.c_void_p], C.c_int),
+    "splbm_dev_halo_unpack_back": ([_vp, C.c_void_p, C.c_void_p], C.c_int),
     "splbm_dev_step_part": ([_vp, C.c_int], C.c_int),
     "splbm_comm_unique_id": ([C.c_void_p], C.c_int),
     "splbm_dev_ipc_blob": ([_vp, C.c_void_p], C.c_int),

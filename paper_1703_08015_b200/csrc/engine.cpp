@@ -148,6 +148,8 @@ struct splbm_dev_engine {
   unsigned long long* peer_flags_up = nullptr;
   unsigned long long* peer_flags_down = nullptr;
   uint64_t peer_down_halo0 = 0;  // first high-halo tile of the lower neighbour
+  uint64_t peer_down_own0 = 0;   // single copy: first top-plane tile of the lower neighbour
+  uint64_t peer_up_own0 = 0;     // single copy: first bottom-plane tile of the upper neighbour
   unsigned long long comm_seq = 0;
   // p2p halo-arrival wait: cuStreamWaitValue64 with CU_STREAM_WAIT_VALUE_FLUSH where the device
   // can flush remote writes (CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES), else the acquire-polling
@@ -230,7 +232,14 @@ struct splbm_dev_engine {
     s.pdl_min_threads = pdl_min_threads;
     s.x2 = x2;
     s.off32 = off32 && n_stored * tile_stride() < (1ull << 32);
-    if (peer_part1) {
+    if (peer_part1 && aa) {  // single copy: phase 1 reads/writes the halo nodes' slots in place
+      if (rd == 0) {
+        s.peer_down = peer_pdf_down[0] ? peer_pdf_down[0] + peer_down_own0 * tile_stride() : nullptr;
+        s.peer_up = peer_pdf_up[0] ? peer_pdf_up[0] + peer_up_own0 * tile_stride() : nullptr;
+        s.halo_lo_end = n_low;
+        s.halo_hi_begin = n_low + n_own;
+      }
+    } else if (peer_part1) {
       s.peer_up = peer_pdf_up[1 - rd];
       s.peer_down = peer_pdf_down[1 - rd] ? peer_pdf_down[1 - rd] + peer_down_halo0 * tile_stride() : nullptr;
       s.top_begin = n_low + n_own - send_high_tiles;
@@ -253,7 +262,6 @@ struct splbm_dev_engine {
   // Slab-overlap parts: 1 = the bottom and top owned planes (their faces are exchanged while
   // part 2, the interior planes, runs); part 2 then swaps the copies and counts the step.
   void step_part(int part, cudaEvent_t before_bump = nullptr) {
-    if (aa) throw config_error("the slab step parts need the two-copy scheme");
     const uint64_t b0 = n_low, b1 = n_low + send_low_tiles;          // bottom plane
     const uint64_t t0 = n_low + n_own - send_high_tiles, t1 = n_low + n_own;  // top plane
     const bool merged = b1 >= t0;  // one or two planes: the boundary covers the whole slab
@@ -285,11 +293,11 @@ struct splbm_dev_engine {
 
   // Face pack / unpack on the engine stream (see splbm_dev_halo_pack / _unpack for the layout).
   void halo_copy(int copy, uint64_t tile0, uint64_t ntiles, int layer, const int* dirs, double* buf,
-                 bool pack) {
-    if (aa) throw config_error("slab halo exchange needs the two-copy scheme");
+                 bool pack, bool mask = false) {
     if (f32) throw config_error("slab halo exchange is built for the f64 engine");
     if (!ntiles || !buf) return;
-    splbm_dev::HaloArgs h{static_cast<double*>(pdf[copy]), buf, tile0, ntiles, a, layer, n_halo_dirs, dirs, pack ? 1 : 0};
+    splbm_dev::HaloArgs h{static_cast<double*>(aa ? pdf[0] : pdf[copy]), buf, tile0, ntiles, a, layer,
+                          n_halo_dirs, dirs, pack ? 1 : 0, mask ? info : nullptr};
     CK(splbm_dev::launch_halo(d, h, stream));
     ++launches;
   }
@@ -300,6 +308,19 @@ struct splbm_dev_engine {
   void unpack_faces(int copy, double* low, double* high) {
     halo_copy(copy, 0, n_low, a - 1, halo_dirs, low, false);
     halo_copy(copy, n_low + n_own, n_high, 0, halo_dirs + n_halo_dirs, high, false);
+  }
+  // Single copy, after a phase-1 step: the halo slots my scatter wrote go back to their owners
+  // (low halo, top layer, upward dirs -> lower rank; high halo, bottom layer, downward dirs ->
+  // upper rank), and the owners store only the slots whose downstream node is non-solid.
+  void pack_back(double* low, double* high) {
+    if (!aa) throw config_error("the backward face exchange is the single-copy scheme's");
+    halo_copy(0, 0, n_low, a - 1, halo_dirs, low, true);
+    halo_copy(0, n_low + n_own, n_high, 0, halo_dirs + n_halo_dirs, high, true);
+  }
+  void unpack_back(double* low, double* high) {
+    if (!aa) throw config_error("the backward face exchange is the single-copy scheme's");
+    halo_copy(0, n_low, send_low_tiles, 0, halo_dirs + n_halo_dirs, low, false, true);
+    halo_copy(0, n_low + n_own - send_high_tiles, send_high_tiles, a - 1, halo_dirs, high, false, true);
   }
 
   // One step of the multi-GPU slab mode: boundary planes, pack their faces, NCCL send/recv on the
@@ -486,8 +507,6 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
   if (desc->single_copy) {  // single PDF array, AA access pattern
     const bool pow2 = e->a == 2 || e->a == 4 || (d == 2 && (e->a == 8 || e->a == 16));
     if (!pow2) throw config_error("single-copy propagation needs a power-of-two tile (a = 2, 4; 2D a <= 16)");
-    if (desc->slab_z0 != 0 || desc->slab_z1 != 0)
-      throw config_error("single-copy propagation is a single-GPU mode (no slab)");
     e->aa = true;
   }
   // ---- device ------------------------------------------------------------------------------
@@ -690,6 +709,13 @@ void host_tm(splbm_dev_engine* e) {
   e->tb_bytes = 0;
 }
 
+// A single-copy slab engine in the swapped layout has some of its post-collision values in the
+// neighbours' memory (p2p) or in its halo copies: its state is readable after an even step count.
+void natural_slab_state(const splbm_dev_engine* e) {
+  if (e->aa && e->read == 1 && (e->n_low || e->n_high))
+    throw config_error("single-copy slab state is readable after an even number of steps");
+}
+
 void check_domain_flag(splbm_dev_engine* e, const char* msg) {
   int flag = 0;
   CK(cudaMemcpyAsync(&flag, e->domain_err, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
@@ -888,6 +914,7 @@ int splbm_dev_fields(splbm_dev_engine* e, double* rho, double* ux, double* uy, d
                      uint8_t* mask, double* mass_out) {
   return guarded([&] {
     checked(e);
+    natural_slab_state(e);
     const int* dims = e->tm.dims;
     const std::size_t n = static_cast<std::size_t>(dims[0]) * dims[1] * dims[2];
     std::vector<double> own_rho;
@@ -994,6 +1021,7 @@ int splbm_dev_fields(splbm_dev_engine* e, double* rho, double* ux, double* uy, d
 int splbm_dev_reduce(splbm_dev_engine* e, double out[3]) {
   return guarded([&] {
     checked(e);
+    natural_slab_state(e);
     const int blocks = 1184;  // 8 x 148 SMs, fixed so the summation order is fixed
     if (!e->reduce_buf) e->reduce_buf = e->alloc<double>(3 * blocks + 3);  // kept: no per-call cudaMalloc
     double* dev = e->reduce_buf;
@@ -1012,6 +1040,7 @@ int splbm_dev_reduce(splbm_dev_engine* e, double out[3]) {
 int splbm_dev_get_pdf(splbm_dev_engine* e, void* f_out) {
   return guarded([&] {
     checked(e);
+    natural_slab_state(e);
     const uint64_t tile_bytes = e->tile_stride() * e->es;
     char* out = static_cast<char*>(f_out);
     if (!e->view().swapped) {
@@ -1097,6 +1126,21 @@ int splbm_dev_halo_unpack(splbm_dev_engine* e, const void* low_dev, const void* 
   });
 }
 
+int splbm_dev_halo_pack_back(splbm_dev_engine* e, void* low_dev, void* high_dev) {
+  return guarded([&] {
+    checked(e);
+    e->pack_back(static_cast<double*>(low_dev), static_cast<double*>(high_dev));
+  });
+}
+
+int splbm_dev_halo_unpack_back(splbm_dev_engine* e, const void* low_dev, const void* high_dev) {
+  return guarded([&] {
+    checked(e);
+    e->unpack_back(const_cast<double*>(static_cast<const double*>(low_dev)),
+                   const_cast<double*>(static_cast<const double*>(high_dev)));
+  });
+}
+
 // IPC blob of a slab engine: what a neighbour needs to store faces into this engine's halos.
 struct IpcBlob {
   uint32_t magic, version;
@@ -1104,6 +1148,7 @@ struct IpcBlob {
   cudaIpcMemHandle_t pdf[2], flags;
   uint64_t raw_pdf[2], raw_flags;  // same-process peers use the pointers directly
   uint64_t n_low, n_own, n_high, send_low_tiles, send_high_tiles, tile_stride;
+  uint32_t single_copy;
 };
 static_assert(sizeof(IpcBlob) <= SPLBM_IPC_BLOB_BYTES, "blob too large");
 
@@ -1117,13 +1162,15 @@ int splbm_dev_ipc_blob(splbm_dev_engine* e, uint8_t* out) {
     }
     IpcBlob b{};
     b.magic = 0x53504c42u;  // "SPLB"
-    b.version = 1;
+    b.version = 2;
     b.pid = static_cast<int32_t>(getpid());
     b.device = e->device;
     for (int k = 0; k < 2; ++k) {
+      if (!e->pdf[k]) continue;  // single copy: one array
       CK(cudaIpcGetMemHandle(&b.pdf[k], e->pdf[k]));
       b.raw_pdf[k] = reinterpret_cast<uint64_t>(e->pdf[k]);
     }
+    b.single_copy = e->aa ? 1u : 0u;
     CK(cudaIpcGetMemHandle(&b.flags, e->flags));
     b.raw_flags = reinterpret_cast<uint64_t>(e->flags);
     b.n_low = e->n_low;
@@ -1141,14 +1188,14 @@ int splbm_dev_p2p_attach(splbm_dev_engine* e, const uint8_t* lower_blob, const u
   return guarded([&] {
     checked(e);
     if (e->p2p || e->comm) throw config_error("engine already has a halo transport");
-    if (e->aa) throw config_error("slab halo exchange needs the two-copy scheme");
     if (e->f32) throw config_error("slab halo exchange is built for the f64 engine");
     if (!e->mrt_K.empty()) throw config_error("peer-store halos are built for the BGK kernels");
     if (!e->flags) throw config_error("call splbm_dev_ipc_blob before attaching");
     if (e->a != 4 && e->a != 2 && !(e->d == 2 && (e->a == 8 || e->a == 16)))
       throw config_error("peer-store halos need a power-of-two tile kernel (a = 2, 4; 2D a <= 16)");
     auto open = [&](const IpcBlob& b, double** pdf, unsigned long long** fl) {
-      if (b.magic != 0x53504c42u || b.version != 1 || b.tile_stride != e->tile_stride())
+      if (b.magic != 0x53504c42u || b.version != 2 || b.tile_stride != e->tile_stride() ||
+          b.single_copy != (e->aa ? 1u : 0u))
         throw config_error("incompatible peer blob");
       if (b.pid == static_cast<int32_t>(getpid())) {
         if (b.device != e->device) {  // one process driving several GPUs: direct peer access
@@ -1169,6 +1216,10 @@ int splbm_dev_p2p_attach(splbm_dev_engine* e, const uint8_t* lower_blob, const u
         return;
       }
       for (int k = 0; k < 2; ++k) {
+        if (!b.raw_pdf[k]) {
+          pdf[k] = nullptr;
+          continue;
+        }
         void* p = nullptr;
         CK(cudaIpcOpenMemHandle(&p, b.pdf[k], cudaIpcMemLazyEnablePeerAccess));
         e->ipc_opened.push_back(p);
@@ -1185,12 +1236,18 @@ int splbm_dev_p2p_attach(splbm_dev_engine* e, const uint8_t* lower_blob, const u
       if (b.n_high != e->send_low_tiles) throw config_error("lower neighbour's halo does not match my bottom plane");
       open(b, e->peer_pdf_down, &e->peer_flags_down);
       e->peer_down_halo0 = b.n_low + b.n_own;
+      e->peer_down_own0 = b.n_low + b.n_own - b.send_high_tiles;
+      if (e->aa && b.send_high_tiles != e->n_low)
+        throw config_error("lower neighbour's top plane does not match my low halo");
     }
     if (upper_blob) {
       IpcBlob b;
       std::memcpy(&b, upper_blob, sizeof(b));
       if (b.n_low != e->send_high_tiles) throw config_error("upper neighbour's halo does not match my top plane");
       open(b, e->peer_pdf_up, &e->peer_flags_up);
+      e->peer_up_own0 = b.n_low;
+      if (e->aa && b.send_low_tiles != e->n_high)
+        throw config_error("upper neighbour's bottom plane does not match my high halo");
     }
     stream_mem_ops();
     {

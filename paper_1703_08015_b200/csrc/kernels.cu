@@ -479,7 +479,7 @@ __host__ __device__ constexpr int aa_threads() {
   return SPLBM_AA_THREADS > (D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA))) ? SPLBM_AA_THREADS
                                                                              : (D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA)));
 }
-template <int D, int LOGA, bool INC, bool MRT, int PHASE, class R>
+template <int D, int LOGA, bool INC, bool MRT, int PHASE, class R, bool PEER = false>
 __global__ void __launch_bounds__(aa_threads<D, LOGA>(),
                                   (MRT ? 2 : (D == 3 ? (PHASE == 1 ? 3 : SPLBM_MINB3) : SPLBM_MINB2)) * 256 / aa_threads<D, LOGA>())
     t2c_aa_kernel(StepArgs args, const __grid_constant__ MrtMatrix<R, MRT ? Lat<D>::Q : 1> mrt) {
@@ -500,8 +500,13 @@ __global__ void __launch_bounds__(aa_threads<D, LOGA>(),
       const uint64_t tt = tile_blk + tl;
       R* b = nullptr;
       if (tt < n_tiles) {
-        const uint32_t s = __ldg(args.nb + (args.t0 + tt) * NBS + dd);
-        b = s == kEmpty ? nullptr : pdf + static_cast<uint64_t>(s) * STRIDE;
+        const uint32_t s = __ldg(args.nb + (args.t0 + tt + (tt >= args.skip_at ? args.skip_by : 0)) * NBS + dd);
+        if (s == kEmpty) b = nullptr;
+        // slab p2p, phase 1: the slots of halo nodes are read and written in place in the
+        // neighbour's owned tiles over NVLink (each slot is touched by exactly one node, this one)
+        else if (PEER && s < args.halo_lo_end) b = reinterpret_cast<R*>(args.peer_down) + static_cast<uint64_t>(s) * STRIDE;
+        else if (PEER && s >= args.halo_hi_begin) b = reinterpret_cast<R*>(args.peer_up) + static_cast<uint64_t>(s - args.halo_hi_begin) * STRIDE;
+        else b = pdf + static_cast<uint64_t>(s) * STRIDE;
       }
       s_base[tl][dd] = b;
     }
@@ -509,7 +514,7 @@ __global__ void __launch_bounds__(aa_threads<D, LOGA>(),
   const int tl = threadIdx.x / NTN;
   const int p = threadIdx.x % NTN;
   const uint64_t tloc = tile_blk + tl;
-  const uint64_t t = args.t0 + tloc;
+  const uint64_t t = args.t0 + tloc + (tloc >= args.skip_at ? args.skip_by : 0);
   const uint32_t info = tloc < n_tiles ? __ldg(args.info + t * NTN + p) : 0u;
   if constexpr (PHASE == 1) __syncthreads();
 #if SPLBM_PDL
@@ -518,7 +523,8 @@ __global__ void __launch_bounds__(aa_threads<D, LOGA>(),
 #endif
   {
     const uint64_t pf = tile_blk + static_cast<uint64_t>(args.l2pf) * TILES + threadIdx.x;
-    l2_prefetch_blocks<Q, NTN, TILES>(pdf, args.t0 + pf, args.l2pf && pf < n_tiles);
+    l2_prefetch_blocks<Q, NTN, TILES>(pdf, args.t0 + pf + (pf >= args.skip_at ? args.skip_by : 0),
+                                      args.l2pf && pf < n_tiles);
   }
   const int type = (info >> 24) & 3;
   R* own = pdf + t * STRIDE;
@@ -806,10 +812,15 @@ __global__ void halo_copy_kernel(HaloArgs args) {
   const int dir = args.dirs[j];
   const uint64_t slot = ((args.tile0 + tk) * Q + dir) * static_cast<uint64_t>(n_tn) +
                         static_cast<uint64_t>(args.layer) * face + fnode;
-  if (args.pack)
+  if (args.pack) {
     args.buf[k] = args.pdf[slot];
-  else
+  } else {
+    if (args.info) {  // single-copy backward unpack: only slots the neighbour's scatter wrote
+      const uint32_t w = args.info[(args.tile0 + tk) * n_tn + static_cast<uint64_t>(args.layer) * face + fnode];
+      if (((w >> 24) & 3u) == 0u || ((w >> opp(dir)) & 1u)) return;
+    }
     args.pdf[slot] = args.buf[k];
+  }
 }
 
 // Natural-layout copy of a tile range of the current state (parity dumps of a swapped AA state).
@@ -881,6 +892,13 @@ static void launch_maybe_pdl(Kern kern, unsigned blocks, cudaStream_t st, const 
 
 template <int D, int LOGA, bool INC, int PHASE, class R>
 static void launch_aa(const StepArgs& a, unsigned blocks, cudaStream_t st) {
+  if constexpr (PHASE == 1 && std::is_same<R, double>::value) {
+    if (!a.mrt_K && (a.peer_up || a.peer_down)) {  // slab boundary planes, p2p single copy
+      t2c_aa_kernel<D, LOGA, INC, false, 1, R, true>
+          <<<blocks, aa_threads<D, LOGA>(), 0, st>>>(a, MrtMatrix<R, 1>{});
+      return;
+    }
+  }
   if (a.mrt_K)
     launch_maybe_pdl(t2c_aa_kernel<D, LOGA, INC, true, PHASE, R>, blocks, st, a,
                      mrt_param<R, Lat<D>::Q>(a.mrt_K), aa_threads<D, LOGA>());

@@ -40,9 +40,13 @@ struct StepArgs {
   // plane tiles [top_begin, ...) is also stored, for the directions leaving upwards, into the
   // upper neighbour's next copy at its low halo tiles (peer_up = that copy's first halo tile);
   // likewise the bottom plane [bot_begin, bot_end) into the lower neighbour's high halo tiles.
+  // Single copy (aa = 1, phase 1) in slab p2p mode: stored tiles below halo_lo_end are the lower
+  // neighbour's top-plane tiles (peer_down = its first one), tiles from halo_hi_begin on are the
+  // upper neighbour's bottom-plane tiles (peer_up = its first one): read and written in place.
   double* peer_up;
   double* peer_down;
   uint64_t top_begin, bot_begin, bot_end;
+  uint64_t halo_lo_end, halo_hi_begin;
 };
 
 // The MRT operator as a kernel parameter (constant bank): the unrolled K_ij * delta_j products
@@ -123,6 +127,10 @@ struct HaloArgs {
   int n_dirs;
   const int* dirs;  // device array of direction indices
   int pack;         // 1: pdf -> buf, 0: buf -> pdf
+  // unpack only: when set, a slot (x, dir) is written only if x is non-solid and x's gather of
+  // opp(dir) is not blocked (the single-copy backward exchange: the downstream node x + e_dir
+  // exists and is non-solid, so the neighbour's scatter wrote it)
+  const uint32_t* info;
 };
 
 cudaError_t launch_step(int d, bool inc, bool f32, const StepArgs& a, cudaStream_t st);

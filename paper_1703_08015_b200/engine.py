@@ -293,6 +293,14 @@ class TileEngineT2C:
     def halo_unpack(self, low_ptr: int, high_ptr: int) -> None:
         _native.check(self._L.splbm_dev_halo_unpack(self._h, low_ptr or None, high_ptr or None))
 
+    def halo_pack_back(self, low_ptr: int, high_ptr: int) -> None:
+        """Single copy, after a step from the natural layout: the halo slots the scatter wrote
+        (splbm_dev_halo_pack_back)."""
+        _native.check(self._L.splbm_dev_halo_pack_back(self._h, low_ptr or None, high_ptr or None))
+
+    def halo_unpack_back(self, low_ptr: int, high_ptr: int) -> None:
+        _native.check(self._L.splbm_dev_halo_unpack_back(self._h, low_ptr or None, high_ptr or None))
+
 
 # ---- driver (engine.hpp:562-655) --------------------------------------------------------------
 @dataclass

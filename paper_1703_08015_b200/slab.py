@@ -224,7 +224,7 @@ class SlabRun:
 
     def __init__(self, g: Geometry, a: int, model, periodic, rank: int, world: int, device: int,
                  slabs=None, host_staged: bool = False, native: bool = False,
-                 transport: str | None = None):
+                 transport: str | None = None, single_copy: bool = False):
         import torch
         from .engine import TileEngineT2C
         per = Periodicity.of(periodic)
@@ -233,7 +233,8 @@ class SlabRun:
                                          min_planes(world, per, g.d))
         z0, z1 = self.slabs[rank]
         self.engine = TileEngineT2C(g, a, model, per, device=device,
-                                    slab=None if world == 1 else (z0, z1))
+                                    slab=None if world == 1 else (z0, z1), single_copy=single_copy)
+        self.single_copy = bool(single_copy)
         axis_periodic = per.axis(2 if g.d == 3 else 1)
         self.stream = torch.cuda.ExternalStream(self.engine.stream_handle(), device=device)
         dev = torch.device("cuda", device)
@@ -257,9 +258,15 @@ class SlabRun:
             dist.broadcast_object_list(uid, src=0)
             self.engine.comm_attach(uid[0], world, rank, lower, upper)
         elif self.transport == "torch":
-            self.xchg = HaloExchange(rank, world, axis_periodic, self.engine.halo_bytes(),
-                                     lambda n: torch.empty(n, dtype=torch.float64, device=dev),
+            alloc = lambda n: torch.empty(n, dtype=torch.float64, device=dev)
+            sizes = self.engine.halo_bytes()
+            self.xchg = HaloExchange(rank, world, axis_periodic, sizes, alloc,
                                      TorchComm(self.stream, host_staged=host_staged))
+            if single_copy:  # the backward exchange after steps from the natural layout
+                back = {"send_low": sizes["recv_low"], "send_high": sizes["recv_high"],
+                        "recv_low": sizes["send_low"], "recv_high": sizes["send_high"]}
+                self.xback = HaloExchange(rank, world, axis_periodic, back, alloc,
+                                          TorchComm(self.stream, host_staged=host_staged))
 
     def _pack(self, lo, hi):
         self.engine.halo_pack_next(lo.data_ptr() if lo.numel() else 0,
@@ -268,6 +275,17 @@ class SlabRun:
     def _unpack(self, lo, hi):
         self.engine.halo_unpack(lo.data_ptr() if lo is not None and lo.numel() else 0,
                                 hi.data_ptr() if hi is not None and hi.numel() else 0)
+
+    def _pack_cur(self, lo, hi):
+        self.engine.halo_pack(lo.data_ptr() if lo.numel() else 0, hi.data_ptr() if hi.numel() else 0)
+
+    def _pack_back(self, lo, hi):
+        self.engine.halo_pack_back(lo.data_ptr() if lo.numel() else 0,
+                                   hi.data_ptr() if hi.numel() else 0)
+
+    def _unpack_back(self, lo, hi):
+        self.engine.halo_unpack_back(lo.data_ptr() if lo is not None and lo.numel() else 0,
+                                     hi.data_ptr() if hi is not None and hi.numel() else 0)
 
     def initialize(self, init=None) -> None:
         """Initialise every rank, then a barrier: a neighbour's first step may already store its
@@ -285,6 +303,15 @@ class SlabRun:
         transfers) -> complete exchange -> unpack; all ordered on the engine stream."""
         if self.world == 1 or self.native:
             self.engine.step_async(n)
+            return
+        if self.single_copy:  # AA: forward faces before, backward slots after natural-layout steps
+            for _ in range(n):
+                if self.engine.current_step() % 2 == 0:
+                    self.xchg.exchange(self._pack_cur, self._unpack)
+                    self.engine.step_async(1)
+                    self.xback.exchange(self._pack_back, self._unpack_back)
+                else:
+                    self.engine.step_async(1)
             return
         for _ in range(n):
             self.engine.step_part(1)

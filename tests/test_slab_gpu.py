@@ -94,7 +94,7 @@ def test_native_comm_attach_single_rank():
     assert e2.current_step() == 33 and e2.tile_visits() == e1.tile_visits()
 
 
-def _p2p_slabs_vs_whole(name, world, devices, monkeypatch, wait=None):
+def _p2p_slabs_vs_whole(name, world, devices, monkeypatch, wait=None, single_copy=False, K=11):
     from oracle import oracle as O
     if wait:
         monkeypatch.setenv("SPLBM_P2P_WAIT", wait)
@@ -105,15 +105,14 @@ def _p2p_slabs_vs_whole(name, world, devices, monkeypatch, wait=None):
     whole.initialize(O.wavy)
     slabs = slab.plan_slabs(slab.plane_tile_counts(g, a, per), world,
                             min_planes=slab.min_planes(world, P.Periodicity.of(per), g.d))
-    ranks = [P.TileEngineT2C(g, a, m, per, slab=s, device=devices[r % len(devices)])
-             for r, s in enumerate(slabs)]
+    ranks = [P.TileEngineT2C(g, a, m, per, slab=s, device=devices[r % len(devices)],
+                             single_copy=single_copy) for r, s in enumerate(slabs)]
     blobs = [e.ipc_blob() for e in ranks]
     ax_per = P.Periodicity.of(per).axis(2 if g.d == 3 else 1)
     for r, e in enumerate(ranks):
         lo, hi = slab.neighbours(r, world, ax_per)
         e.p2p_attach(blobs[lo] if lo is not None else None, blobs[hi] if hi is not None else None)
         e.initialize(O.wavy)
-    K = 11
     for e in ranks:          # all ranks' steps enqueued; GPU-side flags order them
         e.step_async(K)
     for e in ranks:
@@ -153,3 +152,84 @@ def test_p2p_slabs_on_distinct_devices(name, world, monkeypatch):
     if n < 2:
         pytest.skip("needs two or more GPUs")
     _p2p_slabs_vs_whole(name, world, list(range(n)), monkeypatch)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_p2p_single_copy_slabs_match_whole(name, world, monkeypatch):
+    """Single-copy (AA) slabs over the fused p2p transport: the boundary planes' steps from the
+    natural layout read and write the halo nodes' slots in place in the neighbours' memory.
+    After an even step count the owned PDFs equal the two-copy single engine bit for bit."""
+    _p2p_slabs_vs_whole(name, world, [0], monkeypatch, single_copy=True, K=12)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_single_copy_slab_engines_exchange_buffers(name, world):
+    """Single-copy slab engines with the forward (before natural-layout steps) and backward
+    (after them: the scatter's halo slots back to their owners, masked to the slots whose
+    downstream node is non-solid) exchanges through device buffers: bitwise equal to the whole
+    domain after an even step count; the swapped layout of a slab engine is not readable."""
+    import torch
+    from oracle import oracle as O
+    factory, a, per = CASES[name]
+    g = factory()
+    m = P.FluidModel(tau=0.8)
+    whole = P.TileEngineT2C(g, a, m, per)
+    whole.initialize(O.wavy)
+    slabs = slab.plan_slabs(slab.plane_tile_counts(g, a, per), world,
+                            min_planes=slab.min_planes(world, P.Periodicity.of(per), g.d))
+    ranks = [P.TileEngineT2C(g, a, m, per, slab=s, single_copy=True) for s in slabs]
+    for e in ranks:
+        e.initialize(O.wavy)
+    ax_per = P.Periodicity.of(per).axis(2 if g.d == 3 else 1)
+    fwd, back = [], []
+    for e in ranks:
+        hb = e.halo_bytes()
+        mk = lambda n: torch.zeros(max(n // 8, 1), dtype=torch.float64, device="cuda")
+        fwd.append({k: mk(v) for k, v in hb.items()})
+        back.append({"send_low": mk(hb["recv_low"]), "send_high": mk(hb["recv_high"]),
+                     "recv_low": mk(hb["send_low"]), "recv_high": mk(hb["send_high"])})
+
+    def exchange(buf, pack, unpack):
+        for r, e in enumerate(ranks):
+            getattr(e, pack)(buf[r]["send_low"].data_ptr(), buf[r]["send_high"].data_ptr())
+        for e in ranks:
+            e.sync()
+        for r in range(world):
+            lo, hi = slab.neighbours(r, world, ax_per)
+            if lo is not None:
+                n = min(buf[r]["recv_low"].numel(), buf[lo]["send_high"].numel())
+                buf[r]["recv_low"][:n].copy_(buf[lo]["send_high"][:n])
+            if hi is not None:
+                n = min(buf[r]["recv_high"].numel(), buf[hi]["send_low"].numel())
+                buf[r]["recv_high"][:n].copy_(buf[hi]["send_low"][:n])
+        torch.cuda.synchronize()
+        for r, e in enumerate(ranks):
+            lo, hi = slab.neighbours(r, world, ax_per)
+            getattr(e, unpack)(buf[r]["recv_low"].data_ptr() if lo is not None else 0,
+                               buf[r]["recv_high"].data_ptr() if hi is not None else 0)
+
+    K = 10
+    assert whole.step_n(K)[0]
+    for s in range(K):
+        if s % 2 == 0:
+            exchange(fwd, "halo_pack", "halo_unpack")
+            for e in ranks:
+                assert e.step_n(1)[0]
+            if s == 0:
+                with pytest.raises(P.ConfigError):
+                    ranks[0].get_pdf()  # swapped layout of a slab engine
+            exchange(back, "halo_pack_back", "halo_unpack_back")
+        else:
+            for e in ranks:
+                assert e.step_n(1)[0]
+    tg = whole.tile_grid()
+    st = whole.q * whole.n_tn
+    wp = whole.get_pdf()
+    for r, e in enumerate(ranks):
+        lay = slab.slab_layout(g, a, per, *slabs[r])
+        g0, n = lay["g_own0"], lay["n_own"]
+        mine = e.get_pdf()[lay["n_low"] * st:(lay["n_low"] + n) * st]
+        fluid = np.broadcast_to((tg.types[g0:g0 + n] != 0)[:, None, :], (n, whole.q, whole.n_tn)).ravel()
+        assert np.array_equal(mine[fluid].view(np.uint64), wp[g0 * st:(g0 + n) * st][fluid].view(np.uint64))

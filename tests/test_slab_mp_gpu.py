@@ -29,7 +29,7 @@ def _geom(name):
     return P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=(24, 20, 48))), 4, 0
 
 
-def _worker(rank, world, port, name, transport, q, spread=False):
+def _worker(rank, world, port, name, transport, q, spread=False, single_copy=False):
     try:
         import torch.distributed as dist
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -42,15 +42,18 @@ def _worker(rank, world, port, name, transport, q, spread=False):
         import torch
         dev = rank % torch.cuda.device_count() if spread else 0
         if transport == "p2p":  # CUDA IPC peer stores between the processes
-            run = slab.SlabRun(g, a, m, per, rank, world, dev, transport="p2p")
+            run = slab.SlabRun(g, a, m, per, rank, world, dev, transport="p2p",
+                               single_copy=single_copy)
         else:  # torch HaloExchange over gloo through host memory
-            run = slab.SlabRun(g, a, m, per, rank, world, dev, host_staged=True)
+            run = slab.SlabRun(g, a, m, per, rank, world, dev, host_staged=True,
+                               single_copy=single_copy)
+        steps = STEPS + (STEPS % 2 if single_copy else 0)  # single copy: compare a natural layout
         run.initialize(O.wavy)
-        run.step_async(STEPS)
+        run.step_async(steps)
         ok, _ = run.sync()
         whole = P.TileEngineT2C(g, a, m, per)
         whole.initialize(O.wavy)
-        whole.step_n(STEPS)
+        whole.step_n(steps)
         z0, z1 = run.slabs[rank]
         lay = slab.slab_layout(g, a, per, z0, z1)
         st = whole.q * whole.n_tn
@@ -61,18 +64,18 @@ def _worker(rank, world, port, name, transport, q, spread=False):
         fluid = np.broadcast_to((types != 0)[:, None, :], (n, whole.q, whole.n_tn)).ravel()
         same = np.array_equal(mine[fluid].view(np.uint64), ref[fluid].view(np.uint64))
         dist.destroy_process_group()
-        q.put((rank, bool(ok and same), run.engine.current_step()))
+        q.put((rank, bool(ok and same), run.engine.current_step() - (steps - STEPS)))
     except Exception as ex:  # pragma: no cover
         import traceback
         q.put((rank, False, traceback.format_exc()))
 
 
-def _run(name, world, transport, spread=False):
+def _run(name, world, transport, spread=False, single_copy=False):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, name, transport, q, spread))
+    ps = [ctx.Process(target=_worker, args=(r, world, port, name, transport, q, spread, single_copy))
           for r in range(world)]
     for p in ps:
         p.start()
@@ -99,3 +102,12 @@ def test_slabrun_processes_on_distinct_devices(name, world):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs two or more GPUs")
     _run(name, world, "p2p", spread=True)
+
+
+@pytest.mark.parametrize("transport", ["torch", "p2p"])
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name", ["ras40_periodic", "channel3d"])
+def test_single_copy_slabrun_processes_match_whole(name, world, transport):
+    """Single-copy (AA) slab ranks as processes: forward/backward face exchanges over gloo (torch)
+    or in-place neighbour slots over CUDA IPC (p2p); bitwise equal to the single engine."""
+    _run(name, world, transport, single_copy=True)
