@@ -14,6 +14,9 @@ from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SPLBM_LIB") or os.path.join(_HERE, "libsplbm_b200.so")
+# The tolerance-mode build (same sources, SPLBM_FMA=1: contracted multiply-adds and a reciprocal
+# velocity division, ~1e-15 per step instead of the bit-exact default; `arithmetic="fma"`).
+FMA_LIB_PATH = os.environ.get("SPLBM_FMA_LIB") or os.path.join(_HERE, "libsplbm_b200_fma.so")
 
 _dp = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
 _u8 = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
@@ -115,9 +118,19 @@ SIGNATURES = {
 }
 
 
-def lib():
-    """The loaded native library; raises if it was not built (no fallback path exists)."""
-    global _lib
+_fma_lib = None
+
+
+def lib(arithmetic: str = "exact"):
+    """The loaded native library; raises if it was not built (no fallback path exists).
+    arithmetic="fma" selects the tolerance-mode build."""
+    global _lib, _fma_lib
+    if arithmetic == "fma":
+        if _fma_lib is None:
+            _fma_lib = load(FMA_LIB_PATH)
+        return _fma_lib
+    if arithmetic != "exact":
+        raise errors.ConfigError("arithmetic must be exact or fma")
     if _lib is None:
         _lib = load(LIB_PATH)
     return _lib
@@ -143,10 +156,12 @@ def load(path: str):
     return L
 
 
-def check(rc: int, step: int | None = None) -> None:
+def check(rc: int, step: int | None = None, lib_=None) -> None:
+    """Raises the errors.hpp exception for a non-zero status; the message is the thread's last
+    error of the library that returned it (`lib_`, default the bit-exact build)."""
     if rc == 0:
         return
-    msg = lib().splbm_last_error().decode(errors="replace")
+    msg = (lib_ or lib()).splbm_last_error().decode(errors="replace")
     raise errors.from_status(rc, msg, step)
 
 

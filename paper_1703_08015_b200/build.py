@@ -15,6 +15,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsplbm_b200.so")
 BUILD = os.path.join(ROOT, "build", "native")
+# the tolerance-mode build: same sources with SPLBM_FMA=1 (contracted multiply-adds)
+FMA_LIB = os.path.join(PKG, "libsplbm_b200_fma.so")
+FMA_BUILD = os.path.join(ROOT, "build", "native_fma")
 SOURCES = ["kernels.cu", "engine.cpp", "tiling.cpp", "tiling_gpu.cu", "geometry.cpp", "geometry_gpu.cu", "nccl_api.cpp",
            "mrt.cpp"]
 HEADERS = ["kernels.h", "lattice.cuh", "common.h", "tiling.h", "tiling_gpu.h", "nccl_api.h", "mrt.h"]
@@ -66,5 +69,11 @@ def build(force: bool = False, verbose: bool = False, defines: list[str] | None 
     return out_lib
 
 
+def build_all(force: bool = False, verbose: bool = False) -> list[str]:
+    """The bit-exact library and the tolerance-mode (SPLBM_FMA=1) library."""
+    return [build(force, verbose),
+            build(force, verbose, defines=["SPLBM_FMA=1"], lib=FMA_LIB, build_dir=FMA_BUILD)]
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build_all(force="--force" in sys.argv, verbose=True))

@@ -135,6 +135,9 @@ def build_sim(cfg: Config) -> E.SimConfig:  # splbm.cpp:136-150
                       single_copy=cfg.get("sim.storage", "two-copy") == "single-copy")
     if cfg.get("sim.storage", "two-copy") not in ("two-copy", "single-copy"):
         raise ConfigError("sim.storage must be two-copy or single-copy")
+    sim.arithmetic = cfg.get("sim.arithmetic", "exact")
+    if sim.arithmetic not in ("exact", "fma"):
+        raise ConfigError("sim.arithmetic must be exact or fma")
     sim.initial_density = cfg.get_float("sim.initial_density", 1.0)
     if "sim.initial_velocity" in cfg:
         v = [float(x) for x in cfg["sim.initial_velocity"].replace(",", " ").split()]

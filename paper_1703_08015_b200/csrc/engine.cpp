@@ -96,6 +96,8 @@ struct splbm_dev_engine {
   void* pdf[2] = {nullptr, nullptr};  // PDF copies in the engine's real type (double / float)
   uint32_t* info = nullptr;
   uint32_t* nb = nullptr;
+  uint32_t* order = nullptr;  // column traversal order of large whole-domain engines (StepArgs::order)
+  int order_block = 0;        // its column edge B in cells (0 = compact order)
   unsigned long long* failed = nullptr;
   long long* step_base = nullptr;
   int* domain_err = nullptr;
@@ -182,7 +184,7 @@ struct splbm_dev_engine {
                     static_cast<void*>(step_base), static_cast<void*>(domain_err),
                     static_cast<void*>(zero_base),
                     static_cast<void*>(halo_dirs), static_cast<void*>(scratch),
-                    static_cast<void*>(reduce_buf),
+                    static_cast<void*>(reduce_buf), static_cast<void*>(order),
                     static_cast<void*>(cells), static_cast<void*>(frame)})
       if (p) cudaFree(p);
     if (ev0) cudaEventDestroy(ev0);
@@ -232,6 +234,7 @@ struct splbm_dev_engine {
     s.pdl_min_threads = pdl_min_threads;
     s.x2 = x2;
     s.off32 = off32 && n_stored * tile_stride() < (1ull << 32);
+    s.order = order;
     if (peer_part1 && aa) {  // single copy: phase 1 reads/writes the halo nodes' slots in place
       if (rd == 0) {
         s.peer_down = peer_pdf_down[0] ? peer_pdf_down[0] + peer_down_own0 * tile_stride() : nullptr;
@@ -253,6 +256,7 @@ struct splbm_dev_engine {
   void launch_range(int rd, uint64_t t_begin, uint64_t t_end) {
     if (t_end <= t_begin) return;
     splbm_dev::StepArgs s = step_args(rd, 0);
+    s.order = nullptr;  // (slab parts: compact ranges)
     s.t0 = t_begin;
     s.n_nodes = (t_end - t_begin) * n_tn;
     CK(splbm_dev::launch_step(d, incompressible != 0, f32, s, stream));
@@ -270,6 +274,7 @@ struct splbm_dev_engine {
         launch_range(read, b0, t1);
       } else if (b1 > b0 && t1 > t0) {  // both planes in one launch, jumping the interior
         splbm_dev::StepArgs s = step_args(read, 0);
+        s.order = nullptr;
         s.t0 = b0;
         s.n_nodes = (send_low_tiles + send_high_tiles) * n_tn;
         s.skip_at = send_low_tiles;
@@ -567,6 +572,24 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
     e->fluid_nodes = e->tb.fluid_nodes;
     e->n_tn = tm.n_tn;
     phase("gpu_tiles");
+    // Column traversal (tiling_gpu.h) when one tile plane of PDFs outgrows a quarter of L2: in the
+    // compact (plane-major) order a tile's -z neighbour was stepped a whole plane earlier and its
+    // face lines have left L2 (1024^3: ~200 MB per plane). SPLBM_ORDER=0 keeps the compact order,
+    // SPLBM_ORDER=B forces columns of B x B cells.
+    if (d == 3 && !e->f32 && (e->a == 2 || e->a == 4) && tm.n_tiles) {
+      int l2 = 0;
+      CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, e->device));
+      const uint64_t plane_bytes = tm.n_tiles / std::max(1, tm.grid_dims[2]) *
+                                   static_cast<uint64_t>(e->q) * tm.n_tn * e->es;
+      int B = plane_bytes * 4 > static_cast<uint64_t>(l2) ? 32 : 0;
+      if (const char* v = std::getenv("SPLBM_ORDER")) B = std::atoi(v);
+      if (B > 0 && (B < tm.grid_dims[0] || B < tm.grid_dims[1])) {
+        e->order = e->alloc<uint32_t>(tm.n_tiles);
+        CK(splbm_dev::build_column_order(e->tb.tile_map, tm.grid_dims, B, tm.n_tiles, e->order, e->stream));
+        e->order_block = B;
+      }
+      phase("column_order");
+    }
   } else {
     tm = build_tile_map(desc->types, d, dims, e->a, e->periodic);
     phase("tile_map");

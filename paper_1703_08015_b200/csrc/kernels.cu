@@ -135,6 +135,13 @@ __device__ __forceinline__ float ld_pdf_rw(const float* p) {
   return v;
 }
 
+// Stored tile of the k-th stepped tile of a launch: the column traversal order when set (large
+// whole-domain engines, StepArgs::order), else the range [t0, ...) with the optional skip.
+__device__ __forceinline__ uint64_t tile_of(const StepArgs& a, uint64_t k) {
+  if (a.order) return __ldg(a.order + k);
+  return a.t0 + k + (k >= a.skip_at ? a.skip_by : 0);
+}
+
 // L2 prefetch of a future CTA's read blocks (the CTA StepArgs::l2pf CTAs ahead, about half a
 // wave): one bulk request per tile block (Q*NTN doubles, contiguous) holds no registers, so more
 // DRAM reads are in flight than the gather alone keeps. Whole blocks measured faster than
@@ -281,7 +288,7 @@ __global__ void __launch_bounds__((step_threads<D, (D == 3 ? (1 << (3 * LOGA)) :
     const uint64_t tt = tile_blk + tl;
     const R* b = nullptr;
     if (tt < n_tiles) {
-      const uint32_t s = __ldg(args.nb + (args.t0 + tt + (tt >= args.skip_at ? args.skip_by : 0)) * NBS + dd);
+      const uint32_t s = __ldg(args.nb + tile_of(args, tt) * NBS + dd);
       b = s == kEmpty ? nullptr : rd + static_cast<uint64_t>(s) * STRIDE;
     }
     s_base[tl][dd] = b;
@@ -290,7 +297,7 @@ __global__ void __launch_bounds__((step_threads<D, (D == 3 ? (1 << (3 * LOGA)) :
   const int p = threadIdx.x % NTN;
   const uint64_t tloc = tile_blk + tl;
   const bool live = tloc < n_tiles;
-  const uint64_t t = args.t0 + tloc + (tloc >= args.skip_at ? args.skip_by : 0);
+  const uint64_t t = live ? tile_of(args, tloc) : 0;
   const uint32_t info = live ? __ldg(args.info + t * NTN + p) : 0u;
   const uint64_t pf = tile_blk + static_cast<uint64_t>(args.l2pf) * TILES + threadIdx.x;
   __syncthreads();
@@ -300,7 +307,7 @@ __global__ void __launch_bounds__((step_threads<D, (D == 3 ? (1 << (3 * LOGA)) :
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
-  l2_prefetch_blocks<Q, NTN, TILES>(rd, args.t0 + pf + (pf >= args.skip_at ? args.skip_by : 0),
+  l2_prefetch_blocks<Q, NTN, TILES>(rd, (args.l2pf && pf < n_tiles && threadIdx.x < TILES) ? tile_of(args, pf) : 0,
                                     args.l2pf && pf < n_tiles);
   const int type = (info >> 24) & 3;
   R* wr = static_cast<R*>(args.write) + t * STRIDE + p;
@@ -500,7 +507,7 @@ __global__ void __launch_bounds__(aa_threads<D, LOGA>(),
       const uint64_t tt = tile_blk + tl;
       R* b = nullptr;
       if (tt < n_tiles) {
-        const uint32_t s = __ldg(args.nb + (args.t0 + tt + (tt >= args.skip_at ? args.skip_by : 0)) * NBS + dd);
+        const uint32_t s = __ldg(args.nb + tile_of(args, tt) * NBS + dd);
         if (s == kEmpty) b = nullptr;
         // slab p2p, phase 1: the slots of halo nodes are read and written in place in the
         // neighbour's owned tiles over NVLink (each slot is touched by exactly one node, this one)
@@ -514,7 +521,7 @@ __global__ void __launch_bounds__(aa_threads<D, LOGA>(),
   const int tl = threadIdx.x / NTN;
   const int p = threadIdx.x % NTN;
   const uint64_t tloc = tile_blk + tl;
-  const uint64_t t = args.t0 + tloc + (tloc >= args.skip_at ? args.skip_by : 0);
+  const uint64_t t = tloc < n_tiles ? tile_of(args, tloc) : 0;
   const uint32_t info = tloc < n_tiles ? __ldg(args.info + t * NTN + p) : 0u;
   if constexpr (PHASE == 1) __syncthreads();
 #if SPLBM_PDL
@@ -523,7 +530,7 @@ __global__ void __launch_bounds__(aa_threads<D, LOGA>(),
 #endif
   {
     const uint64_t pf = tile_blk + static_cast<uint64_t>(args.l2pf) * TILES + threadIdx.x;
-    l2_prefetch_blocks<Q, NTN, TILES>(pdf, args.t0 + pf + (pf >= args.skip_at ? args.skip_by : 0),
+    l2_prefetch_blocks<Q, NTN, TILES>(pdf, (args.l2pf && pf < n_tiles && threadIdx.x < TILES) ? tile_of(args, pf) : 0,
                                       args.l2pf && pf < n_tiles);
   }
   const int type = (info >> 24) & 3;

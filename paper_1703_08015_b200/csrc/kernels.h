@@ -47,6 +47,9 @@ struct StepArgs {
   double* peer_down;
   uint64_t top_begin, bot_begin, bot_end;
   uint64_t halo_lo_end, halo_hi_begin;
+  // Traversal order (power-of-two 3D kernels, whole-domain engines): the k-th stepped tile is
+  // order[k] (tiling_gpu.h build_column_order); nullptr = the compact order t0 + k.
+  const uint32_t* order;
 };
 
 // The MRT operator as a kernel parameter (constant bank): the unrolled K_ij * delta_j products

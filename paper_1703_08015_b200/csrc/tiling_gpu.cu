@@ -147,7 +147,78 @@ __global__ void neighbour_kernel(Grid g, const uint32_t* tile_map, const uint32_
 
 unsigned blocks_for(uint64_t n, unsigned threads) { return static_cast<unsigned>((n + threads - 1) / threads); }
 
+// Cell of position j of the block-column traversal: columns of B x B cells in (x, y) (the last
+// ones ragged), column-major over (by, bx), inside a column z-major, then y, then x.
+__device__ __forceinline__ uint64_t column_cell(uint64_t j, const int* gd, int B) {
+  const uint64_t gx = gd[0], gy = gd[1], gz = gd[2];
+  const uint64_t nbx = (gx + B - 1) / B;
+  const uint64_t full_rows = gy / B;  // column rows of height B (the last one may be shorter)
+  // column row `br` (cells y in [br*B, br*B+h)) holds gx * h * gz cells
+  const uint64_t row_cells = gx * static_cast<uint64_t>(B) * gz;
+  uint64_t br = j / row_cells;
+  if (br > full_rows) br = full_rows;
+  uint64_t r = j - br * row_cells;
+  const uint64_t h = (br < full_rows) ? static_cast<uint64_t>(B) : gy - full_rows * B;
+  // inside a column row: columns bx of width w (last one ragged), each w * h * gz cells
+  const uint64_t col_cells = static_cast<uint64_t>(B) * h * gz;
+  uint64_t bx = r / col_cells;
+  const uint64_t full_cols = gx / B;
+  if (bx > full_cols) bx = full_cols;
+  r -= bx * col_cells;
+  const uint64_t w = (bx < full_cols) ? static_cast<uint64_t>(B) : gx - full_cols * B;
+  (void)nbx;
+  const uint64_t cz = r / (w * h);
+  const uint64_t rr = r % (w * h);
+  const uint64_t cy = br * B + rr / w;
+  const uint64_t cx = bx * B + rr % w;
+  return cx + gx * (cy + gy * cz);
+}
+
+__global__ void column_flags_kernel(uint64_t C, Grid g, int B, const uint32_t* tile_map, uint32_t* flags) {
+  const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= C) return;
+  flags[j] = tile_map[column_cell(j, g.gd, B)] != kEmptyTile;
+}
+
+__global__ void column_order_kernel(uint64_t C, Grid g, int B, const uint32_t* tile_map,
+                                    const uint32_t* pos, uint32_t* order) {
+  const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= C) return;
+  const uint32_t t = tile_map[column_cell(j, g.gd, B)];
+  if (t != kEmptyTile) order[pos[j]] = t;
+}
+
 }  // namespace
+
+cudaError_t build_column_order(const uint32_t* tile_map, const int grid_dims[3], int B,
+                               uint64_t n_tiles, uint32_t* order, cudaStream_t st) {
+  Grid g{};
+  for (int k = 0; k < 3; ++k) g.gd[k] = grid_dims[k];
+  const uint64_t C = static_cast<uint64_t>(g.gd[0]) * g.gd[1] * g.gd[2];
+  if (!C || !n_tiles) return cudaSuccess;
+  uint32_t *flags = nullptr, *pos = nullptr;
+  void* temp = nullptr;
+  size_t temp_bytes = 0;
+  cudaError_t err = cudaSuccess;
+  auto ok = [&](cudaError_t e) {
+    if (err == cudaSuccess) err = e;
+    return err == cudaSuccess;
+  };
+  do {
+    if (!ok(cudaMalloc(&flags, C * 4)) || !ok(cudaMalloc(&pos, C * 4))) break;
+    column_flags_kernel<<<blocks_for(C, 256), 256, 0, st>>>(C, g, B, tile_map, flags);
+    if (!ok(cudaGetLastError())) break;
+    if (!ok(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, flags, pos, static_cast<int>(C), st))) break;
+    if (!ok(cudaMalloc(&temp, temp_bytes))) break;
+    if (!ok(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, flags, pos, static_cast<int>(C), st))) break;
+    column_order_kernel<<<blocks_for(C, 256), 256, 0, st>>>(C, g, B, tile_map, pos, order);
+    if (!ok(cudaGetLastError())) break;
+    ok(cudaStreamSynchronize(st));
+  } while (false);
+  for (void* p : {static_cast<void*>(flags), static_cast<void*>(pos), temp})
+    if (p) cudaFree(p);
+  return err;
+}
 
 void free_tile_build(TileBuildOut* o) {
   for (void* p : {static_cast<void*>(o->tile_map), static_cast<void*>(o->cell_of),

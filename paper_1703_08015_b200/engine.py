@@ -41,13 +41,18 @@ class TileEngineT2C:
     the multi-GPU slab mode, `single_copy=True` the in-place AA propagation (one PDF
     array instead of two, bit-identical results) and `precision="f32"` the
     TileEngineT2C<float> instantiation (the reference CLI's precision=f32, tools/splbm.cpp:278).
+    `arithmetic="fma"` is the opt-in tolerance mode (libsplbm_b200_fma.so: contracted
+    multiply-adds and a reciprocal velocity division, like the reference built with
+    -march=native; within 1e-13 per step and 1e-10 after 1000 steps of the bit-exact default,
+    tests/test_device_fma.py).
     """
 
     def __init__(self, g: Geometry, a: int, model: FluidModel, periodic=None, device: int = 0,
-                 slab: tuple | None = None, single_copy: bool = False, precision: str = "f64"):
+                 slab: tuple | None = None, single_copy: bool = False, precision: str = "f64",
+                 arithmetic: str = "exact"):
         if precision not in ("f64", "f32"):
             raise ConfigError("precision must be f32 or f64")
-        L = _native.lib()
+        L = _native.lib(arithmetic)
         q = 9 if g.d == 2 else 19
         rates = None
         if model.collision == CollisionKind.MRT and model.mrt_rates:
@@ -73,9 +78,10 @@ class TileEngineT2C:
         desc.single_copy = int(bool(single_copy))
         desc.single_precision = int(precision == "f32")
         h = C.c_void_p()
-        _native.check(L.splbm_dev_create(C.byref(desc), C.byref(h)))
+        _native.check(L.splbm_dev_create(C.byref(desc), C.byref(h)), lib_=L)
         self._h = h
         self._L = L
+        self.arithmetic = arithmetic
         self.geometry_dims = tuple(int(v) for v in g.dims)
         self.d = g.d
         self.model = model
@@ -84,12 +90,15 @@ class TileEngineT2C:
         self.precision = precision
         self.dtype = np.float32 if precision == "f32" else np.float64
         info = _native.DevInfo()
-        _native.check(L.splbm_dev_get_info(h, C.byref(info)))
+        _native.check(L.splbm_dev_get_info(h, C.byref(info)), lib_=L)
         self.info = info
         self.a = info.a
         self.q = info.q
         self.n_tn = info.n_tn
         self._grid = None
+
+    def _chk(self, rc: int, step: int | None = None) -> None:
+        _native.check(rc, step, lib_=self._L)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -104,14 +113,14 @@ class TileEngineT2C:
             T = int(np.prod(gd))
             L = self._L
             tile_map = np.empty(T, np.uint32)
-            _native.check(L.splbm_dev_get_tile_grid(self._h, _native.ptr(tile_map), None, None,
+            self._chk(L.splbm_dev_get_tile_grid(self._h, _native.ptr(tile_map), None, None,
                                                     None, None))
             nt = int(self.info.n_tiles_global)
             origins = np.empty(max(nt, 1) * 3, np.int32)
             types = np.empty(max(nt, 1) * self.n_tn, np.uint8)
             fc = np.empty(max(nt, 1), np.uint32)
             nb = np.empty(max(nt, 1) * 27, np.uint32)
-            _native.check(L.splbm_dev_get_tile_grid(self._h, None, _native.ptr(origins),
+            self._chk(L.splbm_dev_get_tile_grid(self._h, None, _native.ptr(origins),
                                                     _native.ptr(types), _native.ptr(fc),
                                                     _native.ptr(nb)))
             self._grid = TileGrid(self.a, self.d, self.n_tn, self.periodic, self.geometry_dims,
@@ -123,7 +132,7 @@ class TileEngineT2C:
 
     def stored_tiles(self) -> np.ndarray:
         out = np.empty(max(int(self.info.n_tiles_stored), 1), np.uint64)
-        _native.check(self._L.splbm_dev_stored_tiles(self._h, out))
+        self._chk(self._L.splbm_dev_stored_tiles(self._h, out))
         return out[: int(self.info.n_tiles_stored)]
 
     def node_coords(self):
@@ -158,10 +167,10 @@ class TileEngineT2C:
         if any(a.size != n for a in arrs):
             raise ConfigError(f"initialize_arrays needs {n} values per moment "
                               f"(got {[a.size for a in arrs]})")
-        _native.check(self._L.splbm_dev_initialize(self._h, *arrs))
+        self._chk(self._L.splbm_dev_initialize(self._h, *arrs))
 
     def initialize_uniform(self, rho0: float = 1.0, u0=(0.0, 0.0, 0.0)) -> None:  # engine.hpp:72-75
-        _native.check(self._L.splbm_dev_initialize_uniform(self._h, float(rho0),
+        self._chk(self._L.splbm_dev_initialize_uniform(self._h, float(rho0),
                                                            np.asarray(u0, np.float64)))
 
     def step(self) -> bool:
@@ -173,21 +182,21 @@ class TileEngineT2C:
         """n steps in one device batch; (ok, first failing step number or 0)."""
         ok = C.c_int()
         fs = C.c_long()
-        _native.check(self._L.splbm_dev_step(self._h, int(n), C.byref(ok), C.byref(fs)))
+        self._chk(self._L.splbm_dev_step(self._h, int(n), C.byref(ok), C.byref(fs)))
         return bool(ok.value), int(fs.value)
 
     def step_async(self, n: int) -> None:
-        _native.check(self._L.splbm_dev_step_async(self._h, int(n)))
+        self._chk(self._L.splbm_dev_step_async(self._h, int(n)))
 
     def sync(self) -> tuple[bool, int]:
         ok = C.c_int()
         fs = C.c_long()
-        _native.check(self._L.splbm_dev_sync(self._h, C.byref(ok), C.byref(fs)))
+        self._chk(self._L.splbm_dev_sync(self._h, C.byref(ok), C.byref(fs)))
         return bool(ok.value), int(fs.value)
 
     def last_batch_ms(self) -> float:
         ms = C.c_float()
-        _native.check(self._L.splbm_dev_last_batch_ms(self._h, C.byref(ms)))
+        self._chk(self._L.splbm_dev_last_batch_ms(self._h, C.byref(ms)))
         return float(ms.value)
 
     def fields(self, with_mass: bool = False, out: FieldData | None = None):
@@ -205,7 +214,7 @@ class TileEngineT2C:
             rho, ux, uy, uz = (np.empty(n) for _ in range(4))
             mask = np.empty(n, np.uint8)
         mass = C.c_double()  # the sequential host mass sum only when asked for
-        _native.check(self._L.splbm_dev_fields(self._h, _native.ptr(rho), _native.ptr(ux),
+        self._chk(self._L.splbm_dev_fields(self._h, _native.ptr(rho), _native.ptr(ux),
                                                _native.ptr(uy), _native.ptr(uz),
                                                _native.ptr(mask), C.byref(mass) if with_mass else None))
         f = FieldData(self.d, self.geometry_dims, mask, rho, ux, uy, uz)
@@ -213,12 +222,12 @@ class TileEngineT2C:
 
     def reduce(self) -> dict:
         out = np.zeros(3)
-        _native.check(self._L.splbm_dev_reduce(self._h, out))
+        self._chk(self._L.splbm_dev_reduce(self._h, out))
         return {"mass": float(out[0]), "max_speed": float(out[1]), "non_finite": int(out[2])}
 
     def padded_dims(self) -> tuple:
         out = np.zeros(3, np.int32)
-        _native.check(self._L.splbm_dev_padded_dims(self._h, out))
+        self._chk(self._L.splbm_dev_padded_dims(self._h, out))
         return tuple(int(v) for v in out)
 
     def tile_visits(self) -> int:
@@ -236,47 +245,47 @@ class TileEngineT2C:
     # ---- parity / plumbing ------------------------------------------------------------------
     def get_pdf(self) -> np.ndarray:
         out = np.empty(int(self.info.n_tiles_stored) * self.q * self.n_tn, self.dtype)
-        _native.check(self._L.splbm_dev_get_pdf(self._h, _native.ptr(out)))
+        self._chk(self._L.splbm_dev_get_pdf(self._h, _native.ptr(out)))
         return out
 
     def set_pdf(self, f: np.ndarray) -> None:
         f = np.ascontiguousarray(f, self.dtype)
         if f.size != int(self.info.n_tiles_stored) * self.q * self.n_tn:
             raise ConfigError("PDF array has the wrong size")
-        _native.check(self._L.splbm_dev_set_pdf(self._h, _native.ptr(f)))
+        self._chk(self._L.splbm_dev_set_pdf(self._h, _native.ptr(f)))
 
     def stream_handle(self) -> int:
         return int(self._L.splbm_dev_stream(self._h) or 0)
 
     def halo_bytes(self) -> dict:
         a, b, c, d = (C.c_uint64() for _ in range(4))
-        _native.check(self._L.splbm_dev_halo_bytes(self._h, C.byref(a), C.byref(b)))
-        _native.check(self._L.splbm_dev_halo_recv_bytes(self._h, C.byref(c), C.byref(d)))
+        self._chk(self._L.splbm_dev_halo_bytes(self._h, C.byref(a), C.byref(b)))
+        self._chk(self._L.splbm_dev_halo_recv_bytes(self._h, C.byref(c), C.byref(d)))
         return {"send_low": a.value, "send_high": b.value, "recv_low": c.value,
                 "recv_high": d.value}
 
     def halo_pack(self, low_ptr: int, high_ptr: int) -> None:
-        _native.check(self._L.splbm_dev_halo_pack(self._h, low_ptr or None, high_ptr or None))
+        self._chk(self._L.splbm_dev_halo_pack(self._h, low_ptr or None, high_ptr or None))
 
     def comm_attach(self, uid: bytes, world: int, rank: int, lower: int | None,
                     upper: int | None) -> None:
         """Native NCCL halo exchange for the slab mode (splbm_dev_comm_attach)."""
         buf = C.create_string_buffer(bytes(uid), 128)
-        _native.check(self._L.splbm_dev_comm_attach(self._h, buf, int(world), int(rank),
+        self._chk(self._L.splbm_dev_comm_attach(self._h, buf, int(world), int(rank),
                                                     -1 if lower is None else int(lower),
                                                     -1 if upper is None else int(upper)))
 
     def ipc_blob(self) -> bytes:
         """What a slab neighbour needs to store faces into this engine (splbm_dev_ipc_blob)."""
         buf = C.create_string_buffer(512)
-        _native.check(self._L.splbm_dev_ipc_blob(self._h, buf))
+        self._chk(self._L.splbm_dev_ipc_blob(self._h, buf))
         return buf.raw
 
     def p2p_attach(self, lower_blob: bytes | None, upper_blob: bytes | None) -> None:
         """Fused NVLink peer-store halo exchange with the slab neighbours (splbm_dev_p2p_attach)."""
         lo = C.create_string_buffer(bytes(lower_blob), 512) if lower_blob else None
         hi = C.create_string_buffer(bytes(upper_blob), 512) if upper_blob else None
-        _native.check(self._L.splbm_dev_p2p_attach(self._h, lo, hi))
+        self._chk(self._L.splbm_dev_p2p_attach(self._h, lo, hi))
 
     @staticmethod
     def comm_unique_id() -> bytes:
@@ -285,21 +294,21 @@ class TileEngineT2C:
         return buf.raw
 
     def step_part(self, part: int) -> None:
-        _native.check(self._L.splbm_dev_step_part(self._h, int(part)))
+        self._chk(self._L.splbm_dev_step_part(self._h, int(part)))
 
     def halo_pack_next(self, low_ptr: int, high_ptr: int) -> None:
-        _native.check(self._L.splbm_dev_halo_pack_next(self._h, low_ptr or None, high_ptr or None))
+        self._chk(self._L.splbm_dev_halo_pack_next(self._h, low_ptr or None, high_ptr or None))
 
     def halo_unpack(self, low_ptr: int, high_ptr: int) -> None:
-        _native.check(self._L.splbm_dev_halo_unpack(self._h, low_ptr or None, high_ptr or None))
+        self._chk(self._L.splbm_dev_halo_unpack(self._h, low_ptr or None, high_ptr or None))
 
     def halo_pack_back(self, low_ptr: int, high_ptr: int) -> None:
         """Single copy, after a step from the natural layout: the halo slots the scatter wrote
         (splbm_dev_halo_pack_back)."""
-        _native.check(self._L.splbm_dev_halo_pack_back(self._h, low_ptr or None, high_ptr or None))
+        self._chk(self._L.splbm_dev_halo_pack_back(self._h, low_ptr or None, high_ptr or None))
 
     def halo_unpack_back(self, low_ptr: int, high_ptr: int) -> None:
-        _native.check(self._L.splbm_dev_halo_unpack_back(self._h, low_ptr or None, high_ptr or None))
+        self._chk(self._L.splbm_dev_halo_unpack_back(self._h, low_ptr or None, high_ptr or None))
 
 
 # ---- driver (engine.hpp:562-655) --------------------------------------------------------------
@@ -318,6 +327,7 @@ class SimConfig:  # engine.hpp:562-576
     snapshot_sink: SnapshotSink | None = None
     device: int = 0
     single_copy: bool = False  # device extension: in-place AA propagation
+    arithmetic: str = "exact"  # device extension: "fma" = the tolerance-mode build
 
     def tile_edge(self, d: int) -> int:
         return self.tile if self.tile > 0 else (16 if d == 2 else 4)
@@ -344,7 +354,8 @@ def make_engine(g: Geometry, cfg: SimConfig, precision: str = "f64") -> TileEngi
     if cfg.method != Method.T2C:
         raise ConfigError("the B200 path implements Method::T2C; Dense/TGB stay on the reference")
     return TileEngineT2C(g, cfg.tile_edge(g.d), cfg.model, cfg.periodic, device=cfg.device,
-                         single_copy=cfg.single_copy, precision=precision)
+                         single_copy=cfg.single_copy, precision=precision,
+                         arithmetic=cfg.arithmetic)
 
 
 def run_simulation(g: Geometry, cfg: SimConfig, precision: str = "f64") -> SimulationResult:

@@ -29,6 +29,18 @@ def test_every_declared_symbol_is_exported_and_bound():
         assert n in _native.SIGNATURES, n
 
 
+def test_tolerance_mode_library_exports_the_same_abi():
+    """libsplbm_b200_fma.so (arithmetic="fma") is the same sources with SPLBM_FMA=1."""
+    L = _native.lib("fma")
+    assert L.missing_symbols == []
+    assert L is not _native.lib()
+    with pytest.raises(P.ConfigError):
+        _native.lib("fast")
+    with pytest.raises(P.ConfigError):
+        P.TileEngineT2C(P.Geometry.filled(2, (16, 16, 1)), 4, P.FluidModel(tau=0.4),
+                        arithmetic="fma")
+
+
 def test_library_is_sm100a():
     data = open(_native.LIB_PATH, "rb").read()
     assert b"sm_100a" in data or b"sm_100" in data
