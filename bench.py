@@ -440,7 +440,7 @@ def run_ours(args):
         line["other_configs"] = other_configs(P, min(K, 64), max(W, 3), peak)
     line["e2e"] = e2e_public_api(P, g, 1000, bench_steps=K)  # configs[1] is a 1000-step run
     if not args.no_configs4:  # the north-star 1024^3 point (BASELINE configs[4], N=1)
-        line["configs4"] = configs4_point(P, args.c4_size, args.c4_phi, K, W, False,
+        line["configs4"] = configs4_point(P, args.c4_size, args.c4_phi, K, W, args.c4_single_copy,
                                           (peak, peak_kind))
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(dims)
@@ -519,6 +519,8 @@ def main():
                     help="skip the BASELINE configs[4] point (N=1) / strong-scaling key (N>1)")
     ap.add_argument("--c4-size", type=int, default=1024, help="configs[4] RAS edge (validation runs)")
     ap.add_argument("--c4-phi", type=float, default=0.2, help="configs[4] porosity target")
+    ap.add_argument("--c4-single-copy", action="store_true",
+                    help="configs[4] key with the single-copy (AA) engines (phi 0.5/0.8 fit)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -324,7 +324,7 @@ class SlabRun:
 
 
 def configs4_strong(P, rank, world, device, size=1024, phi=0.2, steps=20, warmup=5,
-                    transport="p2p", single_copy_ref=False):
+                    transport="p2p", single_copy=False):
     """BASELINE configs[4] strong scaling inside a torchrun job: the RAS size^3 (d 40, seed 7,
     periodic, phi target `phi`) split into z-slabs balanced by non-empty tiles, `steps` timed steps
     (CUDA events on the engine stream, max over ranks), then rank 0 alone steps the whole domain
@@ -346,7 +346,7 @@ def configs4_strong(P, rank, world, device, size=1024, phi=0.2, steps=20, warmup
     slabs = plan_slabs(plane_tile_counts(g, 4, Periodicity.of(per)), world,
                        min_planes(world, per, g.d))
     run = SlabRun(g, 4, P.FluidModel(tau=0.8), per, rank, world, device, slabs=slabs,
-                  transport=transport)
+                  transport=transport, single_copy=single_copy)
     eng = run.engine
     eng.initialize_uniform(1.0, (0.01, 0.005, 0.0))
     dist.barrier()
@@ -377,7 +377,8 @@ def configs4_strong(P, rank, world, device, size=1024, phi=0.2, steps=20, warmup
     dist.barrier()
     out = None
     if rank == 0:
-        whole = P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8), per, device=device)
+        whole = P.TileEngineT2C(g, 4, P.FluidModel(tau=0.8), per, device=device,
+                                single_copy=single_copy)
         whole.initialize_uniform(1.0, (0.01, 0.005, 0.0))
         ok1, _ = whole.step_n(warmup)
         whole.step_async(steps)
@@ -386,7 +387,8 @@ def configs4_strong(P, rank, world, device, size=1024, phi=0.2, steps=20, warmup
         v1 = nf * steps / t1 / 1e6
         vN = nf * steps / t / 1e6
         out = {"workload": f"configs[4] RAS {size}^3 d=40 seed 7 periodic, phi target {phi}, "
-                           f"tiles 4^3, two PDF copies, z-slabs balanced by non-empty tiles",
+                           f"tiles 4^3, {'single-copy (AA)' if single_copy else 'two PDF copies'}, "
+                           f"z-slabs balanced by non-empty tiles",
                "scaling": "strong", "n_gpus": world, "steps": steps, "warmup": warmup,
                "value": round(vN, 1), "unit": "MLUPS", "ms_per_step": round(t / steps * 1e3, 4),
                "n1_value": round(v1, 1), "n1_ms_per_step": round(t1 / steps * 1e3, 4),
@@ -427,6 +429,9 @@ def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured"), ras1024=F
                             **({"device_id": torch.device("cuda", device)}
                                if torch.cuda.device_count() >= world else {}))
     transport = os.environ.get("SPLBM_SLAB_TRANSPORT", "p2p")
+    single_copy = bool(ras1024 and getattr(args, "single_copy", False))
+    if single_copy and transport == "nccl":
+        transport = "p2p"  # the native NCCL schedule is the two-copy one
     if ras1024:
         per = (1, 1, 1)
         g = P.generate(P.GeometryKind.Ras3D, P.GenerateParams(
@@ -434,7 +439,8 @@ def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured"), ras1024=F
         slabs = plan_slabs(plane_tile_counts(g, 4, Periodicity.of(per)), world,
                            min_planes(world, per, g.d))
         workload = (f"configs[4] RAS 1024^3 d=40 seed 7 periodic, phi target {args.phi}, z-slabs "
-                    f"balanced by non-empty tiles")
+                    f"balanced by non-empty tiles"
+                    + (", single-copy (AA) propagation" if single_copy else ""))
     else:
         per = None
         g = P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=(128, 128, 128 * world)))
@@ -443,7 +449,7 @@ def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured"), ras1024=F
         workload = f"D3Q19 BGK fp64 channel 128x128x{128 * world}, z-slab per GPU (128^3 nodes each)"
     try:
         run = SlabRun(g, 4, P.FluidModel(tau=0.8), per, rank, world, device, slabs=slabs,
-                      transport=transport)
+                      transport=transport, single_copy=single_copy)
         ok_setup = 1.0
     except Exception:  # noqa: BLE001 - e.g. no peer access between these GPUs
         ok_setup = 0.0
@@ -453,7 +459,7 @@ def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured"), ras1024=F
     if flag.item() < 1.0:  # every rank falls back together: native NCCL send/recv halos
         transport = "nccl"
         run = SlabRun(g, 4, P.FluidModel(tau=0.8), per, rank, world, device, slabs=slabs,
-                      transport=transport)
+                      transport=transport, single_copy=single_copy)
     dist.barrier()  # transports up before the first step
     eng = run.engine
     if ras1024:
@@ -549,7 +555,8 @@ def bench_main(args, P, clock_sampler=None, peak=(6547.2, "measured"), ras1024=F
         # the north-star curve (BASELINE configs[4]) beside the weak-scaled headline value
         c4 = configs4_strong(P, rank, world, device, size=getattr(args, "c4_size", 1024),
                              phi=getattr(args, "c4_phi", 0.2), steps=args.steps,
-                             warmup=args.warmup, transport=transport)
+                             warmup=args.warmup, transport=transport,
+                             single_copy=getattr(args, "c4_single_copy", False))
         if rank == 0:
             line["configs4_strong"] = c4
     if rank == 0:
