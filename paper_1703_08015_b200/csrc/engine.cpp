@@ -572,21 +572,23 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
     e->fluid_nodes = e->tb.fluid_nodes;
     e->n_tn = tm.n_tn;
     phase("gpu_tiles");
-    // Column traversal (tiling_gpu.h) when one tile plane of PDFs outgrows a quarter of L2: in the
-    // compact (plane-major) order a tile's -z neighbour was stepped a whole plane earlier and its
-    // face lines have left L2 (1024^3: ~200 MB per plane). SPLBM_ORDER=0 keeps the compact order,
-    // SPLBM_ORDER=B forces columns of B x B cells.
+    // Column traversal (tiling_gpu.h), an experiment switch: SPLBM_ORDER=BY[xBX] steps the tiles
+    // in (x, y) columns of BX x BY cells (BX default: whole rows = row bands), each walked
+    // z-major, so a tile's -z neighbour was stepped one column-plane earlier instead of a whole
+    // plane (1024^3: ~200 MB per plane, beyond L2). Measured slower than the compact order on
+    // every workload tried (DESIGN.md kept/dropped table): off by default.
     if (d == 3 && !e->f32 && (e->a == 2 || e->a == 4) && tm.n_tiles) {
-      int l2 = 0;
-      CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, e->device));
-      const uint64_t plane_bytes = tm.n_tiles / std::max(1, tm.grid_dims[2]) *
-                                   static_cast<uint64_t>(e->q) * tm.n_tn * e->es;
-      int B = plane_bytes * 4 > static_cast<uint64_t>(l2) ? 32 : 0;
-      if (const char* v = std::getenv("SPLBM_ORDER")) B = std::atoi(v);
-      if (B > 0 && (B < tm.grid_dims[0] || B < tm.grid_dims[1])) {
+      int BY = 0, BX = 0;
+      if (const char* v = std::getenv("SPLBM_ORDER")) {
+        BY = std::atoi(v);
+        if (const char* x = std::strchr(v, 'x')) BX = std::atoi(x + 1);
+      }
+      if (BX <= 0) BX = tm.grid_dims[0];
+      if (BY > 0 && (BX < tm.grid_dims[0] || BY < tm.grid_dims[1])) {
         e->order = e->alloc<uint32_t>(tm.n_tiles);
-        CK(splbm_dev::build_column_order(e->tb.tile_map, tm.grid_dims, B, tm.n_tiles, e->order, e->stream));
-        e->order_block = B;
+        CK(splbm_dev::build_column_order(e->tb.tile_map, tm.grid_dims, BX, BY, tm.n_tiles, e->order,
+                                         e->stream));
+        e->order_block = BY;
       }
       phase("column_order");
     }

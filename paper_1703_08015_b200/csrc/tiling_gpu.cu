@@ -147,50 +147,48 @@ __global__ void neighbour_kernel(Grid g, const uint32_t* tile_map, const uint32_
 
 unsigned blocks_for(uint64_t n, unsigned threads) { return static_cast<unsigned>((n + threads - 1) / threads); }
 
-// Cell of position j of the block-column traversal: columns of B x B cells in (x, y) (the last
-// ones ragged), column-major over (by, bx), inside a column z-major, then y, then x.
-__device__ __forceinline__ uint64_t column_cell(uint64_t j, const int* gd, int B) {
+// Cell of position j of the block-column traversal: columns of BX x BY cells in (x, y) (the last
+// ones ragged), column-major over (by, bx), inside a column z-major, then y, then x. BX = gx gives
+// row bands (each (band, plane) piece is one contiguous run of the compact order).
+__device__ __forceinline__ uint64_t column_cell(uint64_t j, const int* gd, int BX, int BY) {
   const uint64_t gx = gd[0], gy = gd[1], gz = gd[2];
-  const uint64_t nbx = (gx + B - 1) / B;
-  const uint64_t full_rows = gy / B;  // column rows of height B (the last one may be shorter)
-  // column row `br` (cells y in [br*B, br*B+h)) holds gx * h * gz cells
-  const uint64_t row_cells = gx * static_cast<uint64_t>(B) * gz;
+  const uint64_t full_rows = gy / BY;  // column rows of height BY (the last one may be shorter)
+  const uint64_t row_cells = gx * static_cast<uint64_t>(BY) * gz;
   uint64_t br = j / row_cells;
   if (br > full_rows) br = full_rows;
   uint64_t r = j - br * row_cells;
-  const uint64_t h = (br < full_rows) ? static_cast<uint64_t>(B) : gy - full_rows * B;
-  // inside a column row: columns bx of width w (last one ragged), each w * h * gz cells
-  const uint64_t col_cells = static_cast<uint64_t>(B) * h * gz;
+  const uint64_t h = (br < full_rows) ? static_cast<uint64_t>(BY) : gy - full_rows * BY;
+  // inside a column row: columns bx of width BX (the last one ragged), each BX * h * gz cells
+  const uint64_t col_cells = static_cast<uint64_t>(BX) * h * gz;
   uint64_t bx = r / col_cells;
-  const uint64_t full_cols = gx / B;
+  const uint64_t full_cols = gx / BX;
   if (bx > full_cols) bx = full_cols;
   r -= bx * col_cells;
-  const uint64_t w = (bx < full_cols) ? static_cast<uint64_t>(B) : gx - full_cols * B;
-  (void)nbx;
+  const uint64_t w = (bx < full_cols) ? static_cast<uint64_t>(BX) : gx - full_cols * BX;
   const uint64_t cz = r / (w * h);
   const uint64_t rr = r % (w * h);
-  const uint64_t cy = br * B + rr / w;
-  const uint64_t cx = bx * B + rr % w;
+  const uint64_t cy = br * BY + rr / w;
+  const uint64_t cx = bx * BX + rr % w;
   return cx + gx * (cy + gy * cz);
 }
 
-__global__ void column_flags_kernel(uint64_t C, Grid g, int B, const uint32_t* tile_map, uint32_t* flags) {
+__global__ void column_flags_kernel(uint64_t C, Grid g, int BX, int BY, const uint32_t* tile_map, uint32_t* flags) {
   const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= C) return;
-  flags[j] = tile_map[column_cell(j, g.gd, B)] != kEmptyTile;
+  flags[j] = tile_map[column_cell(j, g.gd, BX, BY)] != kEmptyTile;
 }
 
-__global__ void column_order_kernel(uint64_t C, Grid g, int B, const uint32_t* tile_map,
+__global__ void column_order_kernel(uint64_t C, Grid g, int BX, int BY, const uint32_t* tile_map,
                                     const uint32_t* pos, uint32_t* order) {
   const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= C) return;
-  const uint32_t t = tile_map[column_cell(j, g.gd, B)];
+  const uint32_t t = tile_map[column_cell(j, g.gd, BX, BY)];
   if (t != kEmptyTile) order[pos[j]] = t;
 }
 
 }  // namespace
 
-cudaError_t build_column_order(const uint32_t* tile_map, const int grid_dims[3], int B,
+cudaError_t build_column_order(const uint32_t* tile_map, const int grid_dims[3], int BX, int BY,
                                uint64_t n_tiles, uint32_t* order, cudaStream_t st) {
   Grid g{};
   for (int k = 0; k < 3; ++k) g.gd[k] = grid_dims[k];
@@ -206,12 +204,12 @@ cudaError_t build_column_order(const uint32_t* tile_map, const int grid_dims[3],
   };
   do {
     if (!ok(cudaMalloc(&flags, C * 4)) || !ok(cudaMalloc(&pos, C * 4))) break;
-    column_flags_kernel<<<blocks_for(C, 256), 256, 0, st>>>(C, g, B, tile_map, flags);
+    column_flags_kernel<<<blocks_for(C, 256), 256, 0, st>>>(C, g, BX, BY, tile_map, flags);
     if (!ok(cudaGetLastError())) break;
     if (!ok(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, flags, pos, static_cast<int>(C), st))) break;
     if (!ok(cudaMalloc(&temp, temp_bytes))) break;
     if (!ok(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, flags, pos, static_cast<int>(C), st))) break;
-    column_order_kernel<<<blocks_for(C, 256), 256, 0, st>>>(C, g, B, tile_map, pos, order);
+    column_order_kernel<<<blocks_for(C, 256), 256, 0, st>>>(C, g, BX, BY, tile_map, pos, order);
     if (!ok(cudaGetLastError())) break;
     ok(cudaStreamSynchronize(st));
   } while (false);

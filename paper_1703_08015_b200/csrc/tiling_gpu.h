@@ -22,10 +22,10 @@ cudaError_t build_tiles_device(const uint8_t* types, int d, const int dims[3], i
 void free_tile_build(TileBuildOut* o);
 
 // Step traversal order for domains whose tile planes outgrow L2: the non-empty tiles listed column
-// by column — (x, y) columns of B x B cells, each walked z-major (then y, then x) — so a tile's
-// +-z neighbours are stepped one column-plane (B^2 cells) apart instead of one full plane. The PDF
-// layout keeps the reference's compact order; only the CTA -> tile mapping changes.
-cudaError_t build_column_order(const uint32_t* tile_map, const int grid_dims[3], int B,
+// by column — (x, y) columns of BX x BY cells, each walked z-major (then y, then x) — so a tile's
+// +-z neighbours are stepped one column-plane (BX*BY cells) apart instead of one full plane. The
+// PDF layout keeps the reference's compact order; only the CTA -> tile mapping changes.
+cudaError_t build_column_order(const uint32_t* tile_map, const int grid_dims[3], int BX, int BY,
                                uint64_t n_tiles, uint32_t* order, cudaStream_t st);
 
 }  // namespace splbm_dev

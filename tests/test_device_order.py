@@ -17,7 +17,7 @@ def _engine(monkeypatch, B, g, per, **kw):
     return e
 
 
-@pytest.mark.parametrize("B", [1, 3, 5, 16])
+@pytest.mark.parametrize("B", ["1", "3", "5", "16", "2x3", "3x1"])
 @pytest.mark.parametrize("flavour", ["two_copy", "single_copy", "mrt", "incompressible"])
 def test_column_order_bitwise(monkeypatch, B, flavour):
     from oracle import oracle as O
