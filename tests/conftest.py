@@ -9,6 +9,9 @@ for p in (ROOT, TESTS):
     if p not in sys.path:
         sys.path.insert(0, p)
 os.environ["PYTHONPATH"] = os.pathsep.join([ROOT, TESTS, os.environ.get("PYTHONPATH", "")])
+# Slab tests run several engines (and their side streams) on one GPU: more hardware work queues
+# make false serialisation between unrelated streams rarer (read at CUDA context creation).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 
 def pytest_configure(config):

@@ -113,8 +113,13 @@ def _p2p_slabs_vs_whole(name, world, devices, monkeypatch, wait=None, single_cop
         lo, hi = slab.neighbours(r, world, ax_per)
         e.p2p_attach(blobs[lo] if lo is not None else None, blobs[hi] if hi is not None else None)
         e.initialize(O.wavy)
-    for e in ranks:          # all ranks' steps enqueued; GPU-side flags order them
-        e.step_async(K)
+    # GPU-side flags order the ranks. Several engines share ONE device here, so their streams can
+    # share hardware work queues: a rank's halo wait queued ahead of a neighbour's boundary planes
+    # in a shared queue would never be satisfied. Enqueue step by step across the ranks (as one
+    # process per GPU never has to); every wait then sits behind the work it waits for.
+    for _ in range(K):
+        for e in ranks:
+            e.step_async(1)
     for e in ranks:
         assert e.sync() == (True, 0)
     assert whole.step_n(K)[0]

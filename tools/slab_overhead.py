@@ -38,8 +38,9 @@ def main():
         e.p2p_attach(blobs[lo] if lo is not None else None, blobs[hi] if hi is not None else None)
     for e in ranks:
         e.initialize_uniform()
-    for e in ranks:
-        e.step_async(8)
+    for _ in range(8):  # interleaved: the engines share one GPU's work queues
+        for e in ranks:
+            e.step_async(1)
     for e in ranks:
         e.sync()
     out = {}
