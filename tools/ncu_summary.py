@@ -1,6 +1,6 @@
 """Summarises ncu --set full reports of the step kernel into profiles/ (JSON + markdown rows).
 
-usage: python tools/ncu_summary.py OUT.json name=path.ncu-rep [...] [--bnode 304 --nodes N]"""
+usage: python tools/ncu_summary.py OUT.json name=path.ncu-rep|raw.csv [...] [--bnode 304 --nodes N]"""
 import csv
 import io
 import json
@@ -32,8 +32,11 @@ def read(path):
     if "@" in path:
         path, k = path.rsplit("@", 1)
         k = int(k)
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    if path.endswith(".csv"):  # an exported `ncu -i REP --page raw --csv` page
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h, u, v = rows[0], rows[1], rows[2 + k]
     rec = {"kernel": v[h.index("Kernel Name")]}

@@ -1,5 +1,5 @@
-"""Regenerates profiles/README.md from profiles/ncu_step_kernel.json, profiles/bench_r1.json and
-profiles/launches_r1.csv."""
+"""Regenerates profiles/README.md from profiles/ncu_step_kernel.json, profiles/bench_r2.json,
+profiles/launches_r2.csv, profiles/bench_ref_r2.json, profiles/ras1024_rn_fma_r2.jsonl and profiles/tma_probe_r2.csv."""
 import csv
 import json
 import os
@@ -10,11 +10,12 @@ PR = os.path.join(ROOT, "profiles")
 ALG = {"channel3d_128": 2032128 * 304, "ras256_phi05": 8540134 * 304,
        "ras256_phi02": 3513249 * 304, "cavity2d_4096_a4": 16764930 * 144,
        "channel3d_128_f32": 2032128 * 152, "channel3d_128_mrt": 2032128 * 304,
-       "channel3d_128_aa_phase1": 2032128 * 304, "channel3d_128_aa_phase2": 2032128 * 304}
+       "channel3d_128_aa_phase1": 2032128 * 304, "channel3d_128_aa_phase2": 2032128 * 304,
+       "vessel4096_a4": 3810696 * 144, "ras1024_phi02": 225477158 * 304}
 
 
 def launches():
-    rows = list(csv.reader(open(os.path.join(PR, "launches_r1.csv"))))
+    rows = list(csv.reader(open(os.path.join(PR, "launches_r2.csv"))))
     hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hdr]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
@@ -34,17 +35,17 @@ def launches():
 
 def main():
     d = json.load(open(os.path.join(PR, "ncu_step_kernel.json")))
-    b = json.load(open(os.path.join(PR, "bench_r1.json")))
-    L = ["# Round-1 profiles (B200, sm_100a)", "",
-         "* `ncu_step_kernel.json`: one `ncu --set full --clock-control none --import-source on -k regex:t2c_step -s 3 -c 1 python tools/profile_case.py <case> 5` capture per workload, summarised by `tools/ncu_summary.py`.",
-         "* `launches_r1.csv`: `ncu --metrics gpu__time_duration.sum --clock-control none -c 200 python bench.py --steps 50 --warmup 3 --no-sweep --no-cpu` (cold-cache, serialised per-launch times: compare shares, not absolutes).",
-         "* `bench_r1.json`: the `python bench.py` line of the same code.", "",
+    b = json.load(open(os.path.join(PR, "bench_r2.json")))
+    L = ["# Profiles (B200, sm_100a), round 2 (round-1 rows marked)", "",
+         "* `ncu_step_kernel.json`: one `ncu --set full --clock-control none --import-source on -k regex:t2c_step -s 4 -c 1 python tools/profile_case.py <case> 6` capture per workload (`tools/gpu_r2f.sh`; configs[4] with `--replay-mode application --cache-control none`), summarised by `tools/ncu_summary.py`; the f32 / MRT / single-copy rows are round 1.",
+         "* `launches_r2.csv`: `ncu --metrics gpu__time_duration.sum --clock-control none -c 400 python bench.py --steps 4 --warmup 3 --no-sweep --no-cpu --no-other --no-configs4` (cold-cache, serialised per-launch times: compare shares, not absolutes).",
+         "* `bench_r2.json` / `bench_ref_r2.json`: the `python bench.py` and `python bench.py --impl reference` lines of the same code (same box, `tools/gpu_r2f.sh`).", "",
          "## Step kernel per launch (ncu)", "",
-         "| workload | kernel | us | DRAM read MB | DRAM write MB | DRAM / algorithmic | DRAM % of peak | issue active % | warps active % | regs | top stalls |",
-         "|---|---|---|---|---|---|---|---|---|---|---|"]
+         "| workload | round | kernel | us | DRAM read MB | DRAM write MB | DRAM / algorithmic | DRAM % of peak | issue active % | warps active % | regs | top stalls |",
+         "|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for k, r in d.items():
         st = ", ".join(f"{n} {v}%" for n, v in list(r["top_stalls_pct"].items())[:3])
-        L.append(f"| {k} | `{r['kernel'].split('(')[0]}` | {r['duration_us']:.1f} | {r['dram_read_bytes'] / 1e6:.0f} | "
+        L.append(f"| {k} | {r.get('round', 1)} | `{r['kernel'].split('(')[0]}` | {r['duration_us']:.1f} | {r['dram_read_bytes'] / 1e6:.0f} | "
                  f"{r['dram_write_bytes'] / 1e6:.0f} | {r['dram_bytes_per_launch'] / ALG[k]:.3f} | {r['dram_pct_peak']:.1f} | "
                  f"{r['issue_active_pct']:.1f} | {r['warps_active_pct']:.1f} | {r['registers']:.0f} | {st} |")
     L += ["", "Dense cases read DRAM/algorithmic slightly below 1: part of the written copy is still dirty in L2 when a "
@@ -70,14 +71,24 @@ def main():
           "| line | phi | storage | device GB | MLUPS | frac of copy peak | SM MHz (median) | throttle | generate s (GPU) | engine build s |",
           "|---|---|---|---|---|---|---|---|---|---|"]
     for f in sorted(os.listdir(PR)):
-        if f.startswith("bench_r1_ras1024") and f.endswith(".json"):
-            x = json.load(open(os.path.join(PR, f)))
+        if not (f.startswith("bench_r1_ras1024") and f.endswith(".json")) and f != "ras1024_rn_fma_r2.jsonl":
+            continue
+        lines = open(os.path.join(PR, f)).read().split("\n")
+        for n, line in enumerate(l for l in lines if l.strip()):
+            x = json.loads(line)
             c = x["config"]
-            L.append(f"| `{f}` | {c['phi']} | {'single copy (AA)' if 'single-copy' in c['workload'] else 'two copies'} | "
+            tag = f if f.endswith(".json") else f"{f} #{n + 1} ({['RN', 'FMA', 'RN'][n]})"
+            hs = x.get("host_seconds", {})
+            L.append(f"| `{tag}` | {c['phi']} | {'single copy (AA)' if 'single-copy' in c['workload'] else 'two copies'} | "
                      f"{c['device_gb']} | {x['value']} | {x['roofline']['frac']} | {x['clocks']['sm_mhz']} | "
-                     f"{', '.join(x['clocks']['reasons']) or '-'} | {x['host_seconds']['generate']} | "
-                     f"{x['host_seconds']['engine_build']} |")
-    ref = os.path.join(PR, "bench_ref_r1.json")
+                     f"{', '.join(x['clocks']['reasons']) or '-'} | {hs.get('generate', '-')} | "
+                     f"{hs.get('engine_build', '-')} |")
+    c4 = b.get("configs4")
+    if c4:
+        L.append(f"| `bench_r2.json` configs4 (200 steps) | {c4['phi']} | two copies | {c4['device_gb']} | {c4['value']} | "
+                 f"{c4['roofline']['frac']} | {c4['clocks']['sm_mhz']} | {', '.join(c4['clocks']['reasons']) or '-'} | "
+                 f"{c4['host_seconds']['generate']} | {c4['host_seconds']['engine_build']} |")
+    ref = os.path.join(PR, "bench_ref_r2.json")
     if os.path.exists(ref):
         r = json.load(open(ref))
         L += ["", f"Reference arm (`bench.py --impl reference`, the reference's own TileEngineT2C<double> on "
