@@ -7,7 +7,7 @@ porosity; % of HBM peak GB/s; at 1/2/4/8 B200).
 Workload at N=1: BASELINE configs[1], the D3Q19 BGK fp64 128^3 channel with bounce-back walls
 (velocity inlet / pressure outlet), tiles 4^3, synthetic geometry. A "step" is one LBM time step
 (one launch of the fused step kernel over all tiles). value = N_f * K / device time of the K
-timed steps (CUDA events on the engine stream, max over ranks). The two PDF copies (1.3 GB) are
+timed steps (CUDA events on the engine stream, max over ranks). The two PDF copies (319 MB each) are
 larger than L2, so no flush is needed between steps. Also reported: the MLUPS-vs-porosity sweep
 (configs[2]: RAS 256^3, d=40, seed 7, periodic), the roofline of the step kernel against the
 measured HBM copy peak, the CPU reference baseline, and an end-to-end number through the public
@@ -342,10 +342,10 @@ def workload_config(n, nf):
     N=1 is BASELINE configs[1]; N>1 is the weak-scaled duct, one 128^3-node z-slab per GPU."""
     if n == 1:
         return {"workload": WORKLOAD_1, "fluid_nodes": int(nf),
-                "l2": "inputs > L2 (two PDF copies of 1.3 GB); no flush", "parallelism": "single GPU"}
+                "l2": "inputs > L2 (two PDF copies of 319 MB each); no flush", "parallelism": "single GPU"}
     return {"workload": f"D3Q19 BGK fp64 channel 128x128x{128 * n}, z-slab per GPU (128^3 nodes each)",
             "fluid_nodes": int(nf),
-            "l2": "inputs > L2 (two PDF copies of 1.3 GB per rank); no flush",
+            "l2": "inputs > L2 (two PDF copies of 319 MB each per rank); no flush",
             "parallelism": f"zslab{n}"}
 
 
