@@ -157,6 +157,11 @@ typedef struct {
   double phi_t;            /* tile porosity (tiling.cpp:223-225) */
   double ratio_tiles;      /* cells / non-empty tiles (tiling.cpp:227) */
   uint64_t n_tiles_global; /* non-empty tiles of the whole tile map */
+  /* Step path: 0 = one step-kernel launch per step (CUDA-graph batches); > 0 = the number of CTAs
+   * of the resident multi-step kernel (small whole-domain engines: a batch of steps inside one
+   * cooperative grid, a grid barrier between steps; SPLBM_RESIDENT=0 disables it). */
+  int resident_ctas;
+  int resident_threads;
 } splbm_dev_info;
 
 /* TileEngineT2C(g, a, model, periodic) ctor (engine.hpp:314-334): validates like the reference

@@ -46,7 +46,8 @@ class DevInfo(C.Structure):
                 ("q", C.c_int), ("a", C.c_int), ("d", C.c_int), ("grid_dims", C.c_int * 3),
                 ("padded_dims", C.c_int * 3), ("fluid_nodes", C.c_uint64),
                 ("device_bytes", C.c_uint64), ("phi_t", C.c_double), ("ratio_tiles", C.c_double),
-                ("n_tiles_global", C.c_uint64)]
+                ("n_tiles_global", C.c_uint64), ("resident_ctas", C.c_int),
+                ("resident_threads", C.c_int)]
 
 
 class SlabLayout(C.Structure):

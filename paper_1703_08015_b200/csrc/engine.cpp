@@ -74,6 +74,14 @@ const StreamMemOps& stream_mem_ops() {
 
 constexpr uint64_t kChunkNodes = 1ull << 22;  // initialize_arrays staging (4 x 32 MB)
 constexpr int kGraphSteps = 32;               // steps per captured graph (even)
+constexpr int kResidentSteps = 1024;          // steps per resident-kernel launch (small domains)
+
+// Resident multi-step kernels are cooperative grids that spin at grid barriers: two of them
+// running at once on one device could each hold SMs the other's unscheduled CTAs need. Every
+// resident launch in the process waits for the previous one on the same device (one event per
+// device), so at most one is in flight.
+std::mutex g_resident_mu;
+std::map<int, cudaEvent_t> g_resident_last;
 
 }  // namespace
 
@@ -118,6 +126,12 @@ struct splbm_dev_engine {
   int x2 = 1;         // StepArgs::x2: f32 two nodes per thread (SPLBM_X2=0 disables)
   int off32 = 1;      // StepArgs::off32 when the slots fit 32 bits (SPLBM_OFF32=0 disables)
   int pipe = 0;       // StepArgs::pipe (SPLBM_PIPE=1: software-pipelined persistent 3D step)
+  // resident multi-step batches (small whole-domain two-copy BGK engines, SPLBM_RESIDENT=0 off):
+  // res_blocks CTAs of res_threads threads, res_tpc tiles each; 0 = one launch per step
+  unsigned res_blocks = 0, res_threads = 0;
+  int res_tpc = 0;
+  unsigned* res_flags = nullptr;  // res_blocks x 32 epoch words (ResidentArgs::flags)
+  unsigned res_epoch = 0;         // resident steps enqueued so far
   // single-copy (AA) propagation: one PDF array (pdf[0]); `read` is then the state parity
   // (0 natural layout, 1 swapped, see t2c_aa_kernel)
   bool aa = false;
@@ -186,6 +200,7 @@ struct splbm_dev_engine {
                     static_cast<void*>(zero_base),
                     static_cast<void*>(halo_dirs), static_cast<void*>(scratch),
                     static_cast<void*>(reduce_buf), static_cast<void*>(order),
+                    static_cast<void*>(res_flags),
                     static_cast<void*>(cells), static_cast<void*>(frame)})
       if (p) cudaFree(p);
     if (ev0) cudaEventDestroy(ev0);
@@ -416,6 +431,30 @@ struct splbm_dev_engine {
     ++launches;
   }
 
+  // k steps from parity rd in one resident launch (+ the counter bump), serialised per device.
+  void enqueue_resident(int rd, int k) {
+    splbm_dev::ResidentArgs ra{};
+    ra.s = step_args(rd, 0);
+    ra.pdf0 = pdf[0];
+    ra.pdf1 = pdf[1];
+    ra.rd0 = rd;
+    ra.nsteps = k;
+    ra.tiles_per_cta = res_tpc;
+    ra.flags = res_flags;
+    ra.epoch0 = res_epoch;
+    res_epoch += static_cast<unsigned>(k);
+    {
+      std::lock_guard<std::mutex> lk(g_resident_mu);
+      cudaEvent_t& last = g_resident_last[device];
+      if (last) CK(cudaStreamWaitEvent(stream, last, 0));
+      else CK(cudaEventCreateWithFlags(&last, cudaEventDisableTiming));
+      CK(splbm_dev::launch_resident(d, incompressible != 0, f32, ra, res_blocks, res_threads, stream));
+      CK(cudaEventRecord(last, stream));
+    }
+    CK(splbm_dev::launch_bump(step_base, k, stream));
+    launches += 2;
+  }
+
   cudaGraphExec_t graph_for(int rd) {
     const auto key = std::make_pair(kGraphSteps, rd);
     auto it = graphs.find(key);
@@ -456,6 +495,14 @@ struct splbm_dev_engine {
       return;
     }
     long left = n;
+    if (res_blocks) {  // small domain: whole batches inside one cooperative grid
+      while (left > 0) {
+        const int k = static_cast<int>(std::min<long>(left, kResidentSteps));
+        enqueue_resident(read, k);
+        if (k & 1) read = 1 - read;
+        left -= k;
+      }
+    }
     while (left >= kGraphSteps) {
       CK(cudaGraphLaunch(graph_for(read), stream));
       launches += kGraphSteps + 1;
@@ -704,6 +751,29 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
     }
   }
   phase("device_tables");
+  // Resident multi-step batches (t2c_resident_kernel) when the whole domain fits one CTA of at
+  // most 1024 threads (512 for D3Q19 f64) per SM: there the launch gap, not HBM, sets the step time.
+  {
+    int coop = 0, sms = 0;
+    CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, e->device));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device));
+    const char* env = std::getenv("SPLBM_RESIDENT");
+    const bool want = env ? std::atoi(env) != 0 : true;
+    if (want && coop && sms > 0 && sms <= splbm_dev::kResidentMaxCtas && !slab_mode && !e->aa && e->mrt_K.empty() && e->n_own > 0 &&
+        nslots < (1ull << 32)) {
+      const uint64_t tpc = (e->n_own + sms - 1) / sms;
+      const uint64_t threads = (tpc * n_tn + 31) / 32 * 32;
+      if (splbm_dev::resident_fits(d, e->incompressible != 0, e->f32, static_cast<unsigned>(threads)) ==
+              cudaSuccess) {
+        e->res_tpc = static_cast<int>(tpc);
+        e->res_threads = static_cast<unsigned>(threads);
+        e->res_blocks = static_cast<unsigned>((e->n_own + tpc - 1) / tpc);
+        e->res_flags = e->alloc<unsigned>(32ull * e->res_blocks);
+        CK(cudaMemset(e->res_flags, 0, 32ull * e->res_blocks * sizeof(unsigned)));
+      }
+      cudaGetLastError();  // a rejected probe leaves no sticky error; clear the last-error slot
+    }
+  }
 }
 
 // GPU-built engines keep the tile cover on the device until a caller needs the host TileMap
@@ -798,6 +868,8 @@ int splbm_dev_get_info(const splbm_dev_engine* e, splbm_dev_info* out) {
     const double cells = static_cast<double>(e->tm.grid_dims[0]) * e->tm.grid_dims[1] * e->tm.grid_dims[2];
     out->ratio_tiles = e->tm.n_tiles ? cells / static_cast<double>(e->tm.n_tiles) : 0.0;
     out->n_tiles_global = e->tm.n_tiles;
+    out->resident_ctas = static_cast<int>(e->res_blocks);
+    out->resident_threads = static_cast<int>(e->res_threads);
   });
 }
 
@@ -894,7 +966,7 @@ int splbm_dev_step_async(splbm_dev_engine* e, long nsteps) {
       CK(cudaMemsetAsync(e->failed, 0xff, sizeof(unsigned long long), e->stream));
     }
     // instantiate the batch graph (host work) before the timing event, not inside the batch
-    if (nsteps >= kGraphSteps && !e->comm && !e->p2p) e->graph_for(e->read);
+    if (nsteps >= kGraphSteps && !e->comm && !e->p2p && !e->res_blocks) e->graph_for(e->read);
     CK(cudaEventRecord(e->ev0, e->stream));
     e->enqueue_steps(nsteps);
     CK(cudaEventRecord(e->ev1, e->stream));

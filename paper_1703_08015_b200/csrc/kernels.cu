@@ -709,6 +709,117 @@ __global__ void __launch_bounds__(aa_threads<D, LOGA>(),
 // Advances the step counter the failure stamps are relative to (one per enqueued batch).
 __global__ void bump_kernel(long long* step_base, long long by) { *step_base += by; }
 
+// ---------------------------------------------------------------------------------------------
+// Resident multi-step kernel for small domains (whole domain on one CTA per SM, e.g. BASELINE
+// configs[0], 65 K nodes: the per-step launch gap is the step time there). One cooperative grid
+// runs a whole batch of steps; every thread keeps its node for the batch, its q gather slots
+// (the natural-state gather of engine.hpp:485-501, blocked directions included) are resolved once
+// into shared memory, and consecutive steps are separated by a neighbour-CTA flag sync. The PDF gathers go
+// through L2 only (ld.global.cg): a copy written by other CTAs in step s is read in step s+1 of
+// the same kernel, so the non-coherent L1 path of the streamed kernels is not allowed here. Same
+// slots, same arithmetic, same zero-fill: bit-identical to the one-launch-per-step path.
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ double ld_l2(const double* p) {
+  double v;
+  asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ float ld_l2(const float* p) {
+  float v;
+  asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Between steps a CTA waits only for the CTAs that own tiles next to its own (the only ones whose
+// step-s values it gathers in step s+1, and the only ones that gathered its step-s inputs, which
+// step s+1 overwrites): each CTA release-stores its step epoch into its own flag word, then its
+// threads poll the neighbour CTAs' flags with acquire loads, one flag per thread. Measured on B200
+// (tools/barrier_probe.cu): a grid-wide barrier costs 1.2-2 us per step, more than the step.
+__device__ __forceinline__ void neighbour_sync(unsigned* flags, unsigned epoch, const uint16_t* nbr,
+                                               int n_nbr) {
+  __syncthreads();
+  if (threadIdx.x == 0) st_release_gpu(flags + blockIdx.x * 32, epoch);  // cumulative over the CTA
+  for (int j = threadIdx.x; j < n_nbr; j += blockDim.x)
+    while (static_cast<int>(ld_acquire_gpu(flags + nbr[j] * 32) - epoch) < 0) {
+    }
+  __syncthreads();
+}
+
+// Largest CTA of the resident kernel: 1024 threads (64 registers) except D3Q19 in f64, whose 19
+// doubles spill at 64 (and at 80) registers: 512 threads.
+template <int D, class R>
+__host__ __device__ constexpr int resident_threads_max() { return D == 3 && sizeof(R) == 8 ? 512 : 1024; }
+
+template <int D, bool INC, class R>
+__global__ void __launch_bounds__(resident_threads_max<D, R>(), 1) t2c_resident_kernel(ResidentArgs ra) {
+  constexpr int Q = Lat<D>::Q;
+  extern __shared__ uint32_t s_src[];  // [Q][blockDim.x] gather slot of direction i
+  const StepArgs& a = ra.s;
+  const int n_tn = a.a * a.a * (D == 3 ? a.a : 1);
+  const uint64_t k = static_cast<uint64_t>(blockIdx.x) * ra.tiles_per_cta * n_tn + threadIdx.x;
+  const bool live = threadIdx.x < static_cast<unsigned>(ra.tiles_per_cta * n_tn) && k < a.n_nodes;
+  const uint64_t t = a.t0 + (live ? k / n_tn : 0);
+  const int p = live ? static_cast<int>(k % n_tn) : 0;
+  const uint32_t info = live ? __ldg(a.info + t * n_tn + p) : 0u;
+  const int type = (info >> 24) & 3;
+  const bool zero_fill = live && type == 0 && (info & (1u << 27));
+  const uint32_t own = static_cast<uint32_t>(t * Q * n_tn + p);  // slot (t, 0, p): < 2^32 (engine)
+  const unsigned bd = blockDim.x;
+#pragma unroll
+  for (int i = 0; i < Q; ++i)
+    s_src[i * bd + threadIdx.x] =
+        type != 0 ? static_cast<uint32_t>(gather_slot<D>(a.nb, info, a.a, n_tn, t, p, i)) : 0u;
+  // the CTAs owning the neighbour tiles of this CTA's tiles (kResidentMaxCtas bits)
+  __shared__ unsigned s_bits[kResidentMaxCtas / 32];
+  __shared__ uint16_t s_nbr[kResidentMaxCtas];
+  __shared__ int s_n_nbr;
+  for (int w = threadIdx.x; w < kResidentMaxCtas / 32; w += bd) s_bits[w] = 0u;
+  if (threadIdx.x == 0) s_n_nbr = 0;
+  __syncthreads();
+  if (live && p == 0) {
+    constexpr int NBS = D == 3 ? 27 : 9;
+    for (int c = 0; c < NBS; ++c) {
+      const uint32_t u = __ldg(a.nb + t * NBS + c);
+      if (u == kEmpty || u < a.t0) continue;
+      const uint64_t owner = (u - a.t0) / ra.tiles_per_cta;
+      if (owner < gridDim.x && owner != blockIdx.x) atomicOr(&s_bits[owner / 32], 1u << (owner % 32));
+    }
+  }
+  __syncthreads();
+  for (unsigned c = threadIdx.x; c < gridDim.x; c += bd)
+    if (s_bits[c / 32] & (1u << (c % 32))) s_nbr[atomicAdd(&s_n_nbr, 1)] = static_cast<uint16_t>(c);
+  __syncthreads();
+  const int n_nbr = s_n_nbr;
+  const long long base = *a.step_base;
+  const R inv_tau = static_cast<R>(a.inv_tau);
+  for (int s = 0; s < ra.nsteps; ++s) {
+    const int rd = (ra.rd0 + s) & 1;
+    const R* src = static_cast<const R*>(rd ? ra.pdf1 : ra.pdf0);
+    R* dst = static_cast<R*>(rd ? ra.pdf0 : ra.pdf1) + own;
+    if (type != 0) {
+      R f[Q];
+#pragma unroll
+      for (int i = 0; i < Q; ++i) f[i] = ld_l2(src + s_src[i * bd + threadIdx.x]);
+      const bool good = type == 1 ? collide_bgk<D, INC>(f, inv_tau)
+                                  : apply_boundary<D, INC>(f, type, (info >> 26) & 1u, a.bc);
+      if (!good) atomicMin(a.failed, static_cast<unsigned long long>(base + s + 1));
+#pragma unroll
+      for (int i = 0; i < Q; ++i) dst[i * n_tn] = f[i];
+    } else if (zero_fill) {
+#pragma unroll
+      for (int i = 0; i < Q; ++i) dst[i * n_tn] = R(0);
+    }
+    if (s + 1 < ra.nsteps) neighbour_sync(ra.flags, ra.epoch0 + s + 1, s_nbr, n_nbr);
+  }
+}
+
 // Slab halo-arrival wait (p2p transport): one thread polls the "faces arrived" flags with
 // system-scope acquire loads until both reach `seq`. The neighbours publish a flag only after
 // their boundary planes (whose peer stores into my halo tiles precede it: stream write-value with
@@ -1201,6 +1312,45 @@ struct UnswapL {
 
 cudaError_t launch_step(int d, bool inc, bool f32, const StepArgs& a, cudaStream_t st) {
   return dispatch<StepL>(d, inc, f32, a, st);
+}
+
+template <int D, bool INC, class R>
+struct ResidentL {
+  static cudaError_t run(const ResidentArgs& ra, unsigned blocks, unsigned threads, cudaStream_t st,
+                         bool probe) {
+    auto kern = t2c_resident_kernel<D, INC, R>;
+    const size_t smem = static_cast<size_t>(Lat<D>::Q) * threads * sizeof(uint32_t);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    if (probe) {  // one CTA of this size resident per SM?
+      if (threads > static_cast<unsigned>(resident_threads_max<D, R>())) return cudaErrorInvalidValue;
+      int occ = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, static_cast<int>(threads), smem);
+      if (e != cudaSuccess) return e;
+      return occ >= 1 ? cudaSuccess : cudaErrorCooperativeLaunchTooLarge;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, ra);
+  }
+};
+
+cudaError_t launch_resident(int d, bool inc, bool f32, const ResidentArgs& ra, unsigned blocks,
+                            unsigned threads, cudaStream_t st) {
+  return dispatch<ResidentL>(d, inc, f32, ra, blocks, threads, st, false);
+}
+
+cudaError_t resident_fits(int d, bool inc, bool f32, unsigned threads) {
+  return dispatch<ResidentL>(d, inc, f32, ResidentArgs{}, 1u, threads, cudaStream_t{}, true);
 }
 
 cudaError_t launch_bump(long long* step_base, long long by, cudaStream_t st) {

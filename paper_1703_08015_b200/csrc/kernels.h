@@ -137,6 +137,25 @@ struct HaloArgs {
   const uint32_t* info;
 };
 
+// Resident multi-step batch (small whole-domain two-copy BGK engines): one cooperative grid of
+// `blocks` (<= kResidentMaxCtas) CTAs x `threads` (tiles_per_cta whole tiles each) runs `nsteps`
+// steps from copy rd0; between steps each CTA waits for the CTAs owning its neighbour tiles
+// (per-CTA epoch flags). StepArgs::read/write are unused (pdf0/pdf1 alternate).
+constexpr int kResidentMaxCtas = 256;
+struct ResidentArgs {
+  StepArgs s;
+  void* pdf0;
+  void* pdf1;
+  int rd0;
+  int nsteps;
+  int tiles_per_cta;
+  unsigned* flags;  // blocks x 32 words: CTA c's step epoch at flags[32 c]; zero at creation
+  unsigned epoch0;  // resident steps completed before this launch (engine counter)
+};
+cudaError_t launch_resident(int d, bool inc, bool f32, const ResidentArgs& a, unsigned blocks,
+                            unsigned threads, cudaStream_t st);
+// cudaSuccess when one CTA of `threads` threads of the resident kernel fits an SM.
+cudaError_t resident_fits(int d, bool inc, bool f32, unsigned threads);
 cudaError_t launch_step(int d, bool inc, bool f32, const StepArgs& a, cudaStream_t st);
 cudaError_t launch_bump(long long* step_base, long long by, cudaStream_t st);
 // Slab p2p: wait (system-scope acquire polling) until the non-null flags reach seq.

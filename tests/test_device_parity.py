@@ -27,13 +27,19 @@ def assert_fields_equal(fo, fd):
         assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), k
 
 
+@pytest.mark.parametrize("path", ["resident", "streamed"])
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_step_bitwise(name, oracle):
+def test_step_bitwise(name, path, oracle, monkeypatch):
+    """`resident`: the default engine (small domains run whole batches in the resident multi-step
+    kernel); `streamed`: SPLBM_RESIDENT=0, one step-kernel launch per step."""
     factory, a, tau, inc, per, init = CASES[name]
     g = factory()
     model = P.FluidModel(P.Compressibility.Incompressible if inc else P.Compressibility.QuasiCompressible,
                          tau=tau)
+    monkeypatch.setenv("SPLBM_RESIDENT", "1" if path == "resident" else "0")
     de = P.TileEngineT2C(g, a, model, per)
+    if path == "streamed":
+        assert de.info.resident_ctas == 0
     oe = make_oracle(oracle, g, a, tau, inc, per)
     tg = de.tile_grid()
     assert np.array_equal(tg.tile_map, oe.tiles["tile_map"])
