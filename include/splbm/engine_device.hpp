@@ -12,6 +12,7 @@
 
 #include <array>
 #include <cstdint>
+#include <stdexcept>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -69,6 +70,8 @@ class TileEngineT2CDeviceT : public Engine<T> {
     desc.single_precision = std::is_same_v<T, float> ? 1 : 0;
     if (desc.mrt_rates && static_cast<int>(model.mrt_rates.size()) != (g.d == 2 ? 9 : 19))
       throw ConfigError("mrt_rates must have one entry per moment");
+    if (splbm_dev_info_size() != sizeof(splbm_dev_info))
+      throw std::runtime_error("libsplbm_b200.so was built from another revision of splbm_b200.h");
     device_detail::check(splbm_dev_create(&desc, &e_));
     device_detail::check(splbm_dev_get_info(e_, &info_));
     tile_.resize(info_.n_tiles_stored);

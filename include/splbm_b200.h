@@ -37,6 +37,9 @@ typedef enum {
 
 const char* splbm_last_error(void);
 const char* splbm_version(void);
+/* sizeof(splbm_dev_info) as compiled into the library: callers built against another revision of
+ * this header compare it with their own sizeof and refuse to run on a mismatch (ABI guard). */
+size_t splbm_dev_info_size(void);
 
 /* ---- geometry (geometry.hpp:27-82; input side of the path) -------------------------------- */
 typedef enum {

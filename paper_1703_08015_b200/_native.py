@@ -64,6 +64,7 @@ _lib = None
 SIGNATURES = {
     "splbm_last_error": ([], C.c_char_p),
     "splbm_version": ([], C.c_char_p),
+    "splbm_dev_info_size": ([], C.c_size_t),
     "splbm_generate": ([C.c_int, C.POINTER(GenerateParams), _u8, C.POINTER(C.c_int), _dp,
                         C.POINTER(C.c_double)], C.c_int),
     "splbm_generate_device": ([C.c_int, C.POINTER(GenerateParams), C.c_int, _u8, C.POINTER(C.c_int),
@@ -154,6 +155,10 @@ def load(path: str):
         fn.argtypes = args
         fn.restype = res
     L.missing_symbols = missing
+    if hasattr(L, "splbm_dev_info_size") and L.splbm_dev_info_size() != C.sizeof(DevInfo):
+        raise ImportError(f"{path} was built from another revision of include/splbm_b200.h "
+                          f"(splbm_dev_info is {L.splbm_dev_info_size()} bytes there, "
+                          f"{C.sizeof(DevInfo)} here); rebuild it")
     return L
 
 

@@ -836,6 +836,7 @@ extern "C" {
 
 const char* splbm_last_error(void) { return g_last_error.c_str(); }
 const char* splbm_version(void) { return "splbm_b200 0.1 (sm_100a)"; }
+size_t splbm_dev_info_size(void) { return sizeof(splbm_dev_info); }
 
 int splbm_dev_create(const splbm_dev_desc* desc, splbm_dev_engine** out) {
   if (!out) return SPLBM_ERR_CONFIG;

@@ -70,6 +70,9 @@ __host__ __device__ constexpr int nb_offset() { return D == 3 ? 0 : 9; }
 #ifndef SPLBM_MINB_MRT2
 #define SPLBM_MINB_MRT2 4  // the 2D MRT step: +12 % vs 2 (interleaved A/B)
 #endif
+#ifndef SPLBM_AA1_MINB
+#define SPLBM_AA1_MINB 4  // single-copy phase 1: 256-thread CTA equivalents per SM (64 registers)
+#endif
 #ifndef SPLBM_ZERO_FILL
 #define SPLBM_ZERO_FILL 1  // write 0.0 to solid slots sharing a 32-B sector with fluid slots
 #endif
@@ -618,7 +621,7 @@ __host__ __device__ constexpr int aa_threads() {
 }
 template <int D, int LOGA, bool INC, bool MRT, int PHASE, class R, bool PEER = false>
 __global__ void __launch_bounds__(aa_threads<D, LOGA>(),
-                                  (MRT ? 2 : (D == 3 ? (PHASE == 1 ? 3 : SPLBM_MINB3) : SPLBM_MINB2)) * 256 / aa_threads<D, LOGA>())
+                                  (MRT ? 2 : (D == 3 ? (PHASE == 1 ? SPLBM_AA1_MINB : SPLBM_MINB3) : SPLBM_MINB2)) * 256 / aa_threads<D, LOGA>())
     t2c_aa_kernel(StepArgs args, const __grid_constant__ MrtMatrix<R, MRT ? Lat<D>::Q : 1> mrt) {
   constexpr int Q = Lat<D>::Q;
   constexpr int A = 1 << LOGA;
@@ -702,8 +705,39 @@ __global__ void __launch_bounds__(aa_threads<D, LOGA>(),
     good = apply_boundary<D, INC>(f, type, (info >> 26) & 1u, args.bc);
   }
   if (!good) atomicMin(args.failed, static_cast<unsigned long long>(*args.step_base + args.rel + 1));
+  if constexpr (PHASE == 1) {
+    // Nothing but f[] stays live through the collision: the node's tile, position and gather word
+    // are re-derived from opaque reads of the CTA/thread index (the compiler cannot keep the old
+    // values instead) and the scatter addresses recomputed from the shared-memory bases. 64
+    // registers without spills (80 with 28 B of spills otherwise): channel / RAS phi 0.5 / 2D
+    // -3 / -6 / -3 % per single-copy step (interleaved A/B, profiles/ab_aa1_r2.txt).
+    uint32_t bx, tx;
+    asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(bx));
+    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tx));
+    const int tl2 = static_cast<int>(tx) / NTN;
+    const int p2 = static_cast<int>(tx) % NTN;
+    const uint64_t t2 = tile_of(args, static_cast<uint64_t>(bx) * TILES + tl2);
+    uint32_t info2;
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(info2) : "l"(args.info + t2 * NTN + p2));
+    R* own2 = pdf + t2 * STRIDE;
+    R* const* nbp2 = s_base[tl2];
+    const int lx2 = p2 & (A - 1), ly2 = (p2 >> LOGA) & (A - 1), lz2 = D == 3 ? (p2 >> (2 * LOGA)) : 0;
 #pragma unroll
-  for (int i = 0; i < Q; ++i) st_stream(PHASE == 1 ? addr(opp(i)) : own + (i * NTN + p), f[i]);
+    for (int i = 0; i < Q; ++i) {
+      const int j = opp(i);
+      const int vx = lx2 - ex<D>(j), vy = ly2 - ey<D>(j), vz = lz2 - ez<D>(j);
+      const int dx = ex<D>(j) ? (vx >> LOGA) : 0;
+      const int dy = ey<D>(j) ? (vy >> LOGA) : 0;
+      const int dz = (D == 3 && ez<D>(j)) ? (vz >> LOGA) : 0;
+      const int sp = (vx & (A - 1)) | ((vy & (A - 1)) << LOGA) | (D == 3 ? ((vz & (A - 1)) << (2 * LOGA)) : 0);
+      const int delta = 13 + dx + 3 * dy + 9 * dz;
+      R* dst = (delta == 13 ? own2 : nbp2[delta - nb_offset<D>()]) + (j * NTN + sp);
+      st_stream(((info2 >> j) & 1u) ? own2 + (i * NTN + p2) : dst, f[i]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < Q; ++i) st_stream(own + (i * NTN + p), f[i]);
+  }
 }
 
 // Advances the step counter the failure stamps are relative to (one per enqueued batch).

@@ -29,6 +29,17 @@ def test_every_declared_symbol_is_exported_and_bound():
         assert n in _native.SIGNATURES, n
 
 
+def test_info_struct_layout_matches_the_library():
+    """The library's sizeof(splbm_dev_info) equals the Python mirror's (a stale build against an
+    older header would otherwise write past the caller's struct)."""
+    for L in (_native.lib(), _native.lib("fma")):
+        assert L.splbm_dev_info_size() == ctypes.sizeof(_native.DevInfo)
+    src = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    body = re.search(r"typedef struct \{([^}]*)\} splbm_dev_info;", src).group(1)
+    fields = re.findall(r"\b([a-z_0-9]+)(?:\[\d+\])?\s*[;,]", body)
+    assert [f for f, _ in _native.DevInfo._fields_] == fields
+
+
 def test_tolerance_mode_library_exports_the_same_abi():
     """libsplbm_b200_fma.so (arithmetic="fma") is the same sources with SPLBM_FMA=1."""
     L = _native.lib("fma")
