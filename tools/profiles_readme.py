@@ -11,7 +11,8 @@ ALG = {"channel3d_128": 2032128 * 304, "ras256_phi05": 8540134 * 304,
        "ras256_phi02": 3513249 * 304, "cavity2d_4096_a4": 16764930 * 144,
        "channel3d_128_f32": 2032128 * 152, "channel3d_128_mrt": 2032128 * 304,
        "channel3d_128_aa_phase1": 2032128 * 304, "channel3d_128_aa_phase2": 2032128 * 304,
-       "vessel4096_a4": 3810696 * 144, "ras1024_phi02": 225477158 * 304}
+       "vessel4096_a4": 3810696 * 144, "ras1024_phi02": 225477158 * 304,
+       "cavity2d_256_a4_resident": 64770 * 144 * 200, "cavity2d_256_a4_streamed": 64770 * 144}
 
 
 def launches():
@@ -37,9 +38,9 @@ def main():
     d = json.load(open(os.path.join(PR, "ncu_step_kernel.json")))
     b = json.load(open(os.path.join(PR, "bench_r2.json")))
     L = ["# Profiles (B200, sm_100a), round 2 (round-1 rows marked)", "",
-         "* `ncu_step_kernel.json`: one `ncu --set full --clock-control none --import-source on -k regex:t2c_step -s 4 -c 1 python tools/profile_case.py <case> 6` capture per workload (`tools/gpu_r2f.sh`; configs[4] with `--replay-mode application --cache-control none`), summarised by `tools/ncu_summary.py`; the f32 / MRT / single-copy rows are round 1.",
+         "* `ncu_step_kernel.json`: one `ncu --set full --clock-control none --import-source on -k regex:t2c_step -s 4 -c 1 python tools/profile_case.py <case> 6` capture per workload (`tools/gpu_r2f.sh`; configs[4] with `--replay-mode application --cache-control none`; the single-copy pair and the configs[0] resident / streamed rows from `tools/gpu_r2n.sh`), summarised by `tools/ncu_summary.py`; the f32 / MRT / cavity 4096² rows are round 1. The `cavity2d_256_a4_resident` launch is a whole 200-step resident batch (2.87 µs per step); its PDFs stay in L2, so DRAM/algorithmic is ~0.",
          "* `launches_r2.csv`: `ncu --metrics gpu__time_duration.sum --clock-control none -c 400 python bench.py --steps 4 --warmup 3 --no-sweep --no-cpu --no-other --no-configs4` (cold-cache, serialised per-launch times: compare shares, not absolutes).",
-         "* `bench_r2.json` / `bench_ref_r2.json`: the `python bench.py` and `python bench.py --impl reference` lines of the same code (same box, `tools/gpu_r2f.sh`).", "",
+         "* `bench_r2.json` / `bench_ref_r2.json`: the `python bench.py` and `python bench.py --impl reference` lines of the same code (same box, `tools/gpu_r2n.sh`).", "",
          "## Step kernel per launch (ncu)", "",
          "| workload | round | kernel | us | DRAM read MB | DRAM write MB | DRAM / algorithmic | DRAM % of peak | issue active % | warps active % | regs | top stalls |",
          "|---|---|---|---|---|---|---|---|---|---|---|---|"]
@@ -71,7 +72,7 @@ def main():
           "| line | phi | storage | device GB | MLUPS | frac of copy peak | SM MHz (median) | throttle | generate s (GPU) | engine build s |",
           "|---|---|---|---|---|---|---|---|---|---|"]
     for f in sorted(os.listdir(PR)):
-        if not (f.startswith("bench_r1_ras1024") and f.endswith(".json")) and f != "ras1024_rn_fma_r2.jsonl":
+        if not (f.startswith(("bench_r1_ras1024", "bench_r2_ras1024")) and f.endswith(".json")) and f != "ras1024_rn_fma_r2.jsonl":
             continue
         lines = open(os.path.join(PR, f)).read().split("\n")
         for n, line in enumerate(l for l in lines if l.strip()):

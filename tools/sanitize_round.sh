@@ -1,6 +1,7 @@
 #!/bin/bash
 # compute-sanitizer memcheck / racecheck / initcheck over the step paths (two copies, single copy,
-# f32, pow2 and generic kernels) and the device RAS generator; summary table on stdout.
+# f32, pow2 and generic kernels, the resident multi-step kernel) and the device RAS generator;
+# summary table on stdout.
 mkdir -p gpurun_out/san
 cd "$(dirname "$0")/.."
 run() {  # name env case
@@ -18,3 +19,8 @@ run cavity2d_a16_single_copy "SPLBM_SINGLE_COPY=1" cavity2d_64_a16
 run random_a3_generic "SPLBM_PRECISION=f64" random_a3
 run ras48_mrt "SPLBM_MODEL=mrt" ras48_periodic
 run ras_device_generator "SPLBM_PRECISION=f64" ras_device_generator
+# round 2: the resident multi-step kernel (small domains: cooperative grid, neighbour-CTA flags)
+run cavity2d_256_resident "SPLBM_PRECISION=f64" cavity2d_256_a4
+run cavity2d_256_resident_f32 "SPLBM_PRECISION=f32" cavity2d_256_a4
+run channel3d_small_resident "SPLBM_PRECISION=f64" channel3d_small
+run channel3d_small_streamed "SPLBM_RESIDENT=0" channel3d_small
