@@ -125,7 +125,6 @@ struct splbm_dev_engine {
   uint64_t pdl_min_threads = 4ull * 148 * 256;  // StepArgs::pdl_min_threads (SPLBM_PDL_MIN)
   int x2 = 1;         // StepArgs::x2: f32 two nodes per thread (SPLBM_X2=0 disables)
   int off32 = 1;      // StepArgs::off32 when the slots fit 32 bits (SPLBM_OFF32=0 disables)
-  int pipe = 0;       // StepArgs::pipe (SPLBM_PIPE=1: software-pipelined persistent 3D step)
   // resident multi-step batches (small whole-domain two-copy BGK engines, SPLBM_RESIDENT=0 off):
   // res_blocks CTAs of res_threads threads, res_tpc tiles each; 0 = one launch per step
   unsigned res_blocks = 0, res_threads = 0;
@@ -251,7 +250,6 @@ struct splbm_dev_engine {
     s.x2 = x2;
     s.off32 = off32 && n_stored * tile_stride() < (1ull << 32);
     s.order = order;
-    s.pipe = pipe && !aa && !peer_part1;
     if (peer_part1 && aa) {  // single copy: phase 1 reads/writes the halo nodes' slots in place
       if (rd == 0) {
         s.peer_down = peer_pdf_down[0] ? peer_pdf_down[0] + peer_down_own0 * tile_stride() : nullptr;
@@ -584,7 +582,6 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
     if (const char* v = std::getenv("SPLBM_PDL_MIN")) e->pdl_min_threads = std::strtoull(v, nullptr, 10);
     if (const char* v = std::getenv("SPLBM_X2")) e->x2 = std::atoi(v);
     if (const char* v = std::getenv("SPLBM_OFF32")) e->off32 = std::atoi(v);
-    if (const char* v = std::getenv("SPLBM_PIPE")) e->pipe = std::atoi(v);
   }
   phase("device_select");
   CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));

@@ -374,136 +374,6 @@ __global__ void __launch_bounds__((step_threads<D, (D == 3 ? (1 << (3 * LOGA)) :
   }
 }
 
-// Software-pipelined persistent step (3D, a = 4, f64; SPLBM_PIPE): each 64-thread CTA walks the
-// tile ordinals blockIdx.x, blockIdx.x + G, ... and overlaps three stages per iteration: the
-// static tables (info word, neighbour row) of tile k+2 are loaded, the 19 gathers of tile k+1 are
-// issued as asynchronous 8-B copies (cp.async, .L2::64B fetch size) into a shared-memory stage,
-// and tile k is collided from the stage filled one iteration earlier. The gathers hold no
-// registers while in flight, so every resident thread keeps a whole node's gathers outstanding
-// through its collision — the in-flight depth the one-shot kernel only has during its load phase
-// (the sparse-medium step is bound by outstanding partial-line requests). Same
-// addresses, same slots, same arithmetic: bit-identical to t2c_step_pow2_kernel.
-#ifndef SPLBM_PIPE_MINB
-#define SPLBM_PIPE_MINB 10  // resident CTAs per SM: 19.9 KB of shared memory each
-#endif
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global.L2::64B [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <bool INC, bool MRT>
-__global__ void __launch_bounds__(64, SPLBM_PIPE_MINB)
-    t2c_step_pipe_kernel(StepArgs args, const __grid_constant__ MrtMatrix<double, MRT ? 19 : 1> mrt) {
-  constexpr int D = 3, Q = 19, LOGA = 2, A = 4, NTN = 64;
-  constexpr uint64_t STRIDE = static_cast<uint64_t>(Q) * NTN;
-  __shared__ double stage[2][Q][NTN];
-  __shared__ const double* s_base[2][27];
-  const double* const rd = static_cast<const double*>(args.read);
-  const uint64_t n_tiles = args.n_nodes / NTN;
-  const uint64_t G = gridDim.x;
-  const int p = threadIdx.x;
-  const int lx = p & (A - 1), ly = (p >> LOGA) & (A - 1), lz = p >> (2 * LOGA);
-
-  auto issue = [&](int buf, uint64_t t, uint32_t w) {  // gathers of one tile into stage[buf]
-    if (((w >> 24) & 3u) != 0u) {
-      const double* own = rd + t * STRIDE;
-      const double* const* nbp = s_base[buf];
-#pragma unroll
-      for (int i = 0; i < Q; ++i) {
-        const int vx = lx - ex<D>(i), vy = ly - ey<D>(i), vz = lz - ez<D>(i);
-        const int dx = ex<D>(i) ? (vx >> LOGA) : 0;
-        const int dy = ey<D>(i) ? (vy >> LOGA) : 0;
-        const int dz = ez<D>(i) ? (vz >> LOGA) : 0;
-        const int sp = (vx & (A - 1)) | ((vy & (A - 1)) << LOGA) | ((vz & (A - 1)) << (2 * LOGA));
-        const int delta = 13 + dx + 3 * dy + 9 * dz;
-        const double* src = (delta == 13 ? own : nbp[delta]) + (i * NTN + sp);
-        const double* bb = own + (opp(i) * NTN + p);  // half-way bounce-back (engine.hpp:498-500)
-        cp_async8(&stage[buf][i][p], ((w >> i) & 1u) ? bb : src);
-      }
-    }
-    cp_async_commit();  // (an empty group for solid nodes keeps the group count uniform)
-  };
-  auto base_of = [&](uint32_t s) -> const double* { return s == kEmpty ? nullptr : rd + static_cast<uint64_t>(s) * STRIDE; };
-
-  // prologue: static tables of the first two ordinals (before the previous step has finished)
-  uint64_t k = blockIdx.x;
-  uint64_t t0 = 0, t1 = 0;
-  uint32_t w0 = 0u, w1 = 0u;
-  if (k < n_tiles) {
-    t0 = tile_of(args, k);
-    w0 = __ldg(args.info + t0 * NTN + p);
-    if (p < 27) s_base[0][p] = base_of(__ldg(args.nb + t0 * 27 + p));
-  }
-  if (k + G < n_tiles) {
-    t1 = tile_of(args, k + G);
-    w1 = __ldg(args.info + t1 * NTN + p);
-    if (p < 27) s_base[1][p] = base_of(__ldg(args.nb + t1 * 27 + p));
-  }
-  __syncthreads();
-#if SPLBM_PDL
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-#endif
-  if (k < n_tiles) issue(0, t0, w0);
-  else cp_async_commit();
-
-  for (int it = 0; k < n_tiles; ++it, k += G) {
-    const int buf = it & 1;
-    const uint64_t k1 = k + G, k2 = k + 2 * G;
-    __syncthreads();  // s_base[buf ^ 1] (ordinal k1) written by every thread
-    if (k1 < n_tiles) issue(buf ^ 1, t1, w1);
-    else cp_async_commit();
-    uint64_t t2 = 0;
-    uint32_t w2 = 0u, s2 = kEmpty;
-    if (k2 < n_tiles) {  // tables of k2: in flight during the collision of k
-      t2 = tile_of(args, k2);
-      w2 = __ldg(args.info + t2 * NTN + p);
-      if (p < 27) s2 = __ldg(args.nb + t2 * 27 + p);
-    }
-    cp_async_wait<1>();  // this thread's gathers of ordinal k have landed
-    const int type = (w0 >> 24) & 3;
-    double* wr = static_cast<double*>(args.write) + t0 * STRIDE + p;
-    if (type == 0) {
-      if (w0 & (1u << 27)) {
-#pragma unroll
-        for (int i = 0; i < Q; ++i) st_stream(wr + i * NTN, 0.0);
-      }
-    } else {
-      double f[Q];
-#pragma unroll
-      for (int i = 0; i < Q; ++i) f[i] = stage[buf][i][p];
-      bool good;
-      if (type == 1) {
-        if constexpr (MRT)
-          good = collide_mrt<D, INC>(f, mrt.K);
-        else
-          good = collide_bgk<D, INC>(f, args.inv_tau);
-      } else {
-        good = apply_boundary<D, INC>(f, type, (w0 >> 26) & 1u, args.bc);
-      }
-      if (!good) atomicMin(args.failed, static_cast<unsigned long long>(*args.step_base + args.rel + 1));
-#pragma unroll
-      for (int i = 0; i < Q; ++i) st_stream(wr + i * NTN, f[i]);
-    }
-    // ordinal k's bases were last read when its gathers were issued (before this iteration's
-    // barrier): the slot now takes ordinal k2's row
-    if (p < 27) s_base[buf][p] = base_of(s2);
-    t0 = t1;
-    w0 = w1;
-    t1 = t2;
-    w1 = w2;
-  }
-  cp_async_wait<0>();
-}
-
 // Two nodes per thread (the f32 engine): a float gather moves half the bytes of a double one, so
 // one node per thread leaves too few bytes in flight; here thread j of a tile's half takes nodes j
 // and j + NTN/2 and issues both gathers (2 x q loads) before either collision: +7-13 % over one
@@ -1172,24 +1042,6 @@ static void launch_maybe_pdl(Kern kern, unsigned blocks, cudaStream_t st, const 
   kern<<<blocks, threads, 0, st>>>(a, m);
 }
 
-// Persistent grid of the pipelined step: every SM filled to its occupancy, at most one CTA per tile.
-template <bool INC, bool MRT, class M>
-static void launch_pipe(const StepArgs& a, uint64_t tiles, cudaStream_t st, const M& m) {
-  static int per_sm[2][2] = {{0, 0}, {0, 0}};
-  static int sms = 0;
-  int& occ = per_sm[INC][MRT];
-  if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, t2c_step_pipe_kernel<INC, MRT>, 64, 0);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (occ < 1) occ = 1;
-  }
-  const uint64_t cap = static_cast<uint64_t>(occ) * sms;
-  const unsigned blocks = static_cast<unsigned>(tiles < cap ? tiles : cap);
-  if (blocks) launch_maybe_pdl(t2c_step_pipe_kernel<INC, MRT>, blocks, st, a, m, 64);
-}
-
 template <int D, int LOGA, bool INC, int PHASE, class R>
 static void launch_aa(const StepArgs& a, unsigned blocks, cudaStream_t st) {
   if constexpr (PHASE == 1 && std::is_same<R, double>::value) {
@@ -1222,12 +1074,6 @@ static void launch_pow2(const StepArgs& a, cudaStream_t st) {
     return;
   }
   if (a.mrt_K) {
-    if constexpr (D == 3 && LOGA == 2 && std::is_same<R, double>::value) {
-      if (a.pipe) {
-        launch_pipe<INC, true>(a, tiles, st, mrt_param<R, Lat<D>::Q>(a.mrt_K));
-        return;
-      }
-    }
     t2c_step_pow2_kernel<D, LOGA, INC, false, true, R>
         <<<blocks, step_threads<D, NTN>(), 0, st>>>(a, mrt_param<R, Lat<D>::Q>(a.mrt_K));
     return;
@@ -1247,12 +1093,6 @@ static void launch_pow2(const StepArgs& a, cudaStream_t st) {
         launch_maybe_pdl(t2c_step_x2_kernel<D, LOGA, INC, R, true>, xb, st, a, none, SPLBM_X2_THREADS);
       else
         launch_maybe_pdl(t2c_step_x2_kernel<D, LOGA, INC, R, false>, xb, st, a, none, SPLBM_X2_THREADS);
-      return;
-    }
-  }
-  if constexpr (D == 3 && LOGA == 2 && std::is_same<R, double>::value) {
-    if (a.pipe) {  // software-pipelined persistent variant (SPLBM_PIPE)
-      launch_pipe<INC, false>(a, tiles, st, none);
       return;
     }
   }

@@ -50,7 +50,6 @@ struct StepArgs {
   // Traversal order (power-of-two 3D kernels, whole-domain engines): the k-th stepped tile is
   // order[k] (tiling_gpu.h build_column_order); nullptr = the compact order t0 + k.
   const uint32_t* order;
-  int pipe;  // 3D a = 4 f64 two-copy: the software-pipelined persistent kernel (t2c_step_pipe_kernel)
 };
 
 // The MRT operator as a kernel parameter (constant bank): the unrolled K_ij * delta_j products

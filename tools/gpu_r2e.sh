@@ -1,4 +1,5 @@
 #!/bin/bash
+# (historical: SPLBM_PIPE selected the software-pipelined step kernel, removed after this A/B)
 # Round 2 (re-entry), first GPU session: smoke, default bench (N=1 line incl. configs4), reference
 # arm, pipelined-step / FMA A/B, launch list + ncu --set full captures of the headline, the sparse
 # RAS 256^3 phi 0.2 and the 1024^3 step.
