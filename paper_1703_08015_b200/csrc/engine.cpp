@@ -123,7 +123,7 @@ struct splbm_dev_engine {
   uint64_t device_bytes = 0;
   uint32_t l2pf = 0;  // step kernel L2 prefetch distance in CTAs (StepArgs::l2pf)
   uint64_t pdl_min_threads = 4ull * 148 * 256;  // StepArgs::pdl_min_threads (SPLBM_PDL_MIN)
-  int x2 = 1;         // StepArgs::x2: f32 two nodes per thread (SPLBM_X2=0 disables)
+  int x2 = 1;         // StepArgs::x2: two nodes per thread, f32 and D2Q9 f64 (SPLBM_X2=0 disables)
   int off32 = 1;      // StepArgs::off32 when the slots fit 32 bits (SPLBM_OFF32=0 disables)
   // resident multi-step batches (small whole-domain two-copy BGK engines, SPLBM_RESIDENT=0 off):
   // res_blocks CTAs of res_threads threads, res_tpc tiles each; 0 = one launch per step

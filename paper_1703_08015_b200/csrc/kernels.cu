@@ -374,11 +374,12 @@ __global__ void __launch_bounds__((step_threads<D, (D == 3 ? (1 << (3 * LOGA)) :
   }
 }
 
-// Two nodes per thread (the f32 engine): a float gather moves half the bytes of a double one, so
-// one node per thread leaves too few bytes in flight; here thread j of a tile's half takes nodes j
-// and j + NTN/2 and issues both gathers (2 x q loads) before either collision: +7-13 % over one
-// node per thread (interleaved A/B). Same addressing, slots and arithmetic as
-// t2c_step_pow2_kernel (BGK, no slab peer stores).
+// Two nodes per thread (the f32 engine, and D2Q9 in f64): a float gather moves half the bytes of a
+// double one (a D2Q9 node has 9 instead of 19 values), so one node per thread leaves too few bytes
+// in flight; here thread j of a tile's half takes nodes j and j + NTN/2 and issues both gathers
+// (2 x q loads) before either collision: +7-13 % over one node per thread for f32, +5 % for D2Q9
+// f64 (interleaved A/B). Same addressing, slots and arithmetic as t2c_step_pow2_kernel (BGK, no
+// slab peer stores).
 template <int D, int LOGA, bool INC, class R, bool O32>
 __global__ void __launch_bounds__(SPLBM_X2_THREADS, SPLBM_X2_MINB)
     t2c_step_x2_kernel(StepArgs args, const __grid_constant__ MrtMatrix<R, 1> mrt) {
@@ -1084,9 +1085,10 @@ static void launch_pow2(const StepArgs& a, cudaStream_t st) {
       return;
     }
   }
-  // f32 only: for f64 two nodes per thread need 128 registers and measured 5-11 % slower
-  if constexpr (sizeof(R) == 4 && NTN >= 16 && (SPLBM_X2_THREADS % (NTN / 2)) == 0) {
-    if (a.x2 && a.skip_by == 0) {  // f32: two nodes per thread
+  // f32, and D2Q9 in f64 (18 values per thread fit 64 registers: vessel tree / dense 4096^2 -5 %,
+  // profiles/ab_x2_2d_r2.txt); D3Q19 f64 would need 128 registers and measured 5-11 % slower
+  if constexpr ((sizeof(R) == 4 || D == 2) && NTN >= 16 && (SPLBM_X2_THREADS % (NTN / 2)) == 0) {
+    if (a.x2 && a.skip_by == 0) {  // two nodes per thread
       constexpr int XT = SPLBM_X2_THREADS / (NTN / 2);
       const unsigned xb = static_cast<unsigned>((tiles + XT - 1) / XT);
       if (a.off32)
