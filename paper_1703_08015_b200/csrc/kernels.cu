@@ -65,7 +65,7 @@ __host__ __device__ constexpr int nb_offset() { return D == 3 ? 0 : 9; }
 #define SPLBM_X2_MINB 16     // ... and resident CTAs per SM (64 registers)
 #endif
 #ifndef SPLBM_MINB_MRT
-#define SPLBM_MINB_MRT 3  // the 3D MRT step (361 extra products per node): 80 registers, +4-9 % vs 2
+#define SPLBM_MINB_MRT 3  // the 3D MRT step when SPLBM_CTAS_MRT3 = 0: 80 registers (+4-9 % vs 2, round 1)
 #endif
 #ifndef SPLBM_MINB_MRT2
 #define SPLBM_MINB_MRT2 4  // the 2D MRT step: +12 % vs 2 (interleaved A/B)
@@ -75,6 +75,10 @@ __host__ __device__ constexpr int nb_offset() { return D == 3 ? 0 : 9; }
 #endif
 #ifndef SPLBM_CTAS3
 #define SPLBM_CTAS3 0  // experiment: resident 64-thread CTAs/SM budgeted for the 3D f64 BGK step (0 = SPLBM_MINB3)
+#endif
+#ifndef SPLBM_CTAS_MRT3
+#define SPLBM_CTAS_MRT3 10  // 3D MRT step: 10 resident 64-thread CTAs/SM = 94 registers, no spills
+                            // (12 CTAs: 80 registers + 144 B of spills, 2-3 % slower, round 2 A/B)
 #endif
 #ifndef SPLBM_ZERO_FILL
 #define SPLBM_ZERO_FILL 1  // write 0.0 to solid slots sharing a 32-B sector with fluid slots
@@ -276,7 +280,7 @@ __global__ void __launch_bounds__(kThreads)
 // plus one shared-memory lookup and two selects — no divergent branches, no dependent global load
 // before the PDF gather.
 template <int D, int LOGA, bool INC, bool PEER, bool MRT, class R>
-__global__ void __launch_bounds__((step_threads<D, (D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA)))>()), (SPLBM_CTAS3 && D == 3 && !MRT && sizeof(R) == 8) ? SPLBM_CTAS3 : (MRT ? (D == 3 ? SPLBM_MINB_MRT : SPLBM_MINB_MRT2) : (D == 3 ? (sizeof(R) == 4 ? SPLBM_MINB3F : SPLBM_MINB3) : (sizeof(R) == 4 ? SPLBM_MINB2F : SPLBM_MINB2))) * 256 / step_threads<D, (D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA)))>())
+__global__ void __launch_bounds__((step_threads<D, (D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA)))>()), (SPLBM_CTAS3 && D == 3 && !MRT && sizeof(R) == 8) ? SPLBM_CTAS3 : (SPLBM_CTAS_MRT3 && D == 3 && MRT) ? SPLBM_CTAS_MRT3 : (MRT ? (D == 3 ? SPLBM_MINB_MRT : SPLBM_MINB_MRT2) : (D == 3 ? (sizeof(R) == 4 ? SPLBM_MINB3F : SPLBM_MINB3) : (sizeof(R) == 4 ? SPLBM_MINB2F : SPLBM_MINB2))) * 256 / step_threads<D, (D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA)))>())
     t2c_step_pow2_kernel(StepArgs args, const __grid_constant__ MrtMatrix<R, MRT ? Lat<D>::Q : 1> mrt) {
   constexpr int Q = Lat<D>::Q;
   const R* const rd = static_cast<const R*>(args.read);
