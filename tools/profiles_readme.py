@@ -38,9 +38,9 @@ def main():
     d = json.load(open(os.path.join(PR, "ncu_step_kernel.json")))
     b = json.load(open(os.path.join(PR, "bench_r2.json")))
     L = ["# Profiles (B200, sm_100a), round 2 (round-1 rows marked)", "",
-         "* `ncu_step_kernel.json`: one `ncu --set full --clock-control none --import-source on -k regex:t2c_step -s 4 -c 1 python tools/profile_case.py <case> 6` capture per workload (`tools/gpu_r2f.sh`; configs[4] with `--replay-mode application --cache-control none`; the single-copy pair and the configs[0] resident / streamed rows from `tools/gpu_r2n.sh`), summarised by `tools/ncu_summary.py`; the f32 / MRT / cavity 4096² rows are round 1. The `cavity2d_256_a4_resident` launch is a whole 200-step resident batch (2.87 µs per step); its PDFs stay in L2, so DRAM/algorithmic is ~0.",
+         "* `ncu_step_kernel.json`: one `ncu --set full --clock-control none --import-source on -k regex:t2c_step -s 4 -c 1 python tools/profile_case.py <case> 6` capture per workload (`tools/gpu_r2f.sh`; configs[4] with `--replay-mode application --cache-control none`; the single-copy pair and the configs[0] resident / streamed rows from `tools/gpu_r2n2.sh`), summarised by `tools/ncu_summary.py`; every row is round 2 (`tools/gpu_r2n2.sh`, `tools/gpu_r2n.sh`, `tools/gpu_r2f.sh` for configs[4]). The `cavity2d_256_a4_resident` launch is a whole 200-step resident batch (2.87 µs per step); its PDFs stay in L2, so DRAM/algorithmic is ~0.",
          "* `launches_r2.csv`: `ncu --metrics gpu__time_duration.sum --clock-control none -c 400 python bench.py --steps 4 --warmup 3 --no-sweep --no-cpu --no-other --no-configs4` (cold-cache, serialised per-launch times: compare shares, not absolutes).",
-         "* `bench_r2.json` / `bench_ref_r2.json`: the `python bench.py` and `python bench.py --impl reference` lines of the same code (same box, `tools/gpu_r2n.sh`).", "",
+         "* `bench_r2.json` / `bench_ref_r2.json`: the `python bench.py` and `python bench.py --impl reference` lines of the same code (same box, `tools/gpu_r2n2.sh`).", "",
          "## Step kernel per launch (ncu)", "",
          "| workload | round | kernel | us | DRAM read MB | DRAM write MB | DRAM / algorithmic | DRAM % of peak | issue active % | warps active % | regs | top stalls |",
          "|---|---|---|---|---|---|---|---|---|---|---|---|"]
