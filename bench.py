@@ -244,7 +244,7 @@ def other_configs(P, K, W, peak):
     return rows
 
 
-def e2e_public_api(P, g, steps, bench_steps=None, samples=3):
+def e2e_public_api(P, g, steps, bench_steps=None, samples=5):
     """End to end through the public API with host buffers: NodeInit fields H2D from pinned host
     memory, `steps` LBM steps (first-failure check), the final (rho, u) FieldData D2H; wall clock,
     median of `samples` runs. `steps` is the workload's run length (BASELINE configs[1]: 1000
