@@ -47,7 +47,7 @@ class DevInfo(C.Structure):
                 ("padded_dims", C.c_int * 3), ("fluid_nodes", C.c_uint64),
                 ("device_bytes", C.c_uint64), ("phi_t", C.c_double), ("ratio_tiles", C.c_double),
                 ("n_tiles_global", C.c_uint64), ("resident_ctas", C.c_int),
-                ("resident_threads", C.c_int)]
+                ("resident_threads", C.c_int), ("mrt_specialised", C.c_int)]
 
 
 class SlabLayout(C.Structure):
@@ -117,6 +117,8 @@ SIGNATURES = {
     "splbm_selftest_divide": ([C.c_uint64, _dp, _dp, _dp], C.c_int),
     "splbm_selftest_divide_f32": ([C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "splbm_mrt_kernel": ([C.c_int, C.c_double, C.c_void_p, _dp], C.c_int),
+    "splbm_mrt_specialise": ([C.c_int, C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_int,
+                              C.POINTER(C.c_int)], C.c_int),
 }
 
 

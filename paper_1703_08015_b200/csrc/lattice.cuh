@@ -12,7 +12,9 @@
 // x != 0 and a zero sum starts from +0, so the omitted terms never change a finite result (the
 // only difference is on states that already fail the step's finite check).
 #pragma once
+#ifndef __CUDACC_RTC__
 #include <cstdint>
+#endif
 
 namespace splbm_dev {
 

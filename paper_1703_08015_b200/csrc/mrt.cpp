@@ -1,6 +1,7 @@
 #include "mrt.h"
 
 #include "common.h"
+#include "mrt_jit.h"
 
 namespace splbm_host {
 
@@ -90,5 +91,28 @@ extern "C" int splbm_mrt_kernel(int d, double tau, const double* rates, double* 
     if (!(tau > 0.5)) throw config_error("relaxation time tau must be > 0.5");
     const auto K = mrt_kernel(d, tau, rates);
     std::copy(K.begin(), K.end(), K_out);
+  });
+}
+
+extern "C" int splbm_mrt_specialise(int d, int incompressible, int single_precision, double tau,
+                                    const double* rates, int tile, int* products_out) {
+  using namespace splbm_host;
+  return guarded([&] {
+    if (d != 2 && d != 3) throw config_error("MRT is supported for D2Q9 and D3Q19 only");
+    if (!(tau > 0.5)) throw config_error("relaxation time tau must be > 0.5");
+    const auto K = mrt_kernel(d, tau, rates);
+    int products = 0;
+    mrt_collision_source(d, incompressible != 0, single_precision != 0, K, &products);
+    if (products_out) *products_out = products;
+    if (tile > 0) {
+      int loga = 0;
+      while ((1 << loga) < tile) ++loga;
+      if ((1 << loga) != tile || loga < 1 || loga > (d == 3 ? 2 : 4))
+        throw config_error("specialised MRT step needs a power-of-two tile edge (3D: 2, 4; 2D: 2..16)");
+      std::vector<char> cubin;
+      std::string lowered, why;
+      if (!mrt_jit_cubin(d, loga, incompressible != 0, single_precision != 0, K, &cubin, &lowered, &why))
+        throw Error(SPLBM_ERR_CUDA, why);
+    }
   });
 }
