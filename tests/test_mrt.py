@@ -108,14 +108,15 @@ def test_specialised_step_compiles(d, tile, f32):
 @pytest.mark.gpu
 @pytest.mark.parametrize("tau,rates", [(0.8, None), (0.6, None), (1.3, None), (0.9, "custom")])
 @pytest.mark.parametrize("precision", ["f64", "f32"])
-@pytest.mark.parametrize("kind", ["ras3d", "cavity2d"])
+@pytest.mark.parametrize("kind", ["ras3d", "cavity2d", "ras3d_a2", "cavity2d_a16"])
 def test_specialised_equals_generic(kind, precision, tau, rates, monkeypatch):
     """Every PDF slot of the specialised MRT step equals the generic one bit for bit."""
-    if kind == "ras3d":
+    if kind.startswith("ras3d"):
         g, a, per = P.generate(P.GeometryKind.Ras3D, P.GenerateParams(
-            dims=(32, 32, 32), sphere_diameter=10, target_porosity=0.6, seed=4)), 4, 7
+            dims=(32, 32, 32), sphere_diameter=10, target_porosity=0.6, seed=4)), 2 if kind.endswith("a2") else 4, 7
     else:
-        g, a, per = P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(96, 64, 1))), 8, 0
+        g, a, per = P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(96, 64, 1))), \
+            16 if kind.endswith("a16") else 8, 0
     q = 19 if g.d == 3 else 9
     r = list(np.linspace(0.3, 1.6, q)) if rates else []
     for inc in (P.Compressibility.QuasiCompressible, P.Compressibility.Incompressible):
