@@ -442,6 +442,10 @@ def run_ours(args):
     if not args.no_configs4:  # the north-star 1024^3 point (BASELINE configs[4], N=1)
         line["configs4"] = configs4_point(P, args.c4_size, args.c4_phi, K, W, args.c4_single_copy,
                                           (peak, peak_kind))
+        # ... and the rest of its porosity range on the same GPU: phi 0.5 / 0.8 only fit 180 GB
+        # with the single-copy (AA) propagation (106 / 147 GB)
+        line["configs4_porosity"] = [configs4_point(P, args.c4_size, phi, min(K, 100), W, True,
+                                                    (peak, peak_kind)) for phi in (0.5, 0.8)]
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(dims)
     print(json.dumps(line))

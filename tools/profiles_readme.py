@@ -89,6 +89,11 @@ def main():
         L.append(f"| `bench_r2.json` configs4 (200 steps) | {c4['phi']} | two copies | {c4['device_gb']} | {c4['value']} | "
                  f"{c4['roofline']['frac']} | {c4['clocks']['sm_mhz']} | {', '.join(c4['clocks']['reasons']) or '-'} | "
                  f"{c4['host_seconds']['generate']} | {c4['host_seconds']['engine_build']} |")
+    for c in b.get("configs4_porosity", []):
+        L.append(f"| `bench_r2.json` configs4_porosity ({c['steps']} steps) | {c['phi']} | single copy (AA) | "
+                 f"{c['device_gb']} | {c['value']} | {c['roofline']['frac']} | {c['clocks']['sm_mhz']} | "
+                 f"{', '.join(c['clocks']['reasons']) or '-'} | {c['host_seconds']['generate']} | "
+                 f"{c['host_seconds']['engine_build']} |")
     ref = os.path.join(PR, "bench_ref_r2.json")
     if os.path.exists(ref):
         r = json.load(open(ref))
