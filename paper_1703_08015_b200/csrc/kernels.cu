@@ -840,14 +840,23 @@ static void launch_pow2(const StepArgs& a, cudaStream_t st) {
       cfg.gridDim = dim3(blocks);
       cfg.blockDim = dim3(step_threads<D, NTN>());
       cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+#if SPLBM_PDL
+      if (static_cast<uint64_t>(blocks) * step_threads<D, NTN>() >= a.pdl_min_threads) {
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+      }
+#endif
       StepArgs args = a;
       MrtMatrix<R, 1> k{};
       void* params[] = {&args, &k};
       cudaLaunchKernelExC(&cfg, a.jit, params);
       return;
     }
-    t2c_step_pow2_kernel<D, LOGA, INC, false, true, R>
-        <<<blocks, step_threads<D, NTN>(), 0, st>>>(a, mrt_param<R, Lat<D>::Q>(a.mrt_K));
+    launch_maybe_pdl(t2c_step_pow2_kernel<D, LOGA, INC, false, true, R>, blocks, st, a,
+                     mrt_param<R, Lat<D>::Q>(a.mrt_K), step_threads<D, NTN>());
     return;
   }
   if constexpr (std::is_same<R, double>::value) {
