@@ -14,6 +14,7 @@ CASES = {
     "cavity2d_4096_a4": lambda: (P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(4096, 4096, 1))), 4, 0),
     "ras48_periodic": lambda: (P.generate(P.GeometryKind.Ras3D, P.GenerateParams(dims=(48, 48, 48), sphere_diameter=12, target_porosity=0.5, seed=2)), 4, 7),
     "channel3d_small": lambda: (P.generate(P.GeometryKind.Channel3D, P.GenerateParams(dims=(30, 18, 21))), 4, 0),
+    "cavity2d_512_a4": lambda: (P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(512, 512, 1))), 4, 0),
     "cavity2d_256_a4": lambda: (P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(256, 256, 1))), 4, 0),
     "cavity2d_64_a16": lambda: (P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(64, 64, 1))), 16, 0),
     "random_a3": lambda: (__import__("cases").random_solids((23, 14, 11), seed=5, frac=0.25), 3, 0),

@@ -24,3 +24,6 @@ run cavity2d_256_resident "SPLBM_PRECISION=f64" cavity2d_256_a4
 run cavity2d_256_resident_f32 "SPLBM_PRECISION=f32" cavity2d_256_a4
 run channel3d_small_resident "SPLBM_PRECISION=f64" channel3d_small
 run channel3d_small_streamed "SPLBM_RESIDENT=0" channel3d_small
+# round 2: the MRT step specialised through NVRTC, the D2Q9 f64 two-nodes-per-thread step
+run ras48_mrt_specialised "SPLBM_MODEL=mrt" ras48_periodic
+run cavity2d_512_x2 "SPLBM_PRECISION=f64" cavity2d_512_a4
