@@ -239,7 +239,10 @@ def other_configs(P, K, W, peak):
         rows.append({"config": name, "steps": steps, "fluid_nodes": nf,
                      "phi_t": round(eng.info.phi_t, 4), "us_per_step": round(ms / steps * 1e3, 2),
                      "mlups": round(mlups, 1), "achieved_gbs": round(gbs, 1),
-                     "frac_of_measured_peak": round(gbs / peak, 4)})
+                     "frac_of_measured_peak": round(gbs / peak, 4),
+                     "step_path": ("resident multi-step kernel" if eng.info.resident_ctas else
+                                   "MRT step specialised for the operator (NVRTC)" if eng.info.mrt_specialised
+                                   else "one step launch per step (CUDA-graph batches)")})
         del eng
     return rows
 
