@@ -131,3 +131,31 @@ def test_specialised_equals_generic(kind, precision, tau, rates, monkeypatch):
             assert e.step_n(30)[0]
             out.append(e.get_pdf().view(np.uint8).copy())
         assert np.array_equal(out[0], out[1]), (inc, precision, tau, rates)
+
+
+@pytest.mark.gpu
+def test_mrt_without_nvrtc_runs_the_generic_kernel(tmp_path):
+    """Without libnvrtc (SPLBM_NVRTC pointing nowhere) an MRT engine falls back to the generic
+    ahead-of-time MRT kernel and produces the same bits."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, paper_1703_08015_b200 as P\n"
+        "g = P.generate(P.GeometryKind.Cavity2D, P.GenerateParams(dims=(64, 64, 1)))\n"
+        "e = P.TileEngineT2C(g, 4, P.FluidModel(collision=P.CollisionKind.MRT, tau=0.7))\n"
+        "e.initialize_uniform(); assert e.step_n(20)[0]\n"
+        "np.save(%r, e.get_pdf()); print(e.info.mrt_specialised)\n")
+    outs = []
+    for k, nvrtc in enumerate(("/nonexistent/libnvrtc.so", None)):
+        env = dict(os.environ)
+        env.pop("SPLBM_NVRTC", None)
+        if nvrtc:
+            env["SPLBM_NVRTC"] = nvrtc
+        f = str(tmp_path / f"pdf{k}.npy")
+        r = subprocess.run([sys.executable, "-c", code % f], env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stderr
+        outs.append((r.stdout.strip().splitlines()[-1], np.load(f)))
+    assert outs[0][0] == "0" and outs[1][0] == "1"
+    assert np.array_equal(outs[0][1].view(np.uint64), outs[1][1].view(np.uint64))
