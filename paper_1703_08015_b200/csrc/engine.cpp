@@ -121,8 +121,10 @@ struct splbm_dev_engine {
   uint8_t* frame = nullptr;             // rho, ux, uy, uz (double) + mask (byte) for one chunk
   uint64_t frame_nodes = 0;             // raster nodes per chunk
   std::vector<double> mrt_K;  // MRT operator (host copy; passed to the kernels by value), empty = BGK
-  const void* mrt_jit = nullptr;  // the step kernel specialised for mrt_K (StepArgs::jit)
-  std::string mrt_jit_why;        // why it is not used (diagnostics)
+  // the kernels specialised for mrt_K (StepArgs::jit): two-copy step, single-copy phases 1 / 2
+  splbm_host::MrtJitKernels mrt_jit;
+  bool mrt_jit_ok = false;
+  std::string mrt_jit_why;  // why they are not used (diagnostics)
   uint64_t device_bytes = 0;
   uint32_t l2pf = 0;  // step kernel L2 prefetch distance in CTAs (StepArgs::l2pf)
   uint64_t pdl_min_threads = 4ull * 148 * 256;  // StepArgs::pdl_min_threads (SPLBM_PDL_MIN)
@@ -253,7 +255,7 @@ struct splbm_dev_engine {
     s.x2 = x2;
     s.off32 = off32 && n_stored * tile_stride() < (1ull << 32);
     s.order = order;
-    s.jit = mrt_jit;
+    s.jit = !mrt_jit_ok ? nullptr : (aa ? mrt_jit.aa[rd] : mrt_jit.step);
     if (peer_part1 && aa) {  // single copy: phase 1 reads/writes the halo nodes' slots in place
       if (rd == 0) {
         s.peer_down = peer_pdf_down[0] ? peer_pdf_down[0] + peer_down_own0 * tile_stride() : nullptr;
@@ -702,14 +704,15 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
   e->scratch = e->alloc<double>(e->scratch_count);
   if (desc->collision == 1) {  // MRT
     e->mrt_K = mrt_kernel(d, desc->tau, desc->mrt_rates);
-    // two-copy power-of-two steps use the kernel specialised for this operator (mrt_jit.cpp);
-    // SPLBM_MRT_JIT=0 keeps the generic instantiation
+    // power-of-two steps (two copies and both single-copy phases) use the kernels specialised for
+    // this operator (mrt_jit.cpp); SPLBM_MRT_JIT=0 keeps the generic instantiations
     const char* jit_env = std::getenv("SPLBM_MRT_JIT");
     const bool pow2 = d == 3 ? (e->a == 2 || e->a == 4) : (e->a == 2 || e->a == 4 || e->a == 8 || e->a == 16);
-    if (!e->aa && pow2 && !(jit_env && std::atoi(jit_env) == 0)) {
+    if (pow2 && !(jit_env && std::atoi(jit_env) == 0)) {
       int loga = 0;
       while ((1 << loga) < e->a) ++loga;
-      e->mrt_jit = splbm_host::mrt_jit_kernel(d, loga, e->incompressible != 0, e->f32, e->mrt_K, &e->mrt_jit_why);
+      e->mrt_jit_ok = splbm_host::mrt_jit_kernels(d, loga, e->incompressible != 0, e->f32, e->mrt_K,
+                                                  &e->mrt_jit, &e->mrt_jit_why);
     }
   } else if (desc->collision != 0) {
     throw config_error("unknown collision kind");
@@ -881,7 +884,7 @@ int splbm_dev_get_info(const splbm_dev_engine* e, splbm_dev_info* out) {
     out->n_tiles_global = e->tm.n_tiles;
     out->resident_ctas = static_cast<int>(e->res_blocks);
     out->resident_threads = static_cast<int>(e->res_threads);
-    out->mrt_specialised = e->mrt_jit ? 1 : 0;
+    out->mrt_specialised = e->mrt_jit_ok ? 1 : 0;
   });
 }
 

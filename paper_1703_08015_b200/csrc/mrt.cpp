@@ -110,7 +110,8 @@ extern "C" int splbm_mrt_specialise(int d, int incompressible, int single_precis
       if ((1 << loga) != tile || loga < 1 || loga > (d == 3 ? 2 : 4))
         throw config_error("specialised MRT step needs a power-of-two tile edge (3D: 2, 4; 2D: 2..16)");
       std::vector<char> cubin;
-      std::string lowered, why;
+      std::vector<std::string> lowered;
+      std::string why;
       if (!mrt_jit_cubin(d, loga, incompressible != 0, single_precision != 0, K, &cubin, &lowered, &why))
         throw Error(SPLBM_ERR_CUDA, why);
     }

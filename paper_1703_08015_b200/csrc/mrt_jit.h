@@ -15,14 +15,21 @@ namespace splbm_host {
 std::string mrt_collision_source(int d, bool incompressible, bool f32, const std::vector<double>& K,
                                  int* products_out);
 
-// NVRTC compilation only (no device needed): the cubin and the kernel's lowered name.
-bool mrt_jit_cubin(int d, int loga, bool incompressible, bool f32, const std::vector<double>& K,
-                   std::vector<char>* cubin, std::string* lowered_name, std::string* why);
+// The kernels compiled for one operator: the two-copy step and the two single-copy (AA) phases.
+struct MrtJitKernels {
+  const void* step = nullptr;                // t2c_step_pow2_kernel<..., GEN = true>
+  const void* aa[2] = {nullptr, nullptr};    // t2c_aa_kernel<..., PHASE 1 / 2, ..., GEN = true>
+};
 
-// The specialised step kernel (a cudaKernel_t, usable as the `func` of cudaLaunchKernelExC) for a
-// power-of-two tile edge 2^loga, or nullptr with *why set (NVRTC missing, compile error, ...).
-// Compiled once per distinct source in the process.
-const void* mrt_jit_kernel(int d, int loga, bool incompressible, bool f32, const std::vector<double>& K,
-                           std::string* why);
+// NVRTC compilation only (no device needed): one cubin with the three kernels and their lowered
+// names (step, AA phase 1, AA phase 2).
+bool mrt_jit_cubin(int d, int loga, bool incompressible, bool f32, const std::vector<double>& K,
+                   std::vector<char>* cubin, std::vector<std::string>* lowered_names, std::string* why);
+
+// The specialised kernels (cudaKernel_t handles, usable as the `func` of cudaLaunchKernelExC) for
+// a power-of-two tile edge 2^loga; false with *why set when NVRTC is missing or fails. Compiled
+// once per distinct operator in the process.
+bool mrt_jit_kernels(int d, int loga, bool incompressible, bool f32, const std::vector<double>& K,
+                     MrtJitKernels* out, std::string* why);
 
 }  // namespace splbm_host

@@ -109,8 +109,10 @@ def test_specialised_step_compiles(d, tile, f32):
 @pytest.mark.parametrize("tau,rates", [(0.8, None), (0.6, None), (1.3, None), (0.9, "custom")])
 @pytest.mark.parametrize("precision", ["f64", "f32"])
 @pytest.mark.parametrize("kind", ["ras3d", "cavity2d", "ras3d_a2", "cavity2d_a16"])
-def test_specialised_equals_generic(kind, precision, tau, rates, monkeypatch):
-    """Every PDF slot of the specialised MRT step equals the generic one bit for bit."""
+@pytest.mark.parametrize("single_copy", [False, True])
+def test_specialised_equals_generic(kind, precision, tau, rates, single_copy, monkeypatch):
+    """Every PDF slot of the specialised MRT step (two copies, or both single-copy phases) equals
+    the generic one bit for bit."""
     if kind.startswith("ras3d"):
         g, a, per = P.generate(P.GeometryKind.Ras3D, P.GenerateParams(
             dims=(32, 32, 32), sphere_diameter=10, target_porosity=0.6, seed=4)), 2 if kind.endswith("a2") else 4, 7
@@ -124,7 +126,7 @@ def test_specialised_equals_generic(kind, precision, tau, rates, monkeypatch):
         for jit in ("1", "0"):
             monkeypatch.setenv("SPLBM_MRT_JIT", jit)
             e = P.TileEngineT2C(g, a, P.FluidModel(inc, P.CollisionKind.MRT, tau=tau, mrt_rates=r), per,
-                                precision=precision)
+                                precision=precision, single_copy=single_copy)
             assert e.info.mrt_specialised == (jit == "1")
             e.initialize(lambda x, y, z: (1.0 + 0.01 * np.sin(0.3 * x + 0.1 * z), 0.01 * np.cos(0.2 * y),
                                           0.005 * np.sin(0.1 * x), 0.002 * np.cos(0.3 * z)))
