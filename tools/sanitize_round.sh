@@ -26,4 +26,5 @@ run channel3d_small_resident "SPLBM_PRECISION=f64" channel3d_small
 run channel3d_small_streamed "SPLBM_RESIDENT=0" channel3d_small
 # round 2: the MRT step specialised through NVRTC, the D2Q9 f64 two-nodes-per-thread step
 run ras48_mrt_specialised "SPLBM_MODEL=mrt" ras48_periodic
+run ras48_single_copy_mrt_specialised "SPLBM_MODEL=mrt SPLBM_SINGLE_COPY=1" ras48_periodic
 run cavity2d_512_x2 "SPLBM_PRECISION=f64" cavity2d_512_a4
