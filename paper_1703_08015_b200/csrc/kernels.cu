@@ -8,11 +8,14 @@
 //   bits 24..25  NodeType; bit 26 bc_degenerate (engine.hpp:409-417)
 //   bit 27       solid node whose 32-B sector holds a non-solid node: written (as 0.0) so
 //                every store sector is whole (no L2 partial-write fills); never read.
-// One thread per tile node (two in the f32 step), 64-thread CTAs for the power-of-two tile
-// kernels (one 4^3 tile per CTA; 256 for the generic and auxiliary kernels), consecutive threads
-// = consecutive p so all q stores of a warp are 256-B coalesced runs; the gather reads the own
-// tile and the face-adjacent neighbour tiles (L2 hits: neighbours are near in the compact
-// z-major order, and the tile blocks two CTAs per SM ahead are bulk-prefetched into L2).
+// One thread per tile node (two in the f32 and D2Q9 f64 steps), 64-thread CTAs for the
+// power-of-two tile kernels (one 4^3 tile per CTA; 256 for the generic and auxiliary kernels),
+// consecutive threads = consecutive p so all q stores of a warp are 256-B coalesced runs; the
+// gather reads the own tile and the face-adjacent neighbour tiles (L2 hits: neighbours are near in
+// the compact z-major order, and the tile blocks two CTAs per SM ahead are bulk-prefetched into
+// L2). The power-of-two two-copy step and the single-copy phases live in step_pow2.cuh /
+// step_aa.cuh, which mrt_jit.cpp also compiles at run time (NVRTC) for each MRT operator; small
+// whole domains run batches of steps in the resident multi-step kernel below.
 #include <cuda_runtime.h>
 
 #include <cstdint>
