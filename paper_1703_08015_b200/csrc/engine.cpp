@@ -772,12 +772,19 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device));
     const char* env = std::getenv("SPLBM_RESIDENT");
     const bool want = env ? std::atoi(env) != 0 : true;
-    if (want && coop && sms > 0 && sms <= splbm_dev::kResidentMaxCtas && !slab_mode && !e->aa && e->mrt_K.empty() && e->n_own > 0 &&
-        nslots < (1ull << 32)) {
-      const uint64_t tpc = (e->n_own + sms - 1) / sms;
-      const uint64_t threads = (tpc * n_tn + 31) / 32 * 32;
-      if (splbm_dev::resident_fits(d, e->incompressible != 0, e->f32, static_cast<unsigned>(threads)) ==
-              cudaSuccess) {
+    // two resident CTAs per SM (half the nodes each) measured 5 % faster than one on configs[0]
+    // (a = 4 and 16; three: no further gain); one when two do not fit. SPLBM_RESIDENT_PER_SM overrides.
+    const char* per_env = std::getenv("SPLBM_RESIDENT_PER_SM");
+    const int first = per_env ? std::max(1, std::atoi(per_env)) : 2;
+    if (want && coop && sms > 0 && !slab_mode && !e->aa && e->mrt_K.empty() && e->n_own > 0 && nslots < (1ull << 32)) {
+      for (int per_sm = first; per_sm >= 1 && !e->res_blocks; --per_sm) {
+        const int ctas = sms * per_sm;
+        if (ctas > splbm_dev::kResidentMaxCtas) continue;
+        const uint64_t tpc = (e->n_own + ctas - 1) / ctas;
+        const uint64_t threads = (tpc * n_tn + 31) / 32 * 32;
+        if (splbm_dev::resident_fits(d, e->incompressible != 0, e->f32, static_cast<unsigned>(threads),
+                                     static_cast<unsigned>(per_sm)) != cudaSuccess)
+          continue;
         e->res_tpc = static_cast<int>(tpc);
         e->res_threads = static_cast<unsigned>(threads);
         e->res_blocks = static_cast<unsigned>((e->n_own + tpc - 1) / tpc);

@@ -865,12 +865,12 @@ struct ResidentL {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    if (probe) {  // one CTA of this size resident per SM?
+    if (probe) {  // `blocks` CTAs of this size resident per SM?
       if (threads > static_cast<unsigned>(resident_threads_max<D, R>())) return cudaErrorInvalidValue;
       int occ = 0;
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, static_cast<int>(threads), smem);
       if (e != cudaSuccess) return e;
-      return occ >= 1 ? cudaSuccess : cudaErrorCooperativeLaunchTooLarge;
+      return occ >= static_cast<int>(blocks) ? cudaSuccess : cudaErrorCooperativeLaunchTooLarge;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(blocks);
@@ -891,8 +891,8 @@ cudaError_t launch_resident(int d, bool inc, bool f32, const ResidentArgs& ra, u
   return dispatch<ResidentL>(d, inc, f32, ra, blocks, threads, st, false);
 }
 
-cudaError_t resident_fits(int d, bool inc, bool f32, unsigned threads) {
-  return dispatch<ResidentL>(d, inc, f32, ResidentArgs{}, 1u, threads, cudaStream_t{}, true);
+cudaError_t resident_fits(int d, bool inc, bool f32, unsigned threads, unsigned per_sm) {
+  return dispatch<ResidentL>(d, inc, f32, ResidentArgs{}, per_sm, threads, cudaStream_t{}, true);
 }
 
 cudaError_t launch_bump(long long* step_base, long long by, cudaStream_t st) {

@@ -90,7 +90,7 @@ struct HaloArgs {
 // `blocks` (<= kResidentMaxCtas) CTAs x `threads` (tiles_per_cta whole tiles each) runs `nsteps`
 // steps from copy rd0; between steps each CTA waits for the CTAs owning its neighbour tiles
 // (per-CTA epoch flags). StepArgs::read/write are unused (pdf0/pdf1 alternate).
-constexpr int kResidentMaxCtas = 256;
+constexpr int kResidentMaxCtas = 512;
 struct ResidentArgs {
   StepArgs s;
   void* pdf0;
@@ -103,8 +103,8 @@ struct ResidentArgs {
 };
 cudaError_t launch_resident(int d, bool inc, bool f32, const ResidentArgs& a, unsigned blocks,
                             unsigned threads, cudaStream_t st);
-// cudaSuccess when one CTA of `threads` threads of the resident kernel fits an SM.
-cudaError_t resident_fits(int d, bool inc, bool f32, unsigned threads);
+// cudaSuccess when `per_sm` CTAs of `threads` threads of the resident kernel fit an SM.
+cudaError_t resident_fits(int d, bool inc, bool f32, unsigned threads, unsigned per_sm = 1);
 cudaError_t launch_step(int d, bool inc, bool f32, const StepArgs& a, cudaStream_t st);
 cudaError_t launch_bump(long long* step_base, long long by, cudaStream_t st);
 // Slab p2p: wait (system-scope acquire polling) until the non-null flags reach seq.
