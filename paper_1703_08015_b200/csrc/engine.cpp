@@ -581,9 +581,9 @@ void build(splbm_dev_engine* e, const splbm_dev_desc* desc) {
     int sms = 148;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device));
     e->l2pf = static_cast<uint32_t>(2 * sms);
-    // single copy: four CTAs per SM ahead (RAS 256^3 phi 0.2 / 0.5: -7 % / -3 % per step, dense
-    // unchanged; the AA kernels keep fewer CTAs resident per SM than the two-copy step)
-    if (e->aa) e->l2pf = static_cast<uint32_t>(4 * sms);
+    // single copy: five CTAs per SM ahead (round 2, with 16 phase-1 CTAs per SM: RAS 256^3 phi 0.2
+    // / 0.5 -3 % / -1 % per step against four, dense unchanged; six and more cost dense 1 %)
+    if (e->aa) e->l2pf = static_cast<uint32_t>(5 * sms);
     if (const char* v = std::getenv("SPLBM_L2PF")) e->l2pf = static_cast<uint32_t>(std::atoi(v));
     if (const char* v = std::getenv("SPLBM_PDL_MIN")) e->pdl_min_threads = std::strtoull(v, nullptr, 10);
     if (const char* v = std::getenv("SPLBM_X2")) e->x2 = std::atoi(v);
