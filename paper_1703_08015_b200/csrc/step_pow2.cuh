@@ -14,7 +14,7 @@ constexpr int kThreads = 256;
 #define SPLBM_STEP_THREADS 64  // CTA size of the 3D power-of-two step kernel
 #endif
 #ifndef SPLBM_AA_THREADS
-#define SPLBM_AA_THREADS 64  // CTA size of the single-copy (AA) kernels
+#define SPLBM_AA_THREADS 128  // CTA size of the single-copy (AA) kernels (two 4^3 tiles: RAS phi 0.2 -2.7 % vs 64)
 #endif
 #ifndef SPLBM_STEP_THREADS2
 #define SPLBM_STEP_THREADS2 64  // CTA size of the 2D power-of-two step kernel
