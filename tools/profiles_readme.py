@@ -38,7 +38,7 @@ def main():
     d = json.load(open(os.path.join(PR, "ncu_step_kernel.json")))
     b = json.load(open(os.path.join(PR, "bench_r2.json")))
     L = ["# Profiles (B200, sm_100a), round 2 (round-1 rows marked)", "",
-         "* `ncu_step_kernel.json`: one `ncu --set full --clock-control none --import-source on -k regex:t2c_step -s 4 -c 1 python tools/profile_case.py <case> 6` capture per workload (`tools/gpu_r2f.sh`; configs[4] with `--replay-mode application --cache-control none`; the single-copy pair and the configs[0] resident / streamed rows from `tools/gpu_r2n2.sh`), summarised by `tools/ncu_summary.py`; every row is round 2 (`tools/gpu_r2n2.sh`, `tools/gpu_r2n.sh`, `tools/gpu_r2f.sh` for configs[4]). The `cavity2d_256_a4_resident` launch is a whole 200-step resident batch (2.87 µs per step); its PDFs stay in L2, so DRAM/algorithmic is ~0.",
+         "* `ncu_step_kernel.json`: one `ncu --set full --clock-control none --import-source on -k regex:t2c_step -s 4 -c 1 python tools/profile_case.py <case> 6` capture per workload (`tools/gpu_r2f.sh`; configs[4] with `--replay-mode application --cache-control none`; the single-copy pair and the configs[0] resident / streamed rows from `tools/gpu_r2n2.sh`), summarised by `tools/ncu_summary.py`; every row is round 2 (`tools/gpu_r2n2.sh`, `tools/gpu_r2n.sh`, `tools/gpu_r2f.sh` for configs[4]). The `cavity2d_256_a4_resident` launch is a whole 200-step resident batch (2.7 µs per step, two CTAs per SM); its PDFs stay in L2, so DRAM/algorithmic is ~0.",
          "* `launches_r2.csv`: `ncu --metrics gpu__time_duration.sum --clock-control none -c 400 python bench.py --steps 4 --warmup 3 --no-sweep --no-cpu --no-other --no-configs4` (cold-cache, serialised per-launch times: compare shares, not absolutes).",
          "* `bench_r2.json` / `bench_ref_r2.json`: the `python bench.py` and `python bench.py --impl reference` lines of the final code (same box, `tools/gpu_final.sh`); `bench_n2_one_gpu_r2.json`: `bench.py --gpus 2` under torchrun with both ranks on one GPU (path validation, not scaling data).",
          "* Interleaved A/B measurements (`tools/ab.py`, one process, engines alternated): `ab_resident_r2.txt` (resident multi-step kernel, configs[0]), `ab_aa1_r2.txt` (single-copy phase-1 register diet), `ab_x2_2d_r2.txt` (D2Q9 f64 two nodes per thread), `ab_mrt_ctas_r2.txt` (MRT at 10 CTAs/SM), `ab_mrt_specialised_r2.txt` (NVRTC-specialised MRT step), and the dropped ones: `ab_pf_range_r2.txt` / `pf_range_1024_r2.txt` (z-range L2 prefetch), `ab_reverse_r2.txt` (alternating traversal), `ab_pairx_r2.txt` (x-neighbour node pairs), `ab_pipe_fma_r2.json` (pipelined step, FMA build).",
