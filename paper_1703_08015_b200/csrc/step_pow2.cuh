@@ -11,7 +11,7 @@ namespace splbm_dev {
 constexpr uint32_t kEmpty = 0xffffffffu;
 constexpr int kThreads = 256;
 #ifndef SPLBM_STEP_THREADS
-#define SPLBM_STEP_THREADS 64  // CTA size of the 3D power-of-two step kernel
+#define SPLBM_STEP_THREADS 64  // CTA size of the 3D power-of-two step kernel (128: BGK +0.2-0.7 %, MRT -1 %, round 2)
 #endif
 #ifndef SPLBM_AA_THREADS
 #define SPLBM_AA_THREADS 128  // CTA size of the single-copy (AA) kernels (two 4^3 tiles: RAS phi 0.2 -2.7 % vs 64)
@@ -62,7 +62,7 @@ __host__ __device__ constexpr int nb_offset() { return D == 3 ? 0 : 9; }
 #define SPLBM_CTAS3 0  // experiment: resident 64-thread CTAs/SM budgeted for the 3D f64 BGK step (0 = SPLBM_MINB3)
 #endif
 #ifndef SPLBM_CTAS_MRT3
-#define SPLBM_CTAS_MRT3 10  // 3D MRT step: 10 resident 64-thread CTAs/SM = 94 registers, no spills
+#define SPLBM_CTAS_MRT3 10  // 3D MRT step: 640 resident threads/SM (10 x 64) = 94 registers, no spills
                             // (12 CTAs: 80 registers + 144 B of spills, 2-3 % slower, round 2 A/B)
 #endif
 #ifndef SPLBM_ZERO_FILL
@@ -153,6 +153,18 @@ __device__ __forceinline__ void l2_prefetch_blocks(const R* pdf, uint64_t tile, 
 template <int D, bool INC, class R>
 __device__ bool collide_mrt_gen(R* f);
 
+// Resident CTAs per SM the power-of-two step is budgeted for (the registers follow): SPLBM_CTAS3 /
+// SPLBM_CTAS_MRT3 count 64-thread CTA equivalents, SPLBM_MINB* 256-thread ones.
+template <int D, int NTN, bool MRT, class R>
+__host__ __device__ constexpr int step_min_blocks() {
+  constexpr int T = step_threads<D, NTN>();
+  return (SPLBM_CTAS3 && D == 3 && !MRT && sizeof(R) == 8) ? SPLBM_CTAS3 * 64 / T
+         : (SPLBM_CTAS_MRT3 && D == 3 && MRT)             ? SPLBM_CTAS_MRT3 * 64 / T
+         : (MRT ? (D == 3 ? SPLBM_MINB_MRT : SPLBM_MINB_MRT2)
+                : (D == 3 ? (sizeof(R) == 4 ? SPLBM_MINB3F : SPLBM_MINB3) : (sizeof(R) == 4 ? SPLBM_MINB2F : SPLBM_MINB2))) *
+               256 / T;
+}
+
 // Fast path for power-of-two tiles of at most 256 nodes (a = 4 in 3D, a <= 16 in 2D): a CTA owns
 // kThreads / n_tn whole tiles. The 27 neighbour-tile base pointers of each tile are staged in
 // shared memory once per CTA (one coalesced read of nb, overlapped with the gather-word load), so
@@ -160,7 +172,8 @@ __device__ bool collide_mrt_gen(R* f);
 // plus one shared-memory lookup and two selects — no divergent branches, no dependent global load
 // before the PDF gather.
 template <int D, int LOGA, bool INC, bool PEER, bool MRT, class R, bool GEN = false>
-__global__ void __launch_bounds__((step_threads<D, (D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA)))>()), (SPLBM_CTAS3 && D == 3 && !MRT && sizeof(R) == 8) ? SPLBM_CTAS3 : (SPLBM_CTAS_MRT3 && D == 3 && MRT) ? SPLBM_CTAS_MRT3 : (MRT ? (D == 3 ? SPLBM_MINB_MRT : SPLBM_MINB_MRT2) : (D == 3 ? (sizeof(R) == 4 ? SPLBM_MINB3F : SPLBM_MINB3) : (sizeof(R) == 4 ? SPLBM_MINB2F : SPLBM_MINB2))) * 256 / step_threads<D, (D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA)))>())
+__global__ void __launch_bounds__((step_threads<D, (D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA)))>()),
+                                  (step_min_blocks<D, (D == 3 ? (1 << (3 * LOGA)) : (1 << (2 * LOGA))), MRT, R>()))
     t2c_step_pow2_kernel(StepArgs args, const __grid_constant__ MrtMatrix<R, (MRT && !GEN) ? Lat<D>::Q : 1> mrt) {
   constexpr int Q = Lat<D>::Q;
   const R* const rd = static_cast<const R*>(args.read);
